@@ -1,0 +1,246 @@
+/*
+ * swiftdec_b200.h — C ABI of the B200 decode-step library (libswiftdec_b200.so).
+ *
+ * Drop-in boundary for the TokenSwift decode step (arXiv 2502.18890). The
+ * reference (swiftdec, pure Python/numpy) has no native FFI; the entry points
+ * below are what a ctypes binding inside swiftdec would call in place of the
+ * numpy code cited beside each one (paths relative to
+ * /root/reference/pkg/src/swiftdec/). INTEGRATION.md shows that binding.
+ *
+ * Conventions
+ *  - Every pointer is DEVICE memory unless its name ends in `_host`.
+ *  - Sizes are element counts. `stream` is a cudaStream_t.
+ *  - dtype codes: SD_F32 = 0 (float), SD_BF16 = 1 (__nv_bfloat16), SD_F64 = 2.
+ *  - Functions never allocate, never synchronise the host, keep no global
+ *    mutable state, and return SD_OK or an error code; sd_last_error() gives
+ *    a message for the calling thread. Argument validation that raises typed
+ *    exceptions in the reference stays in the host layer.
+ *  - KV layout, one layer: [kv_head][row][head_dim], `head_stride` elements
+ *    between heads (= capacity * head_dim). Layers are `layer_stride` apart.
+ */
+#ifndef SWIFTDEC_B200_H
+#define SWIFTDEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* exported even when the library is compiled with -fvisibility=hidden */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define SD_OK 0
+#define SD_EINVAL 1
+#define SD_ECUDA 2
+#define SD_EUNSUPPORTED 3
+
+#define SD_F32 0
+#define SD_BF16 1
+#define SD_F64 2
+
+/* fixed capacities of the device tree / step-result records */
+#define SD_TREE_MAX_ROWS 256   /* 1 + nodes */
+#define SD_TREE_MAX_PATHS 512
+#define SD_TREE_MAX_DEPTH 8
+#define SD_MASK_WORDS 8        /* SD_TREE_MAX_ROWS / 32 */
+
+typedef void* sd_stream_t;
+
+int sd_version(void);
+const char* sd_last_error(void);
+
+/* ---- dense-layer plumbing (model.py:234-236, 278, 306-311) ---- */
+/* h[t,:] = embed[tokens[t],:] (as f32) */
+int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, float* h, sd_stream_t stream);
+/* h += delta (if delta); x = h * gain / sqrt(mean(h^2) + eps) -> x (x_dtype) */
+int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain, float eps,
+                   void* x, int x_dtype, sd_stream_t stream);
+/* out = a / (1 + exp(-a)) */
+int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stream);
+/* out = a + b (f32), cast_out = (cast_dtype) out (nullable) */
+int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int cast_dtype, size_t n,
+                sd_stream_t stream);
+
+/* ---- RoPE + KV staging (model.py:216-232, 276-289; kvcache.py:91-96) ----
+ * qkv: [T][(H + 2*Hk) * dh] f32 (columns q | k | v). Interleaved-pair RoPE at
+ * positions[t] from fp64-derived cos/sin tables [max_pos][dh/2] (f32).
+ * q_rot = rope(q) * q_scale -> [T][H][dh] (q_dtype); q_pre = q (f32, nullable).
+ * k_raw (nullable), k_rot, v written at row (row_offset + t) of each kv head.
+ * rows_dev (nullable): rows t >= *rows_dev are skipped. */
+int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t* positions,
+                  const float* rope_cos, const float* rope_sin, float q_scale,
+                  void* q_rot, int q_dtype, float* q_pre,
+                  void* k_raw, void* k_rot, void* v, int kv_dtype, int64_t head_stride, int64_t row_offset,
+                  const int32_t* rows_dev, sd_stream_t stream);
+
+/* ---- split-KV attention: verify tree / draft / AR (model.py:238-247, 290-305) ----
+ * Row t (query head j uses kv head j / (H/Hk)) attends to
+ *   cache rows [0, ctx)  (src_kind 0: k_cache holds K_rot;
+ *                          src_kind 1: k_cache holds K_raw of partial-cache
+ *                          slots, rotated on load at rank ranks[slot] —
+ *                          kvcache.py:158-165)
+ *   + tree rows j <= t of the request with mask bit j set (mask_bits
+ *     [T][mask_words]; NULL = causal). Self is always visible.
+ * q: [T][H][dh] (q_dtype, already rotated and scaled). out: [T][H][dh].
+ * T <= SD_TREE_MAX_ROWS. rows_dev (nullable): live row count <= T read on
+ * device (rows beyond it produce zeros), so a padded verify forward needs no
+ * host round trip. Partial-cache slots with rank < 0 are holes and skipped.
+ * Split boundaries depend on ctx only (bitwise identical across GPU counts). */
+size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx);
+int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
+                 int src_kind, const void* k_cache, const void* v_cache, int kv_dtype, int64_t head_stride,
+                 int ctx, const int32_t* ranks, const float* rope_cos, const float* rope_sin,
+                 const void* k_tree, const void* v_tree, int64_t tree_head_stride,
+                 const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
+                 void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
+
+/* ---- Eq. 2 importance (kvcache.py:243-265) ----
+ * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),
+ * heads summed in ascending order. per_head (nullable): [L][Hk][end-start]. */
+int sd_importance_scores(const float* q_sum, const void* k_raw, int kv_dtype, int64_t layer_stride,
+                         int64_t head_stride, int L, int H, int Hk, int dh, int start, int end,
+                         float* scores, float* per_head, sd_stream_t stream);
+/* scores[l][i] = sum over kv heads (ascending) of per_head[l][k][i]; used after
+ * an all-gather of per-head partials (sharded refresh). */
+int sd_sum_head_scores(const float* per_head, int L, int Hk, int n, float* scores, sd_stream_t stream);
+
+/* ---- partial cache build / maintenance (kvcache.py:191-354) ----
+ * Partial cache per layer: slots [0, count) with pos, rank (position order),
+ * score (NaN = unscored) and K_raw / V in [kv_head][slot][dh]. */
+/* top-(take) of positions [sink, sink+n_cand) by (-score, pos), per layer
+ * (kvcache.py:286): slot sink+i <- i-th best; slots < sink <- sink positions. */
+size_t sd_select_workspace_bytes(int L, int n_cand);
+int sd_select_topk(const float* scores, int L, int n_cand, int sink, int take,
+                   int32_t* ppos, int32_t* prank, float* pscore, int slot_cap,
+                   void* workspace, size_t workspace_bytes, sd_stream_t stream);
+/* mirror (kvcache.py:300-319): slots sink.. hold positions upto-1 down to sink */
+int sd_mirror_positions(int L, int upto, int sink, int32_t* ppos, int32_t* prank, float* pscore,
+                        int slot_cap, sd_stream_t stream);
+/* copy K_raw/V rows at ppos[l][slot] for slots [0, count) from the full cache */
+int sd_gather_slots(int L, int count, const int32_t* ppos, int slot_cap, const void* full_k_raw,
+                    const void* full_v, int kv_dtype, int64_t full_layer_stride, int64_t full_head_stride,
+                    void* pk, void* pv, int64_t part_layer_stride, int64_t part_head_stride,
+                    int Hk, int dh, sd_stream_t stream);
+/* evict slots evict_slots_host[0..n_evict) (they become holes: pos = rank =
+ * -1) and admit positions first_pos..first_pos+a-1 into new_slots_host[0..a)
+ * (kvcache.py:215-225, 332-354). Slots [0, hi) are scanned; count_after =
+ * live entries after the update; ranks stay a dense position order. */
+int sd_partial_update(int L, int hi, int count_after, int first_pos, int a, const int32_t* new_slots_host,
+                      int n_evict, const int32_t* evict_slots_host, int32_t* ppos, int32_t* prank,
+                      float* pscore, int slot_cap, const void* full_k_raw, const void* full_v, int kv_dtype,
+                      int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                      int64_t part_layer_stride, int64_t part_head_stride, int Hk, int dh, sd_stream_t stream);
+
+/* ---- reconcile (kvcache.py:116-127) + last_queries (engine.py:280) ----
+ * keep offsets / count read from the device step result. Rows base+keep[i] ->
+ * base+i for K_raw, K_rot, V; q_sum[l][h] = sum_i q_pre[l][keep[i]][h]. */
+int sd_reconcile(int L, const int32_t* result, int base_len, void* k_raw, void* k_rot, void* v, int kv_dtype,
+                 int64_t layer_stride, int64_t head_stride, int Hk, int dh,
+                 const float* q_pre, int q_rows, int H, float* q_sum, sd_stream_t stream);
+
+/* ---- sampling (sampling.py:142-224, engine.py:155-181, 207-245) ---- */
+/* member mask source for sd_sample_rows */
+#define SD_MEMBER_NONE 0     /* no penalty                                      */
+#define SD_MEMBER_MASK 1     /* explicit uint8 mask [rows][V]                    */
+#define SD_MEMBER_WINDOW 2   /* window counts, all rows (draft heads / AR)       */
+#define SD_MEMBER_TREE 3     /* window counts + per-row branch splice (verify)   */
+#define SD_TRUNC_NONE 0
+#define SD_TRUNC_TOP_P 1
+#define SD_TRUNC_MIN_P 2
+#define SD_TRUNC_ETA 3
+#define SD_IN_LOGITS_F32 0
+#define SD_IN_LOGITS_F64 1
+#define SD_IN_PROBS_F64 2
+
+typedef struct {
+  int rows, V, in_kind;
+  double temperature, theta;
+  int ctrl_style;
+  int member_kind;
+  const uint8_t* member_mask;      /* SD_MEMBER_MASK */
+  const int32_t* win_count;        /* [V] */
+  const int32_t* win_ring;         /* [W] ring storage */
+  const int64_t* state;            /* device session state (ring head/len) */
+  int window;                      /* W */
+  const int32_t* tree;             /* device tree record (SD_MEMBER_TREE) */
+  int depth;                       /* gamma + 1 */
+  int trunc_kind;
+  double trunc_value, eta_alpha;   /* eta_alpha < 0 -> sqrt(eps) */
+  uint64_t seed;
+  const int32_t* positions;        /* [rows] draw keys; NULL -> tree-derived (n, n+d+1) */
+  int64_t n;                       /* tree-derived keys: row 0 -> n, node -> n + depth + 1 */
+  double* probs_out;               /* nullable [rows][V]: penalised softmax */
+  double* trunc_out;               /* nullable [rows][V]: truncated + renormalised */
+  int32_t* token_out;              /* nullable [rows]: inverse-CDF draw */
+} sd_sample_args;
+int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t stream);
+
+/* per-head top-w of the penalised draft distributions, ties to lower id
+ * (engine.py:207-215). out: concatenated candidates, head k gets widths[k]. */
+int sd_draft_topw(const float* logits, int heads, int V, const int32_t* win_count, double temperature,
+                  double theta, int ctrl_style, const int32_t* widths_host, int32_t* out, sd_stream_t stream);
+
+/* ---- n-gram table (ngram.py:18-66): open-addressing hash + per-first-token chains ----
+ * Table memory = sd_ngram_bytes(n, cap, V) bytes, zero-initialised by sd_ngram_init. */
+size_t sd_ngram_bytes(int n, int cap, int V);
+int sd_ngram_init(void* table, int n, int cap, int V, sd_stream_t stream);
+int sd_ngram_update(void* table, const int32_t* seq, int n_tail, int n_new, sd_stream_t stream);
+/* out_grams [k][n], out_count [1] */
+int sd_ngram_retrieve(const void* table, const int32_t* first, int k, int32_t* out_grams, int32_t* out_count,
+                      sd_stream_t stream);
+int sd_ngram_frequency(const void* table, const int32_t* grams, int count, int32_t* out, sd_stream_t stream);
+int sd_ngram_size(const void* table, int32_t* out, sd_stream_t stream);
+
+/* ---- tree (tree.py:87-175) + acceptance/commit (engine.py:247-290) ----
+ * Device tree record layout: see sd_tree_layout(). */
+int sd_tree_layout(int32_t* offsets_host, int n);
+/* per_head: concatenated candidates; grams [n_grams][depth] (n_grams from
+ * device when n_grams_dev != NULL, else n_grams_host). Writes the verify rows:
+ * row 0 = pending (state) at base_pos, node i at base_pos + 1 + depth. */
+int sd_tree_build(const int32_t* per_head, const int32_t* widths_host, int depth, const int32_t* grams,
+                  const int32_t* n_grams_dev, int n_grams_host, const int64_t* state, int64_t base_pos,
+                  int32_t* tree, sd_stream_t stream);
+/* retrieve (first = per_head[0]) + build in one launch */
+int sd_draft_tree(const void* ngram_table, int k, const int32_t* per_head, const int32_t* widths_host,
+                  int depth, const int64_t* state, int64_t base_pos, int32_t* grams_scratch, int32_t* tree,
+                  sd_stream_t stream);
+
+/* session state (int64[16]) slots */
+#define SD_ST_RING_HEAD 0
+#define SD_ST_RING_LEN 1
+#define SD_ST_HIST_LEN 2
+#define SD_ST_PENDING 3
+#define SD_ST_ERROR 4
+/* step result (int32[32]) slots */
+#define SD_RES_ACCEPTED 0
+#define SD_RES_BEST 1
+#define SD_RES_PICK 2
+#define SD_RES_ORIGIN 3
+#define SD_RES_ROWS 4
+#define SD_RES_PATHS 5
+#define SD_RES_PENDING 6   /* int32 copy of the pending token (next draft input) */
+#define SD_RES_YS 8
+#define SD_RES_KEEP 16
+
+/* acceptance + commit: path validity vs y, uniform pick at
+ * (select_seed, n), accepted count, ys, keep offsets -> result; then window
+ * push, history append, n-gram update (ngram may be NULL), pending <- last ys. */
+int sd_accept_commit(const int32_t* tree, const int32_t* y, uint64_t select_seed, int64_t n, int depth, int bonus,
+                     int64_t* state, int32_t* win_ring, int32_t* win_count, int window, int32_t* history,
+                     void* ngram_table, int32_t* result, sd_stream_t stream);
+/* push tokens into the penalty window (sampling.py:98-109) */
+int sd_window_push(const int32_t* tokens, int count, int64_t* state, int32_t* win_ring, int32_t* win_count,
+                   int window, sd_stream_t stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif

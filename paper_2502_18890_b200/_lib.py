@@ -1,0 +1,159 @@
+"""ctypes binding of libswiftdec_b200.so (the C ABI in include/swiftdec_b200.h).
+
+There is no fallback: if the library is missing or no CUDA device is present
+the product path raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libswiftdec_b200.so")
+
+SD_F32, SD_BF16, SD_F64 = 0, 1, 2
+TREE_MAX_ROWS, TREE_MAX_PATHS, TREE_MAX_DEPTH, MASK_WORDS = 256, 512, 8, 8
+MEMBER_NONE, MEMBER_MASK, MEMBER_WINDOW, MEMBER_TREE = 0, 1, 2, 3
+TRUNC_NONE, TRUNC_TOP_P, TRUNC_MIN_P, TRUNC_ETA = 0, 1, 2, 3
+IN_LOGITS_F32, IN_LOGITS_F64, IN_PROBS_F64 = 0, 1, 2
+ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR = 0, 1, 2, 3, 4
+RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_YS, RES_KEEP = 0, 1, 2, 3, 4, 5, 6, 8, 16
+
+P = C.c_void_p
+I32 = C.c_int32
+I64 = C.c_int64
+INT = C.c_int
+F32 = C.c_float
+F64 = C.c_double
+SZ = C.c_size_t
+U64 = C.c_uint64
+
+
+class SampleArgs(C.Structure):
+    _fields_ = [
+        ("rows", INT), ("V", INT), ("in_kind", INT),
+        ("temperature", F64), ("theta", F64),
+        ("ctrl_style", INT), ("member_kind", INT),
+        ("member_mask", P), ("win_count", P), ("win_ring", P), ("state", P),
+        ("window", INT), ("tree", P), ("depth", INT), ("trunc_kind", INT),
+        ("trunc_value", F64), ("eta_alpha", F64), ("seed", U64),
+        ("positions", P), ("n", I64),
+        ("probs_out", P), ("trunc_out", P), ("token_out", P),
+    ]
+
+
+_SIGS = {
+    "sd_version": (INT, []),
+    "sd_last_error": (C.c_char_p, []),
+    "sd_embed": (INT, [P, INT, P, INT, INT, P, P]),
+    "sd_add_rmsnorm": (INT, [P, P, INT, INT, P, F32, P, INT, P]),
+    "sd_silu": (INT, [P, P, INT, SZ, P]),
+    "sd_add_cast": (INT, [P, P, P, P, INT, SZ, P]),
+    "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, P]),
+    "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),
+    "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P,
+                           P, INT, P, SZ, P]),
+    "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
+    "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
+    "sd_select_workspace_bytes": (SZ, [INT, INT]),
+    "sd_select_topk": (INT, [P, INT, INT, INT, INT, P, P, P, INT, P, SZ, P]),
+    "sd_mirror_positions": (INT, [INT, INT, INT, P, P, P, INT, P]),
+    "sd_gather_slots": (INT, [INT, INT, P, INT, P, P, INT, I64, I64, P, P, I64, I64, INT, INT, P]),
+    "sd_partial_update": (INT, [INT, INT, INT, INT, INT, P, INT, P, P, P, P, INT, P, P, INT, I64, I64, P, P, I64,
+                                I64, INT, INT, P]),
+    "sd_reconcile": (INT, [INT, P, INT, P, P, P, INT, I64, I64, INT, INT, P, INT, INT, P, P]),
+    "sd_sample_rows": (INT, [P, C.POINTER(SampleArgs), P]),
+    "sd_draft_topw": (INT, [P, INT, INT, P, F64, F64, INT, P, P, P]),
+    "sd_ngram_bytes": (SZ, [INT, INT, INT]),
+    "sd_ngram_init": (INT, [P, INT, INT, INT, P]),
+    "sd_ngram_update": (INT, [P, P, INT, INT, P]),
+    "sd_ngram_retrieve": (INT, [P, P, INT, P, P, P]),
+    "sd_ngram_frequency": (INT, [P, P, INT, P, P]),
+    "sd_ngram_size": (INT, [P, P, P]),
+    "sd_tree_layout": (INT, [P, INT]),
+    "sd_tree_build": (INT, [P, P, INT, P, P, INT, P, I64, P, P]),
+    "sd_draft_tree": (INT, [P, INT, P, P, INT, P, I64, P, P, P]),
+    "sd_accept_commit": (INT, [P, P, U64, I64, INT, INT, P, P, P, INT, P, P, P, P]),
+    "sd_window_push": (INT, [P, INT, P, P, P, INT, P]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+class LibraryError(RuntimeError):
+    pass
+
+
+def load(require_cuda: bool = True):
+    """Load the library (once). Raises when it is missing — there is no CPU path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise LibraryError(
+            f"{LIB_PATH} not built; run `python -m paper_2502_18890_b200.build_lib` (nvcc, sm_100a)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise LibraryError("paper_2502_18890_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
+
+
+def call(name: str, *args):
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        msg = load().sd_last_error().decode(errors="replace")
+        raise LibraryError(f"{name} failed (code {rc}): {msg}")
+    return rc
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a tensor (None passes NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dcode(dtype: torch.dtype) -> int:
+    if dtype == torch.bfloat16:
+        return SD_BF16
+    if dtype == torch.float32:
+        return SD_F32
+    if dtype == torch.float64:
+        return SD_F64
+    raise ValueError(f"unsupported dtype {dtype}")
+
+
+def host_i32(values):
+    arr = (I32 * max(1, len(values)))(*[int(v) for v in values])
+    return arr
+
+
+_TREE_LAYOUT = None
+
+
+def tree_layout() -> dict:
+    global _TREE_LAYOUT
+    if _TREE_LAYOUT is None:
+        buf = (I32 * 32)()
+        n = load().sd_tree_layout(buf, 32)
+        names = ["T", "NPATHS", "HEADNODES", "DEPTH", "NGRAMS", "TOK", "POS", "PARENT", "NDEPTH", "PNODES",
+                 "PORIGIN", "POIDX", "MASK", "TOTAL", "MAX_ROWS", "MAX_PATHS", "MAX_DEPTH", "MASK_WORDS"]
+        _TREE_LAYOUT = {k: int(buf[i]) for i, k in enumerate(names[:n])}
+    return _TREE_LAYOUT

@@ -1,0 +1,464 @@
+// Split-KV attention for the decode step: tree verification over the full
+// cache, draft attention over the rank-rotated partial cache, AR decode and
+// causal prefill blocks — one kernel family, CUDA-core fp32 math.
+//
+// Reference semantics: model.py:238-247 (_attend: softmax(q.k/sqrt(dh)) V with
+// query head j on kv head j // G), model.py:290-300 (masked: cache + ancestors
+// + self), model.py:301-305 (causal), kvcache.py:158-165 (draft keys rotated at
+// rank 0..m-1).
+//
+// Grid: x = cache chunk (chunk length is a function of ctx only, so the result
+// is bitwise independent of how many GPUs share the heads) + 1 tree chunk,
+// y = kv head, z = query-row tile. Each CTA writes an un-normalised partial
+// (o / l, lse) per query row; sd_attention then merges chunks in fixed order.
+#include "common.cuh"
+
+namespace sd {
+
+struct AttnParams {
+  const void* q;
+  int T, H, Hk, G;
+  const void* k_cache;
+  const void* v_cache;
+  int64_t head_stride;
+  int ctx;
+  const int32_t* ranks;
+  const float* cosT;
+  const float* sinT;
+  const void* k_tree;
+  const void* v_tree;
+  int64_t tree_head_stride;
+  const uint32_t* mask;
+  int mask_words;
+  int chunk, n_chunks;
+  float* ws_o;
+  float* ws_lse;
+  const int32_t* rows_dev;  // nullable: live row count (<= T) read on device
+};
+
+__device__ __forceinline__ int live_rows(const AttnParams& p) {
+  if (!p.rows_dev) return p.T;
+  const int t = *p.rows_dev;
+  return t < p.T ? t : p.T;
+}
+
+// partial-cache slots with rank < 0 are holes (evicted, not yet reused)
+__device__ __forceinline__ uint32_t slot_valid_bits(const int32_t* __restrict__ ranks, int kb, int nk, int lane) {
+  const bool ok = lane < nk && ranks[kb + lane] >= 0;
+  return __ballot_sync(0xffffffffu, ok);
+}
+
+static inline int chunk_len_for(int ctx) {
+  int c = (ctx + 31) / 32;
+  c = (c + 255) / 256 * 256;
+  return c < 256 ? 256 : c;
+}
+static inline int n_chunks_for(int ctx) {
+  if (ctx <= 0) return 0;
+  const int c = chunk_len_for(ctx);
+  return (ctx + c - 1) / c;
+}
+
+// Stage 32 keys (rows key0.. of a source) into Ks [32][DH+1] / Vs [32][DH] as
+// fp32; `lane_stride` threads cooperate (a warp or the whole CTA).
+template <int DH, typename KT, bool ROT>
+__device__ __forceinline__ void stage_tile(float* Ks, float* Vs, const KT* __restrict__ K, const KT* __restrict__ V,
+                                           int key0, int nkeys, const int32_t* __restrict__ ranks,
+                                           const float* __restrict__ cosT, const float* __restrict__ sinT, int tid,
+                                           int nthreads) {
+  constexpr int HALF = DH / 2;
+  // K: pairs so RoPE can be applied on load
+  for (int i = tid; i < 32 * HALF; i += nthreads) {
+    const int j = i / HALF, e = i - j * HALF;
+    float a = 0.f, b = 0.f;
+    if (j < nkeys) {
+      const int64_t row = key0 + j;
+      a = to_f(K[row * DH + 2 * e]);
+      b = to_f(K[row * DH + 2 * e + 1]);
+      if (ROT) {
+        const int64_t r = ranks[row];
+        const float c = cosT[r * HALF + e], s = sinT[r * HALF + e];
+        const float ra = a * c - b * s, rb = a * s + b * c;
+        a = ra;
+        b = rb;
+      }
+    }
+    Ks[j * (DH + 1) + 2 * e] = a;
+    Ks[j * (DH + 1) + 2 * e + 1] = b;
+  }
+  for (int i = tid; i < 32 * DH; i += nthreads) {
+    const int j = i / DH, e = i - j * DH;
+    Vs[j * DH + e] = j < nkeys ? to_f(V[(int64_t)(key0 + j) * DH + e]) : 0.f;
+  }
+}
+
+// Online-softmax update of RPW query rows against one 32-key tile (lane = key).
+// vis[r]: bitmask of visible keys of this tile for row r (0 = row inactive).
+template <int DH, int RPW>
+__device__ __forceinline__ void tile_update(const float* __restrict__ Ks, const float* __restrict__ Vs,
+                                            const float* const* qrow, const uint32_t* vis, float* m, float* l,
+                                            float (*acc)[(DH >= 32 ? DH / 32 : 1)], int lane) {
+  constexpr int EPL = DH >= 32 ? DH / 32 : 1;
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    if (vis[r] == 0u) continue;  // warp-uniform
+    const float* q = qrow[r];
+    float s = 0.f;
+#pragma unroll 16
+    for (int d = 0; d < DH; ++d) s = fmaf(q[d], Ks[lane * (DH + 1) + d], s);
+    const bool on = (vis[r] >> lane) & 1u;
+    s = on ? s : -INFINITY;
+    const float tmax = warp_max(s);
+    const float mn = fmaxf(m[r], tmax);
+    if (mn == -INFINITY) continue;         // nothing visible yet (warp-uniform)
+    const float corr = __expf(m[r] - mn);  // m = -inf initially -> 0
+    const float p = on ? __expf(s - mn) : 0.f;
+    l[r] = l[r] * corr + warp_sum(p);
+    m[r] = mn;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[r][e] *= corr;
+    if (DH >= 32 || lane < DH) {
+#pragma unroll 8
+      for (int j = 0; j < 32; ++j) {
+        const float pj = __shfl_sync(0xffffffffu, p, j);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[r][e] = fmaf(pj, Vs[j * DH + lane * EPL + e], acc[r][e]);
+      }
+    } else {
+      for (int j = 0; j < 32; ++j) (void)__shfl_sync(0xffffffffu, p, j);
+    }
+  }
+}
+
+// visibility bits of tile keys [kt0, kt0+32) of the tree chunk for request row t
+__device__ __forceinline__ uint32_t tree_vis(const uint32_t* __restrict__ mask, int mask_words, int t, int kt0,
+                                             int nkeys) {
+  uint32_t bits;
+  if (mask) {
+    const int w = kt0 >> 5;  // kt0 multiple of 32
+    bits = w < mask_words ? mask[t * mask_words + w] : 0u;
+  } else {
+    bits = 0xffffffffu;
+  }
+  // only rows j <= t (ancestors and self); self always
+  const int lim = t - kt0;  // keys kt0..kt0+lim visible by causality
+  uint32_t causal = lim >= 31 ? 0xffffffffu : (lim < 0 ? 0u : ((1u << (lim + 1)) - 1u));
+  bits &= causal;
+  if (lim >= 0 && lim < 32) bits |= (1u << lim);
+  const uint32_t valid = nkeys >= 32 ? 0xffffffffu : ((1u << nkeys) - 1u);
+  return bits & valid;
+}
+
+// Mode A: 8 warps split 64 query rows (8 each); the CTA stages shared 32-key tiles.
+template <int DH, typename QT, typename KT, bool ROT>
+__global__ void __launch_bounds__(256) attn_rows_kernel(AttnParams p) {
+  constexpr int EPL = DH >= 32 ? DH / 32 : 1;
+  constexpr int RPW = 8;
+  extern __shared__ float smem[];
+  float* Qs = smem;                // [64][DH]
+  float* Ks = Qs + 64 * DH;        // [32][DH+1]
+  float* Vs = Ks + 32 * (DH + 1);  // [32][DH]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kvh = blockIdx.y;
+  const int Tl = live_rows(p);
+  const int GT = p.G * Tl;
+  const int rho0 = blockIdx.z * 64;
+  if (rho0 >= GT) return;
+  const bool tree = (int)blockIdx.x == p.n_chunks;
+  // load Q rows of this tile
+  for (int i = tid; i < 64 * DH; i += 256) {
+    const int rr = i / DH, d = i - rr * DH;
+    const int rho = rho0 + rr;
+    float v = 0.f;
+    if (rho < GT) {
+      const int t = rho / p.G, g = rho - t * p.G;
+      v = to_f(((const QT*)p.q)[((int64_t)t * p.H + kvh * p.G + g) * DH + d]);
+    }
+    Qs[i] = v;
+  }
+  const KT* K;
+  const KT* V;
+  int k_begin, k_end;
+  if (tree) {
+    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
+    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    k_begin = 0;
+    k_end = Tl;
+  } else {
+    K = (const KT*)p.k_cache + kvh * p.head_stride;
+    V = (const KT*)p.v_cache + kvh * p.head_stride;
+    k_begin = blockIdx.x * p.chunk;
+    k_end = min(p.ctx, k_begin + p.chunk);
+  }
+  float m[RPW], l[RPW], acc[RPW][EPL];
+  const float* qrow[RPW];
+  int trow[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[r][e] = 0.f;
+    const int rr = warp + 8 * r;
+    qrow[r] = Qs + rr * DH;
+    trow[r] = (rho0 + rr < GT) ? (rho0 + rr) / p.G : -1;
+  }
+  __syncthreads();
+  for (int kb = k_begin; kb < k_end; kb += 32) {
+    const int nk = min(32, k_end - kb);
+    if (tree || !ROT)
+      stage_tile<DH, KT, false>(Ks, Vs, K, V, kb, nk, nullptr, nullptr, nullptr, tid, 256);
+    else
+      stage_tile<DH, KT, true>(Ks, Vs, K, V, kb, nk, p.ranks, p.cosT, p.sinT, tid, 256);
+    __syncthreads();
+    uint32_t vis[RPW];
+    uint32_t valid = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
+    if (ROT && !tree) valid = slot_valid_bits(p.ranks, kb, nk, lane);
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+      vis[r] = trow[r] < 0 ? 0u : (tree ? tree_vis(p.mask, p.mask_words, trow[r], kb, nk) : valid);
+    tile_update<DH, RPW>(Ks, Vs, qrow, vis, m, l, acc, lane);
+    __syncthreads();
+  }
+  // write partials
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    if (trow[r] < 0) continue;
+    const int rho = rho0 + warp + 8 * r;
+    const int t = trow[r], g = rho - t * p.G, head = kvh * p.G + g;
+    const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + head;
+    const float inv = l[r] > 0.f ? 1.f / l[r] : 0.f;
+    if (DH >= 32 || lane < DH) {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) p.ws_o[oi * DH + lane * EPL + e] = acc[r][e] * inv;
+    }
+    if (lane == 0) p.ws_lse[oi] = l[r] > 0.f ? m[r] + __logf(l[r]) : -INFINITY;
+  }
+}
+
+// Mode B (G*T <= 8 rows: draft / AR): 4 warps split the chunk's keys, each warp
+// handles every row, then the warps' states are merged in fixed order.
+template <int DH, typename QT, typename KT, bool ROT>
+__global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
+  constexpr int EPL = DH >= 32 ? DH / 32 : 1;
+  constexpr int RPW = 8, NW = 4;
+  extern __shared__ float smem[];
+  float* Qs = smem;                         // [8][DH]
+  float* Wk = Qs + 8 * DH;                  // per warp: K [32][DH+1], V [32][DH]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float* Ks = Wk + warp * (32 * (DH + 1) + 32 * DH);
+  float* Vs = Ks + 32 * (DH + 1);
+  const int kvh = blockIdx.y;
+  const int Tl = live_rows(p);
+  const int GT = p.G * Tl;
+  const bool tree = (int)blockIdx.x == p.n_chunks;
+  for (int i = tid; i < 8 * DH; i += 128) {
+    const int rr = i / DH, d = i - rr * DH;
+    float v = 0.f;
+    if (rr < GT) {
+      const int t = rr / p.G, g = rr - t * p.G;
+      v = to_f(((const QT*)p.q)[((int64_t)t * p.H + kvh * p.G + g) * DH + d]);
+    }
+    Qs[i] = v;
+  }
+  const KT* K;
+  const KT* V;
+  int k_begin, k_end;
+  if (tree) {
+    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
+    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    k_begin = 0;
+    k_end = Tl;
+  } else {
+    K = (const KT*)p.k_cache + kvh * p.head_stride;
+    V = (const KT*)p.v_cache + kvh * p.head_stride;
+    k_begin = blockIdx.x * p.chunk;
+    k_end = min(p.ctx, k_begin + p.chunk);
+  }
+  float m[RPW], l[RPW], acc[RPW][EPL];
+  const float* qrow[RPW];
+  int trow[RPW];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    m[r] = -INFINITY;
+    l[r] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[r][e] = 0.f;
+    qrow[r] = Qs + r * DH;
+    trow[r] = r < GT ? r / p.G : -1;
+  }
+  __syncthreads();
+  for (int kb = k_begin + 32 * warp; kb < k_end; kb += 32 * NW) {
+    const int nk = min(32, k_end - kb);
+    if (tree || !ROT)
+      stage_tile<DH, KT, false>(Ks, Vs, K, V, kb, nk, nullptr, nullptr, nullptr, lane, 32);
+    else
+      stage_tile<DH, KT, true>(Ks, Vs, K, V, kb, nk, p.ranks, p.cosT, p.sinT, lane, 32);
+    __syncwarp();
+    uint32_t vis[RPW];
+    uint32_t valid = nk >= 32 ? 0xffffffffu : ((1u << nk) - 1u);
+    if (ROT && !tree) valid = slot_valid_bits(p.ranks, kb, nk, lane);
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+      vis[r] = trow[r] < 0 ? 0u : (tree ? tree_vis(p.mask, p.mask_words, trow[r], kb, nk) : valid);
+    tile_update<DH, RPW>(Ks, Vs, qrow, vis, m, l, acc, lane);
+    __syncwarp();
+  }
+  __syncthreads();
+  // cross-warp merge through shared memory (reuse the staging area)
+  float* Sm = Wk;                // [NW][RPW] m
+  float* Sl = Sm + NW * RPW;     // [NW][RPW] l
+  float* So = Sl + NW * RPW;     // [NW][RPW][DH]
+  if (lane == 0) {
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      Sm[warp * RPW + r] = m[r];
+      Sl[warp * RPW + r] = l[r];
+    }
+  }
+  if (DH >= 32 || lane < DH) {
+#pragma unroll
+    for (int r = 0; r < RPW; ++r)
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) So[(warp * RPW + r) * DH + lane * EPL + e] = acc[r][e];
+  }
+  __syncthreads();
+  for (int i = tid; i < RPW * DH; i += 128) {
+    const int r = i / DH, d = i - r * DH;
+    if (r >= GT) continue;
+    float M = -INFINITY;
+    for (int w = 0; w < NW; ++w) M = fmaxf(M, Sm[w * RPW + r]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < NW; ++w) {
+        const float sc = __expf(Sm[w * RPW + r] - M);
+        L += Sl[w * RPW + r] * sc;
+        O += So[(w * RPW + r) * DH + d] * sc;
+      }
+    }
+    const int t = r / p.G, g = r - t * p.G, head = kvh * p.G + g;
+    const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + head;
+    p.ws_o[oi * DH + d] = L > 0.f ? O / L : 0.f;
+    if (d == 0) p.ws_lse[oi] = L > 0.f ? M + __logf(L) : -INFINITY;
+  }
+}
+
+// merge chunk partials in ascending chunk order -> out [T][H][DH]
+template <int DH, typename OT>
+__global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
+                                  int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out) {
+  const int row = blockIdx.x;  // t * H + head
+  if (rows_dev && row / H >= *rows_dev) {  // padded row: defined zeros
+    for (int d = threadIdx.x; d < DH; d += blockDim.x) out[(int64_t)row * DH + d] = from_f<OT>(0.f);
+    return;
+  }
+  float M = -INFINITY;
+  for (int c = 0; c < nsplit; ++c) M = fmaxf(M, ws_lse[(int64_t)c * TH + row]);
+  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
+    float L = 0.f, O = 0.f;
+    for (int c = 0; c < nsplit; ++c) {
+      const float lse = ws_lse[(int64_t)c * TH + row];
+      if (lse == -INFINITY) continue;
+      const float w = __expf(lse - M);
+      L += w;
+      O += w * ws_o[((int64_t)c * TH + row) * DH + d];
+    }
+    out[(int64_t)row * DH + d] = from_f<OT>(L > 0.f ? O / L : 0.f);
+  }
+}
+
+template <int DH, typename QT, typename KT, typename OT>
+static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaStream_t st) {
+  AttnParams p = p0;
+  const int GT = p.G * p.T;
+  dim3 grid(p.n_chunks + 1, p.Hk, 1);
+  if (GT <= 8) {
+    const size_t smem = (8 * DH + 4 * (32 * (DH + 1) + 32 * DH)) * sizeof(float);
+    auto kern = src_kind ? attn_keys_kernel<DH, QT, KT, true> : attn_keys_kernel<DH, QT, KT, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 128, smem, st>>>(p);
+  } else {
+    grid.z = (GT + 63) / 64;
+    const size_t smem = (64 * DH + 32 * (DH + 1) + 32 * DH) * sizeof(float);
+    auto kern = src_kind ? attn_rows_kernel<DH, QT, KT, true> : attn_rows_kernel<DH, QT, KT, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    kern<<<grid, 256, smem, st>>>(p);
+  }
+  int rc = check_launch("sd_attention(partial)");
+  if (rc) return rc;
+  attn_merge_kernel<DH, OT><<<p.T * p.H, DH >= 128 ? 128 : (DH < 32 ? 32 : DH), 0, st>>>(
+      p.ws_o, p.ws_lse, p.n_chunks + 1, p.T * p.H, p.H, p.rows_dev, (OT*)out);
+  return check_launch("sd_attention(merge)");
+}
+
+template <int DH>
+static int dispatch_types(const AttnParams& p, int q_dtype, int kv_dtype, int out_dtype, int src_kind, void* out,
+                          cudaStream_t st) {
+  typedef __nv_bfloat16 bf;
+  if (q_dtype == SD_BF16 && kv_dtype == SD_BF16 && out_dtype == SD_BF16)
+    return launch_attention<DH, bf, bf, bf>(p, src_kind, out, st);
+  if (q_dtype == SD_F32 && kv_dtype == SD_BF16 && out_dtype == SD_BF16)
+    return launch_attention<DH, float, bf, bf>(p, src_kind, out, st);
+  if (q_dtype == SD_F32 && kv_dtype == SD_F32 && out_dtype == SD_F32)
+    return launch_attention<DH, float, float, float>(p, src_kind, out, st);
+  set_error("sd_attention: unsupported dtype combination q=%d kv=%d out=%d", q_dtype, kv_dtype, out_dtype);
+  return SD_EUNSUPPORTED;
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
+  const size_t ns = (size_t)n_chunks_for(ctx) + 1;
+  return ns * (size_t)T * H * (dh + 1) * sizeof(float);
+}
+
+int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int src_kind, const void* k_cache,
+                 const void* v_cache, int kv_dtype, int64_t head_stride, int ctx, const int32_t* ranks,
+                 const float* rope_cos, const float* rope_sin, const void* k_tree, const void* v_tree,
+                 int64_t tree_head_stride, const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
+                 void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
+  SD_REQUIRE(T > 0 && T <= SD_TREE_MAX_ROWS, "sd_attention: T=%d out of range", T);
+  SD_REQUIRE(H > 0 && Hk > 0 && H % Hk == 0, "sd_attention: heads");
+  SD_REQUIRE(ctx >= 0, "sd_attention: ctx");
+  SD_REQUIRE(!mask_bits || mask_words * 32 >= T, "sd_attention: mask words");
+  SD_REQUIRE(src_kind == 0 || (ranks && rope_cos && rope_sin), "sd_attention: partial source needs ranks/rope");
+  SD_REQUIRE(workspace_bytes >= sd_attention_workspace_bytes(T, H, dh, ctx), "sd_attention: workspace too small");
+  AttnParams p;
+  p.q = q;
+  p.T = T;
+  p.H = H;
+  p.Hk = Hk;
+  p.G = H / Hk;
+  p.k_cache = k_cache;
+  p.v_cache = v_cache;
+  p.head_stride = head_stride;
+  p.ctx = ctx;
+  p.ranks = ranks;
+  p.cosT = rope_cos;
+  p.sinT = rope_sin;
+  p.k_tree = k_tree;
+  p.v_tree = v_tree;
+  p.tree_head_stride = tree_head_stride;
+  p.mask = mask_bits;
+  p.mask_words = mask_words;
+  p.chunk = chunk_len_for(ctx);
+  p.n_chunks = n_chunks_for(ctx);
+  p.ws_o = (float*)workspace;
+  p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
+  p.rows_dev = rows_dev;
+  auto st = as_stream(stream);
+  switch (dh) {
+    case 8: return dispatch_types<8>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    case 16: return dispatch_types<16>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    case 32: return dispatch_types<32>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    case 64: return dispatch_types<64>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    case 128: return dispatch_types<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    default: set_error("sd_attention: head_dim %d unsupported", dh); return SD_EUNSUPPORTED;
+  }
+}
+
+}  // extern "C"

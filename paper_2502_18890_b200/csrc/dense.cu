@@ -1,0 +1,204 @@
+// Dense-layer plumbing around the cuBLAS GEMMs + RoPE/KV staging.
+// Reference: model.py:216-236 (rope, rmsnorm), 276-289 (per-row q/k/v, stage),
+// 306-311 (residual, SiLU MLP, final norm); kvcache.py:91-96 (stage).
+#include <stdarg.h>
+
+#include "common.cuh"
+
+namespace sd {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return SD_ECUDA;
+  }
+  return SD_OK;
+}
+
+template <typename T>
+__global__ void embed_kernel(const int32_t* __restrict__ tok, const T* __restrict__ E, int d, float* __restrict__ h) {
+  const int t = blockIdx.x;
+  const T* row = E + (int64_t)tok[t] * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) h[(int64_t)t * d + i] = to_f(row[i]);
+}
+
+// one block per row: h += delta; x = h * gain / sqrt(mean(h^2) + eps)
+template <typename XT>
+__global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
+                                   const float* __restrict__ gain, float eps, XT* __restrict__ x) {
+  __shared__ float red[32];
+  const int64_t base = (int64_t)blockIdx.x * d;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    float v = h[base + i];
+    if (delta) {
+      v += delta[base + i];
+      h[base + i] = v;
+    }
+    ss += v * v;
+  }
+  ss = block_reduce(ss, red, [](float a, float b) { return a + b; });
+  const float inv = rsqrtf(ss / (float)d + eps);
+  for (int i = threadIdx.x; i < d; i += blockDim.x) x[base + i] = from_f<XT>(h[base + i] * (gain[i] * inv));
+}
+
+template <typename OT>
+__global__ void silu_kernel(const float* __restrict__ a, OT* __restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = a[i];
+    out[i] = from_f<OT>(v / (1.f + __expf(-v)));
+  }
+}
+
+template <typename OT>
+__global__ void add_cast_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
+                                OT* __restrict__ cast, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const float v = a[i] + b[i];
+    out[i] = v;
+    if (cast) cast[i] = from_f<OT>(v);
+  }
+}
+
+// grid: T rows; threads over (head, pair) for H q-heads + 2 Hk kv-heads.
+template <typename QT, typename KT>
+__global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, int dh,
+                                  const int32_t* __restrict__ positions, const float* __restrict__ cosT,
+                                  const float* __restrict__ sinT, float q_scale, QT* __restrict__ q_rot,
+                                  float* __restrict__ q_pre, KT* __restrict__ k_raw, KT* __restrict__ k_rot,
+                                  KT* __restrict__ v, int64_t head_stride, int64_t row_offset,
+                                  const int32_t* __restrict__ rows_dev) {
+  const int t = blockIdx.x;
+  if (rows_dev && t >= *rows_dev) return;
+  const int half = dh >> 1;
+  const int width = (H + 2 * Hk) * dh;
+  const float* row = qkv + (int64_t)t * width;
+  const int64_t pos = positions[t];
+  const float* cs = cosT + pos * half;
+  const float* sn = sinT + pos * half;
+  const int64_t dst_row = row_offset + t;
+  const int pairs = (H + Hk) * half;  // rotated heads (q then k)
+  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
+    const int head = i / half, j = i - head * half;
+    const float a = row[head * dh + 2 * j], b = row[head * dh + 2 * j + 1];
+    const float c = cs[j], s = sn[j];
+    const float ra = a * c - b * s, rb = a * s + b * c;
+    if (head < H) {
+      const int64_t o = ((int64_t)t * H + head) * dh + 2 * j;
+      q_rot[o] = from_f<QT>(ra * q_scale);
+      q_rot[o + 1] = from_f<QT>(rb * q_scale);
+      if (q_pre) {
+        q_pre[o] = a;
+        q_pre[o + 1] = b;
+      }
+    } else {
+      const int kh = head - H;
+      const int64_t o = kh * head_stride + dst_row * dh + 2 * j;
+      k_rot[o] = from_f<KT>(ra);
+      k_rot[o + 1] = from_f<KT>(rb);
+      if (k_raw) {
+        k_raw[o] = from_f<KT>(a);
+        k_raw[o + 1] = from_f<KT>(b);
+      }
+    }
+  }
+  for (int i = threadIdx.x; i < Hk * dh; i += blockDim.x) {
+    const int kh = i / dh, e = i - kh * dh;
+    v[kh * head_stride + dst_row * dh + e] = from_f<KT>(row[(H + Hk) * dh + i]);
+  }
+}
+
+static int grid_for(size_t n) {
+  size_t g = (n + 255) / 256;
+  if (g > 148 * 32) g = 148 * 32;
+  return (int)(g ? g : 1);
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+int sd_version(void) { return 1; }
+const char* sd_last_error(void) { return sd::g_err; }
+
+int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, float* h, sd_stream_t stream) {
+  SD_REQUIRE(T > 0 && d > 0, "sd_embed: bad sizes");
+  auto st = as_stream(stream);
+  if (dtype == SD_BF16)
+    embed_kernel<<<T, 256, 0, st>>>(tokens, (const __nv_bfloat16*)embed, d, h);
+  else if (dtype == SD_F32)
+    embed_kernel<<<T, 256, 0, st>>>(tokens, (const float*)embed, d, h);
+  else
+    SD_REQUIRE(false, "sd_embed: dtype");
+  return check_launch("sd_embed");
+}
+
+int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain, float eps, void* x, int x_dtype,
+                   sd_stream_t stream) {
+  SD_REQUIRE(T > 0 && d > 0, "sd_add_rmsnorm: bad sizes");
+  auto st = as_stream(stream);
+  const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
+  if (x_dtype == SD_BF16)
+    add_rmsnorm_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x);
+  else if (x_dtype == SD_F32)
+    add_rmsnorm_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x);
+  else
+    SD_REQUIRE(false, "sd_add_rmsnorm: dtype");
+  return check_launch("sd_add_rmsnorm");
+}
+
+int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stream) {
+  auto st = as_stream(stream);
+  if (out_dtype == SD_BF16)
+    silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (__nv_bfloat16*)out, n);
+  else if (out_dtype == SD_F32)
+    silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (float*)out, n);
+  else
+    SD_REQUIRE(false, "sd_silu: dtype");
+  return check_launch("sd_silu");
+}
+
+int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int cast_dtype, size_t n,
+                sd_stream_t stream) {
+  auto st = as_stream(stream);
+  if (cast_dtype == SD_BF16)
+    add_cast_kernel<<<grid_for(n), 256, 0, st>>>(a, b, out, (__nv_bfloat16*)cast_out, n);
+  else
+    add_cast_kernel<<<grid_for(n), 256, 0, st>>>(a, b, out, (float*)cast_out, n);
+  return check_launch("sd_add_cast");
+}
+
+int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t* positions, const float* rope_cos,
+                  const float* rope_sin, float q_scale, void* q_rot, int q_dtype, float* q_pre, void* k_raw,
+                  void* k_rot, void* v, int kv_dtype, int64_t head_stride, int64_t row_offset,
+                  const int32_t* rows_dev, sd_stream_t stream) {
+  SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 2) == 0, "sd_rope_stage: bad sizes");
+  auto st = as_stream(stream);
+#define SD_RS(QT, KT)                                                                                          \
+  rope_stage_kernel<QT, KT><<<T, 256, 0, st>>>(qkv, H, Hk, dh, positions, rope_cos, rope_sin, q_scale, (QT*)q_rot, \
+                                              q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev)
+  if (q_dtype == SD_F32 && kv_dtype == SD_F32)
+    SD_RS(float, float);
+  else if (q_dtype == SD_BF16 && kv_dtype == SD_BF16)
+    SD_RS(__nv_bfloat16, __nv_bfloat16);
+  else if (q_dtype == SD_F32 && kv_dtype == SD_BF16)
+    SD_RS(float, __nv_bfloat16);
+  else
+    SD_REQUIRE(false, "sd_rope_stage: dtype combo");
+#undef SD_RS
+  return check_launch("sd_rope_stage");
+}
+
+}  // extern "C"

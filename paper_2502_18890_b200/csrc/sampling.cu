@@ -1,0 +1,487 @@
+// Contextual-penalty sampling on device, fp64 arithmetic like the reference.
+// Reference: sampling.py:142-162 (Eq. 3 penalty + softmax), 193-216
+// (top-p / min-p / eta truncation), 219-224 (inverse-CDF at the (seed, pos)
+// deviate), 120-139 (shrunk window masks); engine.py:155-181 (per verify row
+// window splice), 207-215 (draft per-head top-w, ties to the lower id),
+// 237-245 (row draw positions).
+//
+// One CTA per row. Membership of token v in row r is computed on the fly from
+// the window's count array plus at most 2*depth patched tokens (tokens slid
+// out of the window by the branch, tokens of the branch itself), so the
+// [T, V] boolean mask of the reference is never materialised.
+#include "common.cuh"
+
+namespace sd {
+
+constexpr int SMP_THREADS = 1024;
+constexpr int MAX_PATCH = 2 * SD_TREE_MAX_DEPTH;
+
+struct SampleDev {
+  int rows, V, in_kind;
+  double temperature, theta;
+  int ctrl_style, member_kind;
+  const uint8_t* member_mask;
+  const int32_t* win_count;
+  const int32_t* win_ring;
+  const int64_t* state;
+  int window;
+  const int32_t* tree;
+  int depth;
+  int trunc_kind;
+  double trunc_value, eta_alpha;
+  uint64_t seed;
+  const int32_t* positions;
+  int64_t n;
+  double* probs_out;
+  double* trunc_out;
+  int32_t* token_out;
+};
+
+struct RowCtx {
+  int n_patch;
+  int patch_tok[MAX_PATCH];
+  int patch_val[MAX_PATCH];
+  int64_t pos;
+};
+
+__device__ __forceinline__ bool is_member(const SampleDev& a, const RowCtx& rc, int row, int v) {
+  switch (a.member_kind) {
+    case SD_MEMBER_MASK: return a.member_mask[(int64_t)row * a.V + v] != 0;
+    case SD_MEMBER_WINDOW: return a.window > 0 && a.win_count[v] > 0;
+    case SD_MEMBER_TREE: {
+      if (a.window <= 0) return false;
+      bool m = a.win_count[v] > 0;
+      for (int i = 0; i < rc.n_patch; ++i)
+        if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
+      return m;
+    }
+    default: return false;
+  }
+}
+
+template <int IN>
+__device__ __forceinline__ double load_in(const void* in, int64_t idx) {
+  if (IN == SD_IN_LOGITS_F32) return (double)((const float*)in)[idx];
+  return ((const double*)in)[idx];
+}
+
+// scaled logit l / (t * I) (sampling.py:142-153)
+__device__ __forceinline__ double scaled(double l, bool member, const SampleDev& a) {
+  if (!member) return l / a.temperature;
+  if (a.ctrl_style) return (l < 0.0 ? l * a.theta : l / a.theta) / a.temperature;
+  return l / (a.temperature * a.theta);
+}
+
+// thread 0: per-row patches (engine.py:155-181) and draw position
+__device__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
+  rc.n_patch = 0;
+  if (a.positions) {
+    rc.pos = a.positions[row];
+  } else {
+    rc.pos = row == 0 ? a.n : a.n + a.tree[tree_off::NDEPTH + row - 1] + 1;
+  }
+  if (a.member_kind != SD_MEMBER_TREE || a.window <= 0 || row == 0) return;
+  const int W = a.window;
+  const int node = row - 1;
+  int branch[SD_TREE_MAX_DEPTH];
+  int b = 0;
+  for (int x = node; x >= 0 && b < SD_TREE_MAX_DEPTH; x = a.tree[tree_off::PARENT + x])
+    branch[b++] = a.tree[tree_off::TOK + 1 + x];  // deepest first
+  const int64_t ring = a.state[SD_ST_RING_LEN], head = a.state[SD_ST_RING_HEAD];
+  int64_t cap = a.depth < ring ? a.depth : ring;
+  int64_t drop = ring + b - W;
+  if (drop < 0) drop = 0;
+  if (drop > cap) drop = cap;
+  // tokens slid out of the window (oldest first), with their removal counts
+  for (int64_t j = 0; j < drop; ++j) {
+    const int tok = a.win_ring[(head + j) % W];
+    int found = -1;
+    for (int i = 0; i < rc.n_patch; ++i)
+      if (rc.patch_tok[i] == tok) found = i;
+    if (found < 0) {
+      found = rc.n_patch++;
+      rc.patch_tok[found] = tok;
+      rc.patch_val[found] = 0;  // used as removal counter for now
+    }
+    rc.patch_val[found] += 1;
+  }
+  for (int i = 0; i < rc.n_patch; ++i) rc.patch_val[i] = (a.win_count[rc.patch_tok[i]] - rc.patch_val[i]) > 0;
+  const int tail = b < W ? b : W;  // last min(b, W) branch tokens = the deepest `tail`
+  for (int j = 0; j < tail; ++j) {
+    const int tok = branch[j];
+    int found = -1;
+    for (int i = 0; i < rc.n_patch; ++i)
+      if (rc.patch_tok[i] == tok) found = i;
+    if (found < 0) {
+      found = rc.n_patch++;
+      rc.patch_tok[found] = tok;
+    }
+    rc.patch_val[found] = 1;
+  }
+}
+
+struct DI {
+  double v;
+  int i;
+};
+__device__ __forceinline__ DI better(DI x, DI y) {  // larger value, ties -> lower index
+  if (x.v > y.v) return x;
+  if (y.v > x.v) return y;
+  return x.i <= y.i ? x : y;
+}
+
+__device__ DI block_argmax(DI x, DI* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    DI y;
+    y.v = __shfl_xor_sync(0xffffffffu, x.v, o);
+    y.i = __shfl_xor_sync(0xffffffffu, x.i, o);
+    x = better(x, y);
+  }
+  __syncthreads();
+  if (lane == 0) scratch[wid] = x;
+  __syncthreads();
+  DI r = scratch[0];
+  for (int w = 1; w < nw; ++w) r = better(r, scratch[w]);
+  __syncthreads();
+  return r;
+}
+
+// inclusive block scan (fp64) -> returns exclusive prefix of this thread
+__device__ double block_exclusive_scan(double v, double* scratch, double* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  __syncthreads();
+  if (lane == 31) scratch[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    double w = lane < nw ? scratch[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < nw) scratch[lane] = w;
+  }
+  __syncthreads();
+  const double before = (wid ? scratch[wid - 1] : 0.0) + (x - v);
+  *total = scratch[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+template <int IN>
+__global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __restrict__ in, SampleDev a) {
+  __shared__ RowCtx rc;
+  __shared__ double dred[32];
+  __shared__ DI ared[32];
+  __shared__ unsigned long long s_u64[4];
+  __shared__ double hmass[256];
+  __shared__ unsigned int hcnt[256];
+  __shared__ int s_int[4];
+  const int row = blockIdx.x, tid = threadIdx.x;
+  if (row >= a.rows) return;
+  if (a.member_kind == SD_MEMBER_TREE && row >= a.tree[tree_off::T]) return;
+  if (tid == 0) row_setup(a, row, rc);
+  __syncthreads();
+  const int V = a.V;
+  const int64_t base = (int64_t)row * V;
+  auto sum_op = [](double x, double y) { return x + y; };
+  auto max_op = [](double x, double y) { return fmax(x, y); };
+
+  // ---- penalised softmax (or given probabilities) ----
+  double m = 0.0, Z = 1.0;
+  const bool is_probs = IN == SD_IN_PROBS_F64;
+  if (!is_probs) {
+    double lm = -INFINITY;
+    for (int v = tid; v < V; v += SMP_THREADS) lm = fmax(lm, scaled(load_in<IN>(in, base + v), is_member(a, rc, row, v), a));
+    m = block_reduce(lm, dred, max_op);
+    double lz = 0.0;
+    for (int v = tid; v < V; v += SMP_THREADS) lz += exp(scaled(load_in<IN>(in, base + v), is_member(a, rc, row, v), a) - m);
+    Z = block_reduce(lz, dred, sum_op);
+  }
+  auto prob = [&](int v) -> double {
+    if (is_probs) return load_in<IN>(in, base + v);
+    const double s = scaled(load_in<IN>(in, base + v), is_member(a, rc, row, v), a);
+    const double e = exp(s - m);
+    return e / Z;
+  };
+  if (a.probs_out)
+    for (int v = tid; v < V; v += SMP_THREADS) a.probs_out[base + v] = prob(v);
+  if (!a.trunc_out && !a.token_out) return;
+
+  // ---- truncation support: keep(v) ----
+  // kinds: none; min_p: p >= thr; eta: p >= thr (or argmax only); top_p: p > pstar or (p == pstar and v <= vcut)
+  double thr = -1.0;  // keep p >= thr
+  double pstar = -1.0;
+  int vcut = -1, only = -1;
+  const int tk = a.trunc_kind;
+  if (tk == SD_TRUNC_MIN_P || tk == SD_TRUNC_ETA || tk == SD_TRUNC_TOP_P) {
+    // pmax and argmax (lowest index)
+    DI best{-1.0, 0x7fffffff};
+    for (int v = tid; v < V; v += SMP_THREADS) best = better(best, DI{prob(v), v});
+    best = block_argmax(best, ared);
+    if (tk == SD_TRUNC_MIN_P) {
+      thr = a.trunc_value * best.v;
+    } else if (tk == SD_TRUNC_ETA) {
+      double le = 0.0;
+      for (int v = tid; v < V; v += SMP_THREADS) {
+        const double p = prob(v);
+        if (p > 0.0) le += p * log(p);
+      }
+      const double ent = -block_reduce(le, dred, sum_op);
+      const double alpha = a.eta_alpha < 0.0 ? sqrt(a.trunc_value) : a.eta_alpha;
+      const double eta = fmin(a.trunc_value, alpha * exp(-ent));
+      if (best.v < eta) only = best.i;  // nothing survives: keep the argmax
+      thr = eta;
+    } else {
+      // ---- top-p: radix descent over fp64 bit patterns with mass histograms ----
+      double total_l = 0.0;
+      for (int v = tid; v < V; v += SMP_THREADS) total_l += prob(v);
+      const double total = block_reduce(total_l, dred, sum_op);
+      if (a.trunc_value >= total) {
+        thr = -1.0;  // keep everything
+      } else {
+        unsigned long long prefix = 0, mask = 0;
+        double above = 0.0;
+        for (int shift = 56; shift >= 0; shift -= 8) {
+          for (int b = tid; b < 256; b += SMP_THREADS) {
+            hmass[b] = 0.0;
+            hcnt[b] = 0;
+          }
+          __syncthreads();
+          for (int v = tid; v < V; v += SMP_THREADS) {
+            const double p = prob(v);
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(p);
+            if ((bits & mask) == prefix) {
+              const int bkt = (int)((bits >> shift) & 255ull);
+              atomicAdd(&hmass[bkt], p);
+              atomicAdd(&hcnt[bkt], 1u);
+            }
+          }
+          __syncthreads();
+          if (tid == 0) {
+            int b = 255;
+            double acc = above;
+            int chosen = -1, lowest = -1;
+            for (; b >= 0; --b) {
+              if (hcnt[b] == 0) continue;
+              lowest = b;
+              if (acc + hmass[b] >= a.trunc_value) {
+                chosen = b;
+                break;
+              }
+              acc += hmass[b];
+            }
+            if (chosen < 0) {  // rounding: mass never reached; take the lowest bucket
+              chosen = lowest < 0 ? 0 : lowest;
+              acc -= lowest < 0 ? 0.0 : hmass[lowest];
+            }
+            s_u64[0] = prefix | ((unsigned long long)chosen << shift);
+            dred[0] = acc;
+          }
+          __syncthreads();
+          prefix = s_u64[0];
+          above = dred[0];
+          mask |= 255ull << shift;
+          __syncthreads();
+        }
+        pstar = __longlong_as_double((long long)prefix);
+        // number of elements equal to pstar needed, lowest indices first
+        unsigned int ceq_l = 0;
+        for (int v = tid; v < V; v += SMP_THREADS) ceq_l += prob(v) == pstar;
+        double ceq_d = block_reduce((double)ceq_l, dred, sum_op);
+        const int ceq = (int)ceq_d;
+        int need = (int)ceil((a.trunc_value - above) / pstar);
+        if (need < 1) need = 1;
+        if (need > ceq) need = ceq;
+        if (need >= ceq) {
+          vcut = V;  // all equal elements kept
+        } else {
+          // index of the need-th equal element: segment scan in index order
+          const int seg = (V + SMP_THREADS - 1) / SMP_THREADS;
+          const int b0 = tid * seg, b1 = min(V, b0 + seg);
+          double c = 0.0;
+          for (int v = b0; v < b1; ++v) c += prob(v) == pstar;
+          double tot;
+          const double before = block_exclusive_scan(c, dred, &tot);
+          if (tid == 0) s_int[0] = V;
+          __syncthreads();
+          if (before < need && before + c >= need) {
+            int k = (int)before;
+            for (int v = b0; v < b1; ++v) {
+              if (prob(v) == pstar && ++k == need) {
+                s_int[0] = v;
+                break;
+              }
+            }
+          }
+          __syncthreads();
+          vcut = s_int[0];
+        }
+      }
+    }
+  }
+  auto kept = [&](int v, double p) -> double {
+    if (tk == SD_TRUNC_NONE) return p;
+    if (only >= 0) return v == only ? p : 0.0;
+    if (tk == SD_TRUNC_TOP_P) {
+      if (pstar < 0.0) return p;
+      return (p > pstar || (p == pstar && v <= vcut)) ? p : 0.0;
+    }
+    return p >= thr ? p : 0.0;
+  };
+  double lk = 0.0;
+  for (int v = tid; v < V; v += SMP_THREADS) lk += kept(v, prob(v));
+  const double K = block_reduce(lk, dred, sum_op);
+  if (a.trunc_out)
+    for (int v = tid; v < V; v += SMP_THREADS) a.trunc_out[base + v] = kept(v, prob(v)) / K;
+  if (!a.token_out) return;
+  // ---- inverse CDF: first v with cumsum(kept / K) > u ----
+  const double u = uniform_at(a.seed, (uint64_t)rc.pos);
+  const int seg = (V + SMP_THREADS - 1) / SMP_THREADS;
+  const int b0 = tid * seg, b1 = min(V, b0 + seg);
+  double ssum = 0.0;
+  for (int v = b0; v < b1; ++v) ssum += kept(v, prob(v)) / K;
+  double tot;
+  const double before = block_exclusive_scan(ssum, dred, &tot);
+  if (tid == 0) s_int[1] = V;
+  __syncthreads();
+  if (b0 < b1 && before + ssum > u && before <= u) {
+    double c = before;
+    for (int v = b0; v < b1; ++v) {
+      c += kept(v, prob(v)) / K;
+      if (c > u) {
+        atomicMin(&s_int[1], v);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int idx = s_int[1];
+    if (idx > V - 1) idx = V - 1;
+    a.token_out[row] = idx;
+  }
+}
+
+// draft per-head top-w: one CTA per head; rank by exp(s - m) (the penalised
+// probability up to the shared 1/Z), ties to the lower id.
+__global__ void __launch_bounds__(SMP_THREADS) draft_topw_kernel(const float* __restrict__ logits, int V,
+                                                                 const int32_t* __restrict__ cnt, double t,
+                                                                 double theta, int ctrl, SampleDev a0, int off0,
+                                                                 int w0, int w1, int w2, int w3, int w4, int w5,
+                                                                 int w6, int w7, int32_t* __restrict__ out) {
+  __shared__ double dred[32];
+  __shared__ DI ared[32];
+  __shared__ int chosen[16];
+  const int head = blockIdx.x, tid = threadIdx.x;
+  const int ws[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
+  int off = 0;
+  for (int k = 0; k < head; ++k) off += ws[k];
+  const int w = ws[head];
+  const float* row = logits + (int64_t)head * V;
+  SampleDev a = a0;
+  a.temperature = t;
+  a.theta = theta;
+  a.ctrl_style = ctrl;
+  auto s_of = [&](int v) -> double {
+    const bool mem = cnt != nullptr && cnt[v] > 0;
+    return scaled((double)row[v], mem, a);
+  };
+  double lm = -INFINITY;
+  for (int v = tid; v < V; v += SMP_THREADS) lm = fmax(lm, s_of(v));
+  const double m = block_reduce(lm, dred, [](double x, double y) { return fmax(x, y); });
+  for (int j = 0; j < w; ++j) {
+    DI best{-1.0, 0x7fffffff};
+    for (int v = tid; v < V; v += SMP_THREADS) {
+      bool taken = false;
+      for (int i = 0; i < j; ++i) taken |= chosen[i] == v;
+      if (!taken) best = better(best, DI{exp(s_of(v) - m), v});
+    }
+    best = block_argmax(best, ared);
+    if (tid == 0) {
+      chosen[j] = best.i;
+      out[off + j] = best.i;
+    }
+    __syncthreads();
+  }
+  (void)off0;
+}
+
+static SampleDev to_dev(const sd_sample_args& h) {
+  SampleDev d;
+  d.rows = h.rows;
+  d.V = h.V;
+  d.in_kind = h.in_kind;
+  d.temperature = h.temperature;
+  d.theta = h.theta;
+  d.ctrl_style = h.ctrl_style;
+  d.member_kind = h.member_kind;
+  d.member_mask = h.member_mask;
+  d.win_count = h.win_count;
+  d.win_ring = h.win_ring;
+  d.state = h.state;
+  d.window = h.window;
+  d.tree = h.tree;
+  d.depth = h.depth;
+  d.trunc_kind = h.trunc_kind;
+  d.trunc_value = h.trunc_value;
+  d.eta_alpha = h.eta_alpha;
+  d.seed = h.seed;
+  d.positions = h.positions;
+  d.n = h.n;
+  d.probs_out = h.probs_out;
+  d.trunc_out = h.trunc_out;
+  d.token_out = h.token_out;
+  return d;
+}
+
+}  // namespace sd
+
+using namespace sd;
+
+extern "C" {
+
+int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t stream) {
+  SD_REQUIRE(args_host && args_host->rows > 0 && args_host->V > 0, "sd_sample_rows: sizes");
+  const sd_sample_args& h = *args_host;
+  SD_REQUIRE(h.temperature > 0.0 && h.theta >= 1.0, "sd_sample_rows: temperature/theta");
+  SD_REQUIRE(h.member_kind != SD_MEMBER_MASK || h.member_mask, "sd_sample_rows: mask");
+  SD_REQUIRE(h.member_kind < SD_MEMBER_WINDOW || h.window == 0 || (h.win_count && h.state),
+             "sd_sample_rows: window");
+  SD_REQUIRE(h.member_kind != SD_MEMBER_TREE || h.tree, "sd_sample_rows: tree");
+  SD_REQUIRE(h.positions || h.tree, "sd_sample_rows: need positions or tree");
+  SampleDev d = to_dev(h);
+  auto st = as_stream(stream);
+  switch (h.in_kind) {
+    case SD_IN_LOGITS_F32: sample_rows_kernel<SD_IN_LOGITS_F32><<<h.rows, SMP_THREADS, 0, st>>>(in, d); break;
+    case SD_IN_LOGITS_F64: sample_rows_kernel<SD_IN_LOGITS_F64><<<h.rows, SMP_THREADS, 0, st>>>(in, d); break;
+    case SD_IN_PROBS_F64: sample_rows_kernel<SD_IN_PROBS_F64><<<h.rows, SMP_THREADS, 0, st>>>(in, d); break;
+    default: SD_REQUIRE(false, "sd_sample_rows: in_kind");
+  }
+  return check_launch("sd_sample_rows");
+}
+
+int sd_draft_topw(const float* logits, int heads, int V, const int32_t* win_count, double temperature, double theta,
+                  int ctrl_style, const int32_t* widths_host, int32_t* out, sd_stream_t stream) {
+  SD_REQUIRE(heads > 0 && heads <= SD_TREE_MAX_DEPTH && V > 0, "sd_draft_topw: sizes");
+  int w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < heads; ++k) {
+    SD_REQUIRE(widths_host[k] >= 1 && widths_host[k] <= 16 && widths_host[k] <= V, "sd_draft_topw: width");
+    w[k] = widths_host[k];
+  }
+  SampleDev a{};
+  draft_topw_kernel<<<heads, SMP_THREADS, 0, as_stream(stream)>>>(logits, V, win_count, temperature, theta,
+                                                                  ctrl_style, a, 0, w[0], w[1], w[2], w[3], w[4],
+                                                                  w[5], w[6], w[7], out);
+  return check_launch("sd_draft_topw");
+}
+
+}  // extern "C"

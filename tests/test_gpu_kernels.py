@@ -1,0 +1,471 @@
+"""Per-kernel parity of the CUDA path against the CPU oracle (oracle/) and the
+reference's golden vectors. Integer outputs are compared bit-exactly; fp32
+paths at 1e-5 relative, bf16 paths at 1e-2 relative (north star tolerance)."""
+
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import engine as OE
+from oracle import kvcache as OK
+from oracle import model as OM
+from oracle import ngram as ON
+from oracle import sampling as OS
+from oracle import tree as OT
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+J = json.load(open(os.path.join(HERE, "golden.json")))
+A = np.load(os.path.join(HERE, "golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2502_18890_b200 import _lib
+    _lib.require_cuda()
+    return _lib
+
+
+def rope_np(x, pos, dh):
+    inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+    return OM.rope(x, pos, inv)
+
+
+def attend_oracle(q, K, V, vis):
+    """q [T, H, dh] (rotated, scaled); K, V [n, Hk, dh]; vis [T, n] bool."""
+    T, H, dh = q.shape
+    Hk = K.shape[1]
+    G = H // Hk
+    s = np.einsum("tkgd,nkd->tkgn", q.reshape(T, Hk, G, dh), K)
+    s = np.where(vis[:, None, None, :], s, -np.inf)
+    s = np.exp(s - s.max(-1, keepdims=True))
+    w = s / s.sum(-1, keepdims=True)
+    return np.einsum("tkgn,nkd->tkgd", w, V).reshape(T, H, dh)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("ctx,T,H,Hk,dh", [(0, 5, 4, 2, 8), (37, 12, 8, 2, 32), (700, 41, 32, 8, 128),
+                                            (3000, 101, 8, 8, 64), (5, 1, 4, 1, 16), (300, 3, 12, 2, 128)])
+def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
+    g = np.random.default_rng(ctx + T)
+    dev = torch.device("cuda")
+    cap = ctx + T + 3
+    K = g.normal(size=(Hk, cap, dh))
+    Vv = g.normal(size=(Hk, cap, dh))
+    q = g.normal(size=(T, H, dh)) / np.sqrt(dh)
+    # random tree over T rows (row 0 root)
+    parent = [-1] + [int(g.integers(0, i)) for i in range(1, T)]
+    mask = np.zeros((T, T), dtype=bool)
+    for i in range(T):
+        j = i
+        while j >= 0:
+            mask[i, j] = True
+            j = parent[j]
+    from paper_2502_18890_b200.model import mask_bits_from_bool
+    bits = torch.as_tensor(mask_bits_from_bool(mask), device=dev)
+    kt = torch.as_tensor(K, dtype=dtype, device=dev).contiguous()
+    vt = torch.as_tensor(Vv, dtype=dtype, device=dev).contiguous()
+    qt = torch.as_tensor(q, dtype=dtype, device=dev).contiguous()
+    out = torch.empty((T, H * dh), dtype=dtype, device=dev)
+    ws = torch.empty(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
+    kd = lib.dcode(dtype)
+    lib.call("sd_attention", lib.ptr(qt), kd, T, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
+             None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, lib.ptr(bits), lib.MASK_WORDS,
+             None, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+    # oracle on the same (rounded) inputs
+    Kr = kt.double().cpu().numpy().transpose(1, 0, 2)
+    Vr = vt.double().cpu().numpy().transpose(1, 0, 2)
+    qr = qt.double().cpu().numpy()
+    vis = np.zeros((T, ctx + T), dtype=bool)
+    vis[:, :ctx] = True
+    vis[:, ctx:] = mask
+    want = attend_oracle(qr, Kr[: ctx + T], Vr[: ctx + T], vis)
+    got = out.double().cpu().numpy().reshape(T, H, dh)
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    np.testing.assert_allclose(got, want, rtol=tol, atol=tol)
+
+
+def test_attention_rows_dev_padding(lib):
+    dev = torch.device("cuda")
+    T, Tl, H, Hk, dh, ctx = 16, 7, 8, 2, 64, 200
+    g = np.random.default_rng(3)
+    cap = ctx + T
+    kt = torch.as_tensor(g.normal(size=(Hk, cap, dh)), dtype=torch.float32, device=dev)
+    vt = torch.as_tensor(g.normal(size=(Hk, cap, dh)), dtype=torch.float32, device=dev)
+    qt = torch.as_tensor(g.normal(size=(T, H, dh)) * 0.1, dtype=torch.float32, device=dev)
+    rows = torch.tensor([Tl], dtype=torch.int32, device=dev)
+    outs = []
+    for rd in (rows, None):
+        TT = T if rd is not None else Tl
+        out = torch.full((TT, H * dh), 7.0, dtype=torch.float32, device=dev)
+        ws = torch.empty(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
+        lib.call("sd_attention", lib.ptr(qt), 0, TT, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), 0, cap * dh, ctx, None,
+                 None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, lib.ptr(rd),
+                 lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
+        outs.append(out)
+    assert torch.equal(outs[0][:Tl], outs[1])
+    assert torch.all(outs[0][Tl:] == 0)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_draft_attention_rank_rope_with_holes(lib, dtype):
+    dev = torch.device("cuda")
+    g = np.random.default_rng(11)
+    H, Hk, dh, cap = 8, 2, 32, 300
+    hi = 260
+    ranks = -np.ones(hi, dtype=np.int32)
+    live = np.sort(g.choice(hi, size=200, replace=False))
+    perm = g.permutation(len(live))
+    ranks[live] = perm  # arbitrary rank per live slot
+    Kraw = g.normal(size=(Hk, cap, dh))
+    V = g.normal(size=(Hk, cap, dh))
+    m = len(live)
+    from paper_2502_18890_b200 import ModelConfig, TinyTransformer
+    mdl = TinyTransformer(ModelConfig(vocab_size=16, hidden_dim=H * dh, num_heads=H, num_kv_heads=Hk,
+                                      max_positions=4096), dtype=dtype)
+    q_raw = g.normal(size=(1, H, dh))
+    k_self = g.normal(size=(1, Hk, dh))
+    v_self = g.normal(size=(1, Hk, dh))
+    q = rope_np(q_raw, [m], dh) / np.sqrt(dh)
+    ks = rope_np(k_self, [m], dh)
+    pk = torch.as_tensor(Kraw, dtype=dtype, device=dev)
+    pv = torch.as_tensor(V, dtype=dtype, device=dev)
+    rk = torch.as_tensor(ranks, device=dev)
+    qt = torch.as_tensor(q, dtype=dtype, device=dev)
+    kt = torch.as_tensor(ks.transpose(1, 0, 2), dtype=dtype, device=dev).contiguous()
+    vt = torch.as_tensor(v_self.transpose(1, 0, 2), dtype=dtype, device=dev).contiguous()
+    out = torch.empty((1, H * dh), dtype=dtype, device=dev)
+    mdl.attention(qt, 1, 1, pk, pv, cap * dh, hi, rk, kt, vt, dh, None, None, out)
+    # oracle: keys sorted by rank, rotated at rank
+    order = live[np.argsort(ranks[live])]
+    Kr = pk.double().cpu().numpy()[:, order].transpose(1, 0, 2)
+    Vr = pv.double().cpu().numpy()[:, order].transpose(1, 0, 2)
+    Krot = rope_np(Kr, np.arange(m), dh)
+    Kall = np.concatenate([Krot, kt.double().cpu().numpy().transpose(1, 0, 2)])
+    Vall = np.concatenate([Vr, vt.double().cpu().numpy().transpose(1, 0, 2)])
+    want = attend_oracle(qt.double().cpu().numpy(), Kall, Vall, np.ones((1, m + 1), dtype=bool))
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    np.testing.assert_allclose(out.double().cpu().numpy().reshape(1, H, dh), want, rtol=tol, atol=tol)
+
+
+def test_importance_scores_golden(lib):
+    from paper_2502_18890_b200 import importance_scores
+    for gs in J["imp_groups"]:
+        q, k = A[f"imp_q{gs}"], A[f"imp_k{gs}"]
+        # dh = 5 is not a supported head size: pad to 8 with zeros (score unchanged)
+        qp = np.zeros((q.shape[0], 8))
+        qp[:, :5] = q
+        kp = np.zeros(k.shape[:2] + (8,))
+        kp[..., :5] = k
+        got = importance_scores(qp, kp, gs).cpu().numpy()
+        np.testing.assert_allclose(got, A[f"imp_s{gs}"], rtol=1e-5, atol=1e-5)
+
+
+@pytest.mark.parametrize("trial", range(10))
+def test_select_topk_golden(lib, trial):
+    """Exact reference order (-score, pos) including ties (kvcache.py:286)."""
+    c = J["select"][trial]
+    sc = torch.as_tensor(A[f"sel{trial}_scores"], dtype=torch.float32, device="cuda").contiguous()
+    Lr, n = sc.shape[0], c["n"]
+    take = c["budget"] - c["sink"]
+    cap = c["budget"] + 8
+    ppos = torch.full((Lr, cap), -1, dtype=torch.int32, device="cuda")
+    prank = torch.full_like(ppos, -1)
+    psc = torch.zeros((Lr, cap), dtype=torch.float32, device="cuda")
+    ws = torch.empty(lib.load().sd_select_workspace_bytes(Lr, n - c["sink"]), dtype=torch.uint8, device="cuda")
+    lib.call("sd_select_topk", lib.ptr(sc), Lr, n - c["sink"], c["sink"], take, lib.ptr(ppos), lib.ptr(prank),
+             lib.ptr(psc), cap, lib.ptr(ws), ws.numel(), lib.stream())
+    got = ppos[:, : c["budget"]].cpu().tolist()
+    assert got == c["positions"]
+    # ranks = position order among selected
+    for l in range(Lr):
+        pos = got[l]
+        want_rank = np.argsort(np.argsort(pos)).tolist()
+        assert prank[l, : c["budget"]].cpu().tolist() == want_rank
+
+
+def test_select_topk_large_random(lib):
+    g = np.random.default_rng(5)
+    Lr, n, sink, take = 3, 20000, 16, 4000
+    sc = np.round(g.normal(size=(Lr, n)), 2).astype(np.float32)  # many ties
+    t = torch.as_tensor(sc, device="cuda")
+    cap = sink + take + 8
+    ppos = torch.full((Lr, cap), -1, dtype=torch.int32, device="cuda")
+    prank = torch.full_like(ppos, -1)
+    psc = torch.zeros((Lr, cap), dtype=torch.float32, device="cuda")
+    ws = torch.empty(lib.load().sd_select_workspace_bytes(Lr, n), dtype=torch.uint8, device="cuda")
+    lib.call("sd_select_topk", lib.ptr(t), Lr, n, sink, take, lib.ptr(ppos), lib.ptr(prank), lib.ptr(psc), cap,
+             lib.ptr(ws), ws.numel(), lib.stream())
+    for l in range(Lr):
+        want = list(range(sink)) + OK.select_body(sc[l].astype(np.float64), sink, sink + n, take)
+        assert ppos[l, : sink + take].cpu().tolist() == want
+
+
+def _partial_case(L_, n, sink, budget):
+    from paper_2502_18890_b200 import FullCache
+    g = np.random.default_rng(n)
+    full = FullCache(L_, 1, 8, capacity=n + 16, dtype=torch.float32)
+    kr = g.normal(size=(L_, 1, n, 8))
+    full.k_raw[:, :, :n] = torch.as_tensor(kr, dtype=torch.float32)
+    full.v[:, :, :n] = torch.arange(n, dtype=torch.float32).view(1, 1, n, 1).expand(L_, 1, n, 8)
+    full.positions = list(range(n))
+    ofull = OK.FullCache(L_, 1, 8, cap=n + 16)
+    ofull.k_raw[:, :n] = kr.transpose(0, 2, 1, 3)
+    ofull.v[:, :n] = np.arange(n, dtype=np.float64)[None, :, None, None]
+    ofull.positions = list(range(n))
+    return full, ofull
+
+
+def test_partial_admit_evict_matches_reference_semantics(lib):
+    """test_kvcache.py:152-160 plus a long random admit/evict/refresh sequence."""
+    from paper_2502_18890_b200 import kvcache as K
+    full, ofull = _partial_case(1, 8, 2, 5)
+    part = K.mirror_partial(full, 2, 5, upto=5)
+    op = OK.mirror_partial(ofull, 2, 5, upto=5)
+    assert part.positions == op.positions == [[0, 1, 4, 3, 2]]
+    part.admit([5, 6], full)
+    part.evict(protected=2)
+    assert part.positions == [[0, 1, 5, 6, 4]]
+    # long run against the oracle, two layers
+    Lr, n = 2, 400
+    full, ofull = _partial_case(Lr, n, 4, 24)
+    part = K.mirror_partial(full, 4, 24, upto=10)
+    op = OK.mirror_partial(ofull, 4, 24, upto=10)
+    g = np.random.default_rng(9)
+    cur = 10
+    while cur < n - 8:
+        if g.random() < 0.1 and cur >= 24:
+            sc = np.round(g.normal(size=(Lr, cur - 4)), 1)
+            part.build_topk(full, torch.as_tensor(sc, dtype=torch.float32, device="cuda"), cur)
+            op = OK.prefill_partial(ofull, 4, 24, sc, upto=cur)
+        a = int(g.integers(1, 5))
+        part.admit_evict(cur, a, full, protected=a)
+        op.admit(list(range(cur, cur + a)), ofull)
+        OK.evict_to_budget(op, protected=a)
+        cur += a
+        assert part.positions == op.positions
+        # ranks are the position order of live slots; data follows slots
+        rk = part.ranks()
+        pos = part.ppos.cpu().numpy()
+        for l in range(Lr):
+            live = [s for s in range(part.hi) if pos[l, s] >= 0]
+            want = np.argsort(np.argsort([pos[l, s] for s in live]))
+            assert [int(rk[l, s]) for s in live] == want.tolist()
+            vals = part.pv[l, 0, live, 0].cpu().numpy()
+            assert np.array_equal(vals, pos[l, live].astype(np.float32))
+
+
+def test_reconcile_and_qsum(lib):
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200 import _lib as Lb
+    full = FullCache(2, 2, 8, capacity=64, dtype=torch.float32)
+    for arr in (full.k_raw, full.k_rot, full.v):
+        arr.copy_(torch.arange(arr.numel(), dtype=torch.float32, device="cuda").view(arr.shape))
+    before = [t.clone() for t in (full.k_raw, full.k_rot, full.v)]
+    base, keep = 10, [0, 2, 3, 7]
+    res = torch.full((32,), -1, dtype=torch.int32)
+    res[Lb.RES_ACCEPTED] = 4
+    res[Lb.RES_KEEP:Lb.RES_KEEP + 4] = torch.tensor(keep)
+    q_pre = torch.randn((2, 12, 4, 8), device="cuda")
+    q_sum = torch.zeros((2, 4, 8), device="cuda")
+    full.reconcile_device(base, res.cuda(), q_pre, 12, 4, q_sum)
+    for b, t in zip(before, (full.k_raw, full.k_rot, full.v)):
+        for i, k in enumerate(keep):
+            assert torch.equal(t[:, :, base + i], b[:, :, base + k])
+    want = sum(q_pre[:, k] for k in keep)
+    torch.testing.assert_close(q_sum, want, rtol=1e-6, atol=1e-6)
+
+
+@pytest.mark.parametrize("trial", range(24))
+def test_sampler_golden(lib, trial):
+    from paper_2502_18890_b200 import sampling as S
+    case = J["sampling"][trial]
+    logits, members = A[f"samp{trial}_logits"], A[f"samp{trial}_members"]
+    cfg = S.SamplerConfig(temperature=case["t"], theta=case["theta"], window=64, ctrl_style=case["ctrl"])
+    probs = S.penalized_probs_masked(logits, members, cfg).cpu().numpy()
+    np.testing.assert_allclose(probs, A[f"samp{trial}_probs"], rtol=1e-12, atol=1e-300)
+    rules = [S.Truncation.min_p(0.1), S.Truncation.top_p(0.9), S.Truncation.eta(0.02),
+             S.Truncation.top_p(0.5), S.Truncation.min_p(0.5)]
+    for ri, rule in enumerate(rules):
+        d = S.truncate(A[f"samp{trial}_probs"], rule).cpu().numpy()
+        np.testing.assert_allclose(d, A[f"samp{trial}_trunc{ri}"], rtol=1e-12, atol=1e-300)
+        got = [S.sample_at(A[f"samp{trial}_trunc{ri}"], pos, seed) for pos, seed in [(0, 0), (5, 1), (777, 3), (4096, 0)]]
+        assert got == case["draws"][str(ri)]
+
+
+def test_sampler_known_answers(lib):
+    """test_sampling.py:128-213 restated against the device sampler."""
+    from paper_2502_18890_b200 import sampling as S
+    from paper_2502_18890_b200.rng import uniform_at
+    assert np.allclose(S.truncate(np.array([0.5, 0.3, 0.2]), S.Truncation.top_p(1.0)).cpu().numpy(), [0.5, 0.3, 0.2])
+    out = S.truncate(np.array([0.5, 0.04, 0.46]), S.Truncation.min_p(0.1)).cpu().numpy()
+    assert out[1] == 0.0
+    out = S.truncate(np.full(4, 0.25), S.Truncation.top_p(0.5)).cpu().numpy()
+    assert np.count_nonzero(out) == 2 and np.allclose(out[out > 0], 0.5)
+    out = S.truncate(np.full(4096, 1 / 4096), S.Truncation.eta(2e-4)).cpu().numpy()
+    assert np.count_nonzero(out) >= 1 and abs(out.sum() - 1) < 1e-9
+    d = np.array([0.3, 0.7])
+    for seed in range(200):
+        assert S.sample_at(d, 0, seed) == (0 if uniform_at(seed, 0) < 0.3 else 1)
+    pm = np.zeros(16)
+    pm[7] = 1.0
+    assert all(S.sample_at(pm, p, s) == 7 for p in range(3) for s in range(3))
+
+
+def test_verify_sampler_tree_rows_match_oracle_node_masks(lib):
+    """Fused per-row window splice (engine.py:155-181) == oracle node_masks."""
+    from paper_2502_18890_b200 import _lib as Lb
+    from paper_2502_18890_b200.sampling import PenaltyWindow
+    g = np.random.default_rng(21)
+    V, W, depth = 64, 12, 4
+    for trial in range(6):
+        hist = g.integers(0, V, size=int(g.integers(0, 30))).tolist()
+        ow = OS.PenaltyWindow(W, V)
+        st = torch.zeros(16, dtype=torch.int64, device="cuda")
+        dw = PenaltyWindow(W, V, state=st)
+        for t in hist:
+            ow.push(t)
+        dw.push_many(hist)
+        per_head = [[int(x) for x in g.choice(V, w, replace=False)] for w in (1, 3, 3, 3)]
+        grams = [tuple([per_head[0][0]] + g.integers(0, V, size=3).tolist()) for _ in range(3)]
+        tree = OT.build_tree(per_head, grams)
+        masks = OS.node_masks(ow, tree.tokens, tree.parent, depth)
+        T = 1 + len(tree)
+        logits = g.normal(scale=2.0, size=(T, V))
+        smp = OS.SamplerConfig(temperature=0.9, theta=1.3, window=W, truncation=OS.Truncation.top_p(0.8), seed=trial)
+        n = 50 + trial
+        want = []
+        dists = OS.penalized_probs_masked(logits, masks, smp)
+        for r in range(T):
+            pos = n if r == 0 else n + tree.depth[r - 1] + 1
+            want.append(OS.sample_at(OS.truncate(dists[r], smp.truncation), pos, smp.seed))
+        # device: tree record + fused sampler
+        rec = torch.zeros(Lb.tree_layout()["TOTAL"], dtype=torch.int32, device="cuda")
+        flat = torch.tensor([t for c in per_head for t in c], dtype=torch.int32, device="cuda")
+        gm = torch.tensor(grams, dtype=torch.int32, device="cuda").reshape(-1)
+        Lb.call("sd_tree_build", Lb.ptr(flat), Lb.host_i32([1, 3, 3, 3]), 4, Lb.ptr(gm), None, len(grams), None, n - 1,
+                Lb.ptr(rec), Lb.stream())
+        lt = torch.as_tensor(logits, dtype=torch.float64, device="cuda")
+        y = torch.full((T,), -1, dtype=torch.int32, device="cuda")
+        probs = torch.empty((T, V), dtype=torch.float64, device="cuda")
+        a = Lb.SampleArgs()
+        a.rows, a.V, a.in_kind = T, V, Lb.IN_LOGITS_F64
+        a.temperature, a.theta, a.ctrl_style = 0.9, 1.3, 0
+        a.member_kind = Lb.MEMBER_TREE
+        a.win_count, a.win_ring, a.state, a.window = Lb.ptr(dw.count), Lb.ptr(dw.ring), Lb.ptr(st), W
+        a.tree, a.depth = Lb.ptr(rec), depth
+        a.trunc_kind, a.trunc_value, a.eta_alpha = Lb.TRUNC_TOP_P, 0.8, -1.0
+        a.seed, a.n = trial, n
+        a.probs_out, a.token_out = Lb.ptr(probs), Lb.ptr(y)
+        Lb.call("sd_sample_rows", Lb.ptr(lt), a, Lb.stream())
+        np.testing.assert_allclose(probs.cpu().numpy(), dists, rtol=1e-12, atol=1e-300)
+        assert y.cpu().tolist() == want
+
+
+def test_draft_topw_matches_stable_argsort(lib):
+    g = np.random.default_rng(2)
+    V = 5000
+    logits = g.normal(scale=3, size=(4, V)).astype(np.float32)
+    logits[1, 17] = logits[1, 4000] = logits[1].max() + 1  # exact tie -> lower id first
+    cnt = np.zeros(V, dtype=np.int32)
+    cnt[g.integers(0, V, size=300)] = 1
+    smp = OS.SamplerConfig(temperature=1.0, theta=1.2, window=64)
+    probs = OS.penalized_probs_masked(logits.astype(np.float64), np.broadcast_to(cnt > 0, (4, V)), smp)
+    widths = [1, 3, 3, 3]
+    want = [int(t) for k in range(4) for t in np.argsort(-probs[k], kind="stable")[: widths[k]]]
+    from paper_2502_18890_b200 import _lib as Lb
+    out = torch.empty(10, dtype=torch.int32, device="cuda")
+    lt = torch.as_tensor(logits, device="cuda")
+    ct = torch.as_tensor(cnt, device="cuda")
+    Lb.call("sd_draft_topw", Lb.ptr(lt), 4, V, Lb.ptr(ct), 1.0, 1.2, 0, Lb.host_i32(widths), Lb.ptr(out), Lb.stream())
+    assert out.cpu().tolist() == want
+
+
+@pytest.mark.parametrize("trial", range(6))
+def test_ngram_golden(lib, trial):
+    from paper_2502_18890_b200 import NGramTable
+    c = J["ngram"][trial]
+    tab = NGramTable(n=c["n"], k_max=64, capacity=8192, vocab_size=64)
+    seq = []
+    for chunk in c["ops"]:
+        tab.update(chunk, seq[-(c["n"] - 1):] if c["n"] > 1 else [])
+        seq.extend(chunk)
+    assert len(tab) == c["size"]
+    for f, want in c["retrieve"].items():
+        assert [list(g) for g in tab.retrieve(int(f), 20)] == want
+    for g, fr in c["freqs"]:
+        assert tab.frequency(tuple(g)) == fr
+
+
+def test_ngram_known_answers(lib):
+    """test_ngram.py:19-98 restated."""
+    from paper_2502_18890_b200 import NGramTable
+    t = NGramTable(n=4, vocab_size=64)
+    t.update([9], history_tail=[1, 2, 3])
+    assert len(t) == 1 and t.frequency((1, 2, 3, 9)) == 1
+    t = NGramTable(n=2, vocab_size=64)
+    t.update([0, 1, 0, 1, 0, 1], history_tail=[])
+    assert t.frequency((0, 1)) == 3 and t.frequency((1, 0)) == 2
+    t = NGramTable(n=2, vocab_size=64)
+    t.update([1, 2], [])
+    t.update([1, 3], [])
+    assert t.retrieve(1, 2) == [(1, 3), (1, 2)]
+    t.update([1, 2], [])
+    assert t.retrieve(1, 2) == [(1, 2), (1, 3)]
+    with pytest.raises(ValueError):
+        NGramTable(n=4, k_max=8, vocab_size=64).retrieve(0, 9)
+    assert NGramTable(n=4, vocab_size=64).retrieve(0, 5) == []
+
+
+@pytest.mark.parametrize("trial", range(40))
+def test_tree_golden(lib, trial):
+    from paper_2502_18890_b200 import TreeConfig, build_tree
+    c = J["trees"][trial]
+    t = build_tree(c["heads"], [tuple(g) for g in c["grams"]], TreeConfig(tuple(c["widths"])))
+    assert t.tokens == c["tokens"]
+    assert t.parent == c["parent"]
+    assert t.depth == c["depth"]
+    assert t.head_node_count == c["head_node_count"]
+    assert [[list(p.tokens), list(p.nodes), p.origin, p.origin_index] for p in t.paths] == c["paths"]
+    assert [np.nonzero(r)[0].tolist() for r in t.mask] == c["mask"]
+
+
+def test_accept_commit_matches_oracle(lib):
+    from paper_2502_18890_b200 import _lib as Lb
+    g = np.random.default_rng(4)
+    V, depth = 40, 4
+    for trial in range(60):
+        per_head = [[int(x) for x in g.choice(V, w, replace=False)] for w in (1, 3, 3, 3)]
+        grams = [tuple([per_head[0][0]] + g.integers(0, V, size=3).tolist()) for _ in range(int(g.integers(0, 5)))]
+        tree = OT.build_tree(per_head, grams)
+        T = 1 + len(tree)
+        # y biased to match the tree tokens so long paths occur
+        y = g.integers(0, V, size=T)
+        for r in range(T):
+            kids = [i for i in range(len(tree)) if tree.parent[i] == r - 1]
+            if kids and g.random() < 0.7:
+                y[r] = tree.tokens[kids[int(g.integers(0, len(kids)))]]
+        seed = int(g.integers(0, 1 << 62))
+        n = int(g.integers(10, 1000))
+        bonus = bool(trial % 5)
+        pick, best_v, acc, ys, keep = OE.accept_paths(tree, y, seed, n, depth, bonus)
+        rec = torch.zeros(Lb.tree_layout()["TOTAL"], dtype=torch.int32, device="cuda")
+        flat = torch.tensor([t for c in per_head for t in c], dtype=torch.int32, device="cuda")
+        gm = torch.tensor(grams if grams else [[0] * 4], dtype=torch.int32, device="cuda").reshape(-1)
+        Lb.call("sd_tree_build", Lb.ptr(flat), Lb.host_i32([1, 3, 3, 3]), 4, Lb.ptr(gm), None, len(grams), None,
+                n - 1, Lb.ptr(rec), Lb.stream())
+        yt = torch.as_tensor(y.astype(np.int32), device="cuda")
+        st = torch.zeros(16, dtype=torch.int64, device="cuda")
+        res = torch.zeros(32, dtype=torch.int32, device="cuda")
+        hist = torch.zeros(64, dtype=torch.int32, device="cuda")
+        Lb.call("sd_accept_commit", Lb.ptr(rec), Lb.ptr(yt), seed, n, depth, int(bonus), Lb.ptr(st), None, None, 0,
+                Lb.ptr(hist), None, Lb.ptr(res), Lb.stream())
+        r = res.cpu().tolist()
+        assert (r[Lb.RES_PICK], r[Lb.RES_BEST], r[Lb.RES_ACCEPTED]) == (pick, best_v, acc)
+        assert r[Lb.RES_YS:Lb.RES_YS + acc] == ys
+        assert r[Lb.RES_KEEP:Lb.RES_KEEP + acc] == keep
+        assert r[Lb.RES_PENDING] == ys[-1]
