@@ -1,0 +1,295 @@
+"""Decode-step benchmark (driver contract; see README / DESIGN.md §Measurement).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg3] [--ctx C]
+
+A step is one TokenSwift decode iteration (Session.step: draft forward over
+the partial cache, n-gram tree, verification forward over the full cache,
+sampling, acceptance, cache maintenance) of LLaMA3.1-8B-shaped random-init
+weights (cfg3 of BASELINE.json) at a fixed point of a 100K-token generation
+from a 4096-token prefix. Time per step is linear in the context length, so
+the default point, the run's mean context (4096 + 100000/2), gives the
+run-average tokens/s. The prefix is prefilled for real; the committed
+context beyond it is synthetic (random K/V, `data: synthetic`).
+
+Rank 0 prints one JSON line. --impl reference times the reference algorithm's
+CPU path (the oracle port; swiftdec is pure numpy, nothing to compile) on the
+host cores on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: model dims, engine, sampler (Table 9 / SURVEY.md §8d)
+    "cfg1": dict(V=32000, d=256, L=2, H=8, Hk=2, prefix=512, gen=2000, B=512, S=32, trunc=("min_p", 1.0), theta=1.2),
+    "cfg2": dict(V=151936, d=1536, L=28, H=12, Hk=2, prefix=2048, gen=20000, B=2048, S=32, trunc=("top_p", 0.9),
+                 theta=1.15),
+    "cfg3": dict(V=128256, d=4096, L=32, H=32, Hk=8, prefix=4096, gen=100000, B=4096, S=32, trunc=("min_p", 0.1),
+                 theta=1.2),
+    "cfg4": dict(V=32000, d=4096, L=32, H=32, Hk=32, prefix=4096, gen=100000, B=4096, S=32, trunc=("top_p", 0.9),
+                 theta=1.15),
+    "cfg5": dict(V=152064, d=5120, L=48, H=40, Hk=8, prefix=4096, gen=100000, B=4096, S=32, trunc=("min_p", 0.05),
+                 theta=1.13),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg3", choices=sorted(CONFIGS))
+    ap.add_argument("--ctx", type=int, default=None, help="committed context at the timed steps")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--attn-reps", type=int, default=3)
+    return ap.parse_args()
+
+
+def workload_name(cfg_name, c, ctx):
+    return (f"{cfg_name}: TokenSwift decode step, random-init {c['L']}L d={c['d']} H={c['H']} Hk={c['Hk']} "
+            f"V={c['V']} (reference arch), tree [1,3,3,3] + k=20 n-grams, partial budget {c['B']} sink {c['S']}, "
+            f"prefix {c['prefix']} prefilled, generation of {c['gen']} at mean context ctx={ctx}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in getattr(self, "lines", []):
+            f = [x.strip() for x in l.split(",")]
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except (ValueError, IndexError):
+                continue
+            for i, n in enumerate(names):
+                if len(f) > 5 + i and f[5 + i].lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def cpu_baseline_line(c, ctx, accepted, tree_rows):
+    from oracle.cpu_baseline import compose_step, host_cores
+    per_step, tps, parts = compose_step(c["d"], c["L"], c["H"], c["Hk"], c["V"], ctx, c["B"], tree_rows=tree_rows,
+                                        accepted=accepted)
+    return {"value": tps, "unit": "tokens/s", "cores": host_cores(), "kind": "port",
+            "sample": (f"oracle (numpy fp64) pieces at full shape, composed: {c['L']} x (1 verify layer, "
+                       f"{tree_rows} rows over ctx {ctx} + 1 draft layer over {c['B']}) + LM head (1/16 vocab "
+                       f"slice x16) + sampling {tree_rows}x{c['V']} + tree/n-gram/accept; "
+                       f"{accepted:.2f} tokens/step; {per_step:.1f} s/step"),
+            "parts_s": {k: round(v, 4) for k, v in parts.items()}}
+
+
+def run_reference(args, c, ctx):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    steps, warm = max(1, min(args.steps, 2)), 0
+    vals = []
+    for _ in range(steps):
+        line = cpu_baseline_line(c, ctx, accepted=4.0, tree_rows=41)
+        vals.append(line["value"])
+    v = statistics.median(vals)
+    out = {"metric": "generated tokens/s (TokenSwift decode, LLaMA3.1-8B shape)", "value": v, "unit": "tokens/s",
+           "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
+           "ms_per_step": 4000.0 / v if v else None, "higher_is_better": True, "scaling": "strong",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": workload_name(args.config, c, ctx), "ctx": ctx},
+           "cpu_baseline": {**line, "value": v},
+           "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    c = CONFIGS[args.config]
+    ctx = args.ctx if args.ctx is not None else c["prefix"] + c["gen"] // 2
+    if args.impl == "reference":
+        run_reference(args, c, ctx)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2502_18890_b200 as sd
+    from paper_2502_18890_b200 import _lib
+    from paper_2502_18890_b200.parallel import init_from_env
+
+    rank, world, local = init_from_env("nccl")
+    torch.cuda.set_device(local)
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {world}")
+    maxpos = c["prefix"] + c["gen"] + 256
+    mcfg = sd.ModelConfig(vocab_size=c["V"], num_layers=c["L"], hidden_dim=c["d"], num_heads=c["H"],
+                          num_kv_heads=c["Hk"], gamma=3, max_positions=maxpos, init_seed=0)
+    model = sd.TinyTransformer(mcfg, dtype=torch.bfloat16, init="device", shard=(rank, world),
+                               group=None)
+    trunc = sd.Truncation(*c["trunc"])
+    ecfg = sd.EngineConfig(target_length=c["gen"], sink_size=c["S"], budget=c["B"], tree=sd.TreeConfig((1, 3, 3, 3)),
+                           k=20, sampler=sd.SamplerConfig(theta=c["theta"], window=1024, truncation=trunc))
+    prompt = sd.rng.random_prompt(c["prefix"], c["V"])
+    t0 = time.perf_counter()
+    sess = sd.Session(model, prompt, ecfg, capacity=c["prefix"] + c["gen"] + 512)
+    prefill_s = time.perf_counter() - t0
+    if ctx > c["prefix"]:
+        sess.set_synthetic_context(ctx)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        sess.step()
+    # ---- timed region: device time (events on the launching stream), max over ranks ----
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = len(sess.records)
+    l0 = _lib.launch_count
+    with ClockSampler(local) as clk:
+        torch.cuda.nvtx.range_push("timed")
+        w0 = time.perf_counter()
+        e0.record(st)
+        for _ in range(args.steps):
+            sess.step()  # public API: includes the per-step D2H of the step result
+        e1.record(st)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - w0
+        torch.cuda.nvtx.range_pop()
+    if world > 1:
+        dist.barrier()
+    launches = _lib.launch_count - l0
+    recs = sess.records[n0:]
+    tokens = sum(r.accepted for r in recs)
+    dev_s = e0.elapsed_time(e1) / 1e3
+    t = torch.tensor([dev_s, wall], device="cuda", dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_s, wall = float(t[0]), float(t[1])
+    # ---- dominant kernel: verification attention, timed alone per layer ----
+    rows = max(1, round(statistics.mean(r.verify_rows for r in recs)))
+    hbm, tflops, peak_kind = measured_peaks()
+    attn = time_verify_attention(sess, model, rows, ctx, reps=args.attn_reps)
+    dh, Hk, H = model.dh, model.Hk, model.H
+    alg_bytes = 2 * ctx * Hk * dh * 2 + 2 * rows * H * dh * 2 + 2 * rows * Hk * dh * 2
+    alg_flops = 4 * rows * H * dh * ctx
+    achieved = alg_bytes / attn["avg_s"] / 1e9
+    bound = "hbm" if (alg_flops / (tflops * 1e12)) < (alg_bytes / (hbm * 1e9)) else "tensor"
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+        return
+    clocks = clk.summary()
+    out = {
+        "metric": "generated tokens/s (TokenSwift decode, LLaMA3.1-8B shape)",
+        "value": tokens / dev_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights; random prompt prefilled; synthetic KV beyond the prefix)",
+        "config": {"workload": workload_name(args.config, c, ctx), "ctx": ctx, "global_batch": 1,
+                   "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (12.4 GB weights + KV per step)"},
+        "e2e": {"value": tokens / wall, "unit": "tokens/s", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 128,
+                "note": "Session.step() wall clock incl. per-step result D2H"},
+        "gpu_launches": launches,
+        "roofline": {"bound": bound, "achieved": achieved if bound == "hbm" else alg_flops / attn["avg_s"] / 1e12,
+                     "peak": hbm if bound == "hbm" else tflops, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+                     "frac": (achieved / hbm) if bound == "hbm" else (alg_flops / attn["avg_s"] / 1e12) / tflops,
+                     "traffic": None, "kernel": "sd_attention verify (split-KV + merge), one layer",
+                     "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes, "alg_flops_per_launch": alg_flops,
+                     "avg_launch_us": attn["avg_s"] * 1e6, "rows": rows,
+                     "share_of_step": attn["avg_s"] * model.config.num_layers / (dev_s / args.steps)},
+        "clocks": clocks,
+        "alpha": statistics.mean(r.accepted for r in recs) / 4.0,
+        "mean_verify_rows": statistics.mean(r.verify_rows for r in recs),
+        "iterations_per_s": args.steps / dev_s, "prefill_s": prefill_s,
+        "refreshes": sum(r.refreshed for r in recs),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        mean_acc = tokens / max(1, len(recs))
+        out["cpu_baseline"] = cpu_baseline_line(c, ctx, accepted=mean_acc, tree_rows=rows)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+
+
+def time_verify_attention(sess, model, rows, ctx, reps=3):
+    """CUDA-event time of the verification attention alone, one launch per
+    layer (each layer's K/V is a distinct >L2 buffer), on the launching stream."""
+    import torch
+    F = sess.full
+    T = rows
+    q = torch.randn((T, model.H, model.dh), device="cuda").mul_(0.1).to(model.dtype)
+    out = torch.empty((T, model.H * model.dh), dtype=model.dtype, device="cuda")
+    from paper_2502_18890_b200.model import mask_bits_from_bool
+    import numpy as np
+    m = np.tril(np.ones((T, T), dtype=bool))
+    bits = torch.as_tensor(mask_bits_from_bool(m), device="cuda")
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    base = min(ctx, len(F))
+    for l in range(model.config.num_layers):  # warm
+        model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
+                        F.v[l, :, base:], F.head_stride, bits, None, out)
+    torch.cuda.synchronize()
+    n = 0
+    e0.record(st)
+    for _ in range(reps):
+        for l in range(model.config.num_layers):
+            model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
+                            F.v[l, :, base:], F.head_stride, bits, None, out)
+            n += 1
+    e1.record(st)
+    torch.cuda.synchronize()
+    return {"avg_s": e0.elapsed_time(e1) / 1e3 / n, "launches": n}
+
+
+if __name__ == "__main__":
+    main()

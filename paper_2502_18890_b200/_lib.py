@@ -111,7 +111,17 @@ def require_cuda():
         raise LibraryError("paper_2502_18890_b200 needs a CUDA device (sm_100a); no CPU fallback exists")
 
 
+# kernels launched per successful entry-point call (for the bench's gpu_launches)
+_LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}
+_NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
+              "sd_ngram_bytes", "sd_tree_layout"}
+launch_count = 0
+
+
 def call(name: str, *args):
+    global launch_count
+    if name not in _NO_LAUNCH:
+        launch_count += _LAUNCHES.get(name, 1)
     rc = getattr(load(), name)(*args)
     if rc != 0:
         msg = load().sd_last_error().decode(errors="replace")

@@ -76,7 +76,8 @@ __device__ __forceinline__ void stage_tile(float* Ks, float* Vs, const KT* __res
       a = to_f(K[row * DH + 2 * e]);
       b = to_f(K[row * DH + 2 * e + 1]);
       if (ROT) {
-        const int64_t r = ranks[row];
+        int64_t r = ranks[row];
+        if (r < 0) r = 0;  // hole slot: masked out by slot_valid_bits, keep the table read in bounds
         const float c = cosT[r * HALF + e], s = sinT[r * HALF + e];
         const float ra = a * c - b * s, rb = a * s + b * c;
         a = ra;

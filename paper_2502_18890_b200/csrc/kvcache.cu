@@ -70,6 +70,7 @@ __device__ __forceinline__ uint32_t ord_f32(float f) {
 }
 // larger key = better: higher score first, then lower position
 __device__ __forceinline__ uint64_t sel_key(float score, int pos) {
+  if (score == 0.0f) score = 0.0f;  // -0.0 ties with +0.0, as in the reference's comparison
   return ((uint64_t)ord_f32(score) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)pos);
 }
 
