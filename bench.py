@@ -277,14 +277,14 @@ def time_verify_attention(sess, model, rows, ctx, reps=3):
     base = min(ctx, len(F))
     for l in range(model.config.num_layers):  # warm
         model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                        F.v[l, :, base:], F.head_stride, bits, None, out)
+                        F.v[l, :, base:], F.head_stride, bits, None, out, F.tmaps, l)
     torch.cuda.synchronize()
     n = 0
     e0.record(st)
     for _ in range(reps):
         for l in range(model.config.num_layers):
             model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                            F.v[l, :, base:], F.head_stride, bits, None, out)
+                            F.v[l, :, base:], F.head_stride, bits, None, out, F.tmaps, l)
             n += 1
     e1.record(st)
     torch.cuda.synchronize()

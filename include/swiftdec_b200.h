@@ -96,7 +96,14 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
                  int ctx, const int32_t* ranks, const float* rope_cos, const float* rope_sin,
                  const void* k_tree, const void* v_tree, int64_t tree_head_stride,
                  const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
+                 const void* tmap_k_host, const void* tmap_v_host, int layer,
                  void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
+/* 128-byte TMA descriptor (CUtensorMap) over a whole [L][Hk][cap][128] bf16
+ * cache array. When sd_attention gets descriptors for K_rot and V (and the
+ * call is bf16 / head_dim 128 / src_kind 0), the cache chunks run on the
+ * tcgen05 tensor-core kernel (TMA-fed, accumulators in TMEM) of `layer`;
+ * k_cache / v_cache must then be that layer's slice of the described arrays. */
+int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host);
 
 /* ---- Eq. 2 importance (kvcache.py:243-265) ----
  * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),

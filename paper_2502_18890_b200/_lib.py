@@ -55,7 +55,8 @@ _SIGS = {
     "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, P]),
     "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P,
-                           P, INT, P, SZ, P]),
+                           P, P, INT, P, INT, P, SZ, P]),
+    "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
     "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
     "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
     "sd_select_workspace_bytes": (SZ, [INT, INT]),
@@ -112,9 +113,9 @@ def require_cuda():
 
 
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
-_LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}
+_LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
-              "sd_ngram_bytes", "sd_tree_layout"}
+              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap"}
 launch_count = 0
 
 

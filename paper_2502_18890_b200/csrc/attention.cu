@@ -34,6 +34,7 @@ struct AttnParams {
   float* ws_o;
   float* ws_lse;
   const int32_t* rows_dev;  // nullable: live row count (<= T) read on device
+  int x_base;               // chunk index of blockIdx.x == 0 (tree-only launches)
 };
 
 __device__ __forceinline__ int live_rows(const AttnParams& p) {
@@ -165,7 +166,8 @@ __global__ void __launch_bounds__(256) attn_rows_kernel(AttnParams p) {
   const int GT = p.G * Tl;
   const int rho0 = blockIdx.z * 64;
   if (rho0 >= GT) return;
-  const bool tree = (int)blockIdx.x == p.n_chunks;
+  const int cx = (int)blockIdx.x + p.x_base;
+  const bool tree = cx == p.n_chunks;
   // load Q rows of this tile
   for (int i = tid; i < 64 * DH; i += 256) {
     const int rr = i / DH, d = i - rr * DH;
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(256) attn_rows_kernel(AttnParams p) {
   } else {
     K = (const KT*)p.k_cache + kvh * p.head_stride;
     V = (const KT*)p.v_cache + kvh * p.head_stride;
-    k_begin = blockIdx.x * p.chunk;
+    k_begin = cx * p.chunk;
     k_end = min(p.ctx, k_begin + p.chunk);
   }
   float m[RPW], l[RPW], acc[RPW][EPL];
@@ -227,7 +229,7 @@ __global__ void __launch_bounds__(256) attn_rows_kernel(AttnParams p) {
     if (trow[r] < 0) continue;
     const int rho = rho0 + warp + 8 * r;
     const int t = trow[r], g = rho - t * p.G, head = kvh * p.G + g;
-    const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + head;
+    const int64_t oi = ((int64_t)cx * p.T + t) * p.H + head;
     const float inv = l[r] > 0.f ? 1.f / l[r] : 0.f;
     if (DH >= 32 || lane < DH) {
 #pragma unroll
@@ -252,7 +254,8 @@ __global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
   const int kvh = blockIdx.y;
   const int Tl = live_rows(p);
   const int GT = p.G * Tl;
-  const bool tree = (int)blockIdx.x == p.n_chunks;
+  const int cx = (int)blockIdx.x + p.x_base;
+  const bool tree = cx == p.n_chunks;
   for (int i = tid; i < 8 * DH; i += 128) {
     const int rr = i / DH, d = i - rr * DH;
     float v = 0.f;
@@ -273,7 +276,7 @@ __global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
   } else {
     K = (const KT*)p.k_cache + kvh * p.head_stride;
     V = (const KT*)p.v_cache + kvh * p.head_stride;
-    k_begin = blockIdx.x * p.chunk;
+    k_begin = cx * p.chunk;
     k_end = min(p.ctx, k_begin + p.chunk);
   }
   float m[RPW], l[RPW], acc[RPW][EPL];
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
       }
     }
     const int t = r / p.G, g = r - t * p.G, head = kvh * p.G + g;
-    const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + head;
+    const int64_t oi = ((int64_t)cx * p.T + t) * p.H + head;
     p.ws_o[oi * DH + d] = L > 0.f ? O / L : 0.f;
     if (d == 0) p.ws_lse[oi] = L > 0.f ? M + __logf(L) : -INFINITY;
   }
@@ -369,10 +372,11 @@ __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* _
 }
 
 template <int DH, typename QT, typename KT, typename OT>
-static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaStream_t st) {
+static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaStream_t st, bool tree_only) {
   AttnParams p = p0;
   const int GT = p.G * p.T;
-  dim3 grid(p.n_chunks + 1, p.Hk, 1);
+  dim3 grid(tree_only ? 1 : p.n_chunks + 1, p.Hk, 1);
+  p.x_base = tree_only ? p.n_chunks : 0;
   if (GT <= 8) {
     const size_t smem = (8 * DH + 4 * (32 * (DH + 1) + 32 * DH)) * sizeof(float);
     auto kern = src_kind ? attn_keys_kernel<DH, QT, KT, true> : attn_keys_kernel<DH, QT, KT, false>;
@@ -394,16 +398,29 @@ static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaS
 
 template <int DH>
 static int dispatch_types(const AttnParams& p, int q_dtype, int kv_dtype, int out_dtype, int src_kind, void* out,
-                          cudaStream_t st) {
+                          cudaStream_t st, bool tree_only = false) {
   typedef __nv_bfloat16 bf;
   if (q_dtype == SD_BF16 && kv_dtype == SD_BF16 && out_dtype == SD_BF16)
-    return launch_attention<DH, bf, bf, bf>(p, src_kind, out, st);
+    return launch_attention<DH, bf, bf, bf>(p, src_kind, out, st, tree_only);
   if (q_dtype == SD_F32 && kv_dtype == SD_BF16 && out_dtype == SD_BF16)
-    return launch_attention<DH, float, bf, bf>(p, src_kind, out, st);
+    return launch_attention<DH, float, bf, bf>(p, src_kind, out, st, tree_only);
   if (q_dtype == SD_F32 && kv_dtype == SD_F32 && out_dtype == SD_F32)
-    return launch_attention<DH, float, float, float>(p, src_kind, out, st);
+    return launch_attention<DH, float, float, float>(p, src_kind, out, st, tree_only);
   set_error("sd_attention: unsupported dtype combination q=%d kv=%d out=%d", q_dtype, kv_dtype, out_dtype);
   return SD_EUNSUPPORTED;
+}
+
+int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
+int tc_n_chunks(int ctx, int Hk);
+int tc_chunk_len(int ctx, int n);
+int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
+                     const int32_t* rows_dev, float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st);
+
+// tensor-core path: all 16-bit, head_dim 128, full-cache source, >= one 64-key tile
+static bool use_tc(const void* tk, const void* tv, int q_dtype, int kv_dtype, int out_dtype, int dh, int src_kind,
+                   int ctx) {
+  return tk && tv && q_dtype == SD_BF16 && kv_dtype == SD_BF16 && out_dtype == SD_BF16 && dh == 128 &&
+         src_kind == 0 && ctx >= 64;
 }
 
 }  // namespace sd
@@ -413,14 +430,21 @@ using namespace sd;
 extern "C" {
 
 size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
-  const size_t ns = (size_t)n_chunks_for(ctx) + 1;
-  return ns * (size_t)T * H * (dh + 1) * sizeof(float);
+  int nc = n_chunks_for(ctx);
+  if (nc < 64) nc = 64;  // tensor-core chunking may use up to 64 chunks
+  return ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
+}
+
+int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host) {
+  SD_REQUIRE(base && tmap_out_host && dh == 128 && L > 0 && Hk > 0 && cap > 0, "sd_make_kv_tmap: args");
+  return tc_make_kv_tmap(base, L, Hk, cap, dh, tmap_out_host);
 }
 
 int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int src_kind, const void* k_cache,
                  const void* v_cache, int kv_dtype, int64_t head_stride, int ctx, const int32_t* ranks,
                  const float* rope_cos, const float* rope_sin, const void* k_tree, const void* v_tree,
                  int64_t tree_head_stride, const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
+                 const void* tmap_k_host, const void* tmap_v_host, int layer,
                  void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
   SD_REQUIRE(T > 0 && T <= SD_TREE_MAX_ROWS, "sd_attention: T=%d out of range", T);
   SD_REQUIRE(H > 0 && Hk > 0 && H % Hk == 0, "sd_attention: heads");
@@ -451,7 +475,19 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   p.ws_o = (float*)workspace;
   p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
   p.rows_dev = rows_dev;
+  p.x_base = 0;
   auto st = as_stream(stream);
+  if (use_tc(tmap_k_host, tmap_v_host, q_dtype, kv_dtype, out_dtype, dh, src_kind, ctx)) {
+    // cache chunks on tcgen05, the masked tree chunk on CUDA cores, then the shared merge
+    p.n_chunks = tc_n_chunks(ctx, Hk);
+    p.chunk = tc_chunk_len(ctx, p.n_chunks);
+    p.n_chunks = (ctx + p.chunk - 1) / p.chunk;
+    p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
+    int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, p.ws_o, p.ws_lse,
+                              p.n_chunks, p.chunk, st);
+    if (rc) return rc;
+    return dispatch_types<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st, /*tree_only=*/true);
+  }
   switch (dh) {
     case 8: return dispatch_types<8>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
     case 16: return dispatch_types<16>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);

@@ -1,0 +1,469 @@
+// Tree-verification attention on the 5th-generation tensor cores (sm_100a).
+//
+// Same contract as the split-KV path in attention.cu (reference model.py:238-247,
+// 290-300): per kv head, the G*T query rows of the tree (query head j uses kv
+// head j / G) attend to the full-cache rows of one key chunk; the CTA writes
+// (o / l, lse) per row and sd_attention merges the chunks (plus the masked tree
+// chunk, done on CUDA cores) in fixed order.
+//
+// One CTA = (key chunk, kv head, 256-row group), 12 warps:
+//   warp 0      TMA producer: K/V tiles of 64 keys x 128 dh (two 128-byte
+//               swizzled boxes each) into a 3-stage ring (mbarrier tx-count);
+//   warp 1      MMA issuer (one thread): S = Q K^T (M=128, N=64, K=16 steps)
+//               into TMEM, double-buffered, one tile ahead; O += P V (M=128,
+//               N=128, V consumed MN-major straight from the TMA layout);
+//   warp 2      TMEM allocator (512 columns: S[2 mtiles][2 bufs] x 64 + O[2] x 128);
+//   warps 4-11  two softmax warpgroups, one per 128-row M-tile: thread = row =
+//               TMEM lane; online softmax in base 2 with lazy rescale (O in
+//               TMEM is rescaled only when the row max grows by > 2^8), P
+//               written to shared memory in the UMMA K-major SW128 layout.
+// Q (pre-rotated, pre-scaled by 1/sqrt(dh)) is staged once per CTA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace sd {
+namespace tc {
+
+constexpr int BN = 64;          // keys per tile
+constexpr int DH = 128;
+constexpr int ST = 3;           // K/V pipeline stages
+constexpr int THREADS = 384;
+constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
+
+constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][half][128 rows][128 B]
+constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [half][64 rows][128 B]
+constexpr int P_BYTES = 128 * BN * 2;           // 16 KB per M-tile: [128 rows][128 B]
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int OFF_V = OFF_K + ST * KV_TILE;
+constexpr int OFF_P = OFF_V + ST * KV_TILE;
+constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+constexpr int N_BAR = 3 * ST + 4 + 2 + 2;
+constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
+constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
+
+// TMEM columns
+constexpr uint32_t COL_S = 0;    // S[mt][buf] at 64 * (2 mt + buf)
+constexpr uint32_t COL_O = 256;  // O[mt] at 256 + 128 mt
+constexpr uint32_t TMEM_COLS = 512;
+
+struct Params {
+  const __nv_bfloat16* q;  // [T][H][128]
+  int T, H, G;
+  int layer, ctx, chunk;
+  const int32_t* rows_dev;
+  float* ws_o;
+  float* ws_lse;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// UMMA shared-memory descriptor (SM100): start>>4 [0,14), LBO>>4 [16,30),
+// SBO>>4 [32,46), version 1 [46,48), layout type [61,64) (2 = SWIZZLE_128B).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor, kind::f16: D f32, A/B bf16, M=128
+__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+// byte offset of 16-byte chunk c of row r in a SWIZZLE_128B K-major tile (128 B rows)
+__device__ __forceinline__ uint32_t sw128(int r, int c) { return (uint32_t)(r * 128 + ((c ^ (r & 7)) << 4)); }
+
+// tcgen05.ld / st of 32 consecutive columns of this warp's 32 TMEM lanes
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+               : "memory");
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+    verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
+                          Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
+  uint64_t* k_full = bars;
+  uint64_t* v_full = bars + ST;
+  uint64_t* kv_empty = bars + 2 * ST;
+  uint64_t* s_full = bars + 3 * ST;      // [mt][buf]
+  uint64_t* p_full = s_full + 4;         // [mt]
+  uint64_t* o_done = p_full + 2;         // [mt]
+  uint32_t* tmem_slot = (uint32_t*)(o_done + 2);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kvh = blockIdx.y;
+  const int T = p.rows_dev ? min(*p.rows_dev, p.T) : p.T;
+  const int GT = p.G * T;
+  const int rg = blockIdx.z * ROWS;
+  if (rg >= GT) return;
+  const int key_begin = blockIdx.x * p.chunk;
+  const int key_end = min(p.ctx, key_begin + p.chunk);
+  const int n_tiles = (key_end - key_begin + BN - 1) / BN;
+  // active warps per M-tile (rows beyond G*T are padding)
+  int act[2];
+  for (int mt = 0; mt < 2; ++mt) {
+    int a = 0;
+    for (int w = 0; w < 4; ++w) a += (rg + 128 * mt + 32 * w) < GT;
+    act[mt] = a;
+  }
+  const int nm = act[1] > 0 ? 2 : 1;
+
+  // ---- stage Q (two M-tiles, K-major SW128) and zero P ----
+  {
+    const int chunks = ROWS * (DH / 8);  // 16-byte chunks
+    for (int i = tid; i < chunks; i += THREADS) {
+      const int row = i >> 4, c = i & 15;
+      const int rho = rg + row;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (rho < GT) {
+        const int t = rho / p.G, g = rho - t * p.G;
+        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8);
+      }
+      const int mt = row >> 7, r = row & 127, half = c >> 3;
+      *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v;
+    }
+    for (int i = tid; i < 2 * P_BYTES / 16; i += THREADS)
+      *reinterpret_cast<uint4*>(smem + OFF_P + i * 16) = make_uint4(0, 0, 0, 0);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&kv_empty[s], 1);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
+    for (int mt = 0; mt < 2; ++mt) {
+      mbar_init(&p_full[mt], 32 * (act[mt] > 0 ? act[mt] : 1));
+      mbar_init(&o_done[mt], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer =================
+    if (lane == 0) {
+      tma_prefetch(&tmap_k);
+      tma_prefetch(&tmap_v);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % ST;
+        if (j >= ST) mbar_wait(&kv_empty[s], ((j / ST) + 1) & 1);
+        const int key0 = key_begin + j * BN;
+        uint8_t* kd = smem + OFF_K + s * KV_TILE;
+        uint8_t* vd = smem + OFF_V + s * KV_TILE;
+        mbar_expect_tx(&k_full[s], KV_TILE);
+        tma_load_4d(kd, &tmap_k, &k_full[s], 0, key0, kvh, p.layer);
+        tma_load_4d(kd + KV_TILE / 2, &tmap_k, &k_full[s], 64, key0, kvh, p.layer);
+        mbar_expect_tx(&v_full[s], KV_TILE);
+        tma_load_4d(vd, &tmap_v, &v_full[s], 0, key0, kvh, p.layer);
+        tma_load_4d(vd + KV_TILE / 2, &tmap_v, &v_full[s], 64, key0, kvh, p.layer);
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t id_qk = idesc_bf16(BN, false);
+      const uint32_t id_pv = idesc_bf16(DH, true);
+      const uint32_t q_base = smem_u32(smem + OFF_Q);
+      auto issue_qk = [&](int j) {
+        const int s = j % ST, b = j & 1;
+        mbar_wait(&k_full[s], (j / ST) & 1);
+        tc_fence_after();
+        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
+        for (int mt = 0; mt < nm; ++mt) {
+#pragma unroll
+          for (int ks = 0; ks < DH / 16; ++ks) {
+            const uint32_t koff = (ks >> 2) * 0, half = ks >> 2, in = (ks & 3) * 32;
+            (void)koff;
+            const uint64_t a = umma_desc(q_base + mt * 32768 + half * 16384 + in, 16, 1024);
+            const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
+            umma_bf16(tmem + COL_S + 64 * (2 * mt + b), a, bd, id_qk, ks > 0);
+          }
+          umma_commit(&s_full[2 * mt + b]);
+        }
+      };
+      issue_qk(0);
+      for (int j = 0; j < n_tiles; ++j) {
+        if (j + 1 < n_tiles) issue_qk(j + 1);
+        const int s = j % ST;
+        mbar_wait(&v_full[s], (j / ST) & 1);
+        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
+        for (int mt = 0; mt < nm; ++mt) {
+          mbar_wait(&p_full[mt], j & 1);
+          tc_fence_after();
+          const uint32_t p_base = smem_u32(smem + OFF_P + mt * P_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BN / 16; ++ks) {
+            const uint64_t a = umma_desc(p_base + ks * 32, 16, 1024);
+            // V tile is [keys][dh] (MN-major for B): dh halves are LBO apart, 8-key groups SBO apart
+            const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
+            umma_bf16(tmem + COL_O + 128 * mt, a, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
+          }
+          umma_commit(&o_done[mt]);
+        }
+        umma_commit(&kv_empty[s]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ================= softmax warpgroups =================
+    const int mt = (warp - 4) >> 2, wl = warp & 3;
+    const int row = 32 * wl + lane;
+    const int rho = rg + 128 * mt + row;
+    const bool warp_active = (rg + 128 * mt + 32 * wl) < GT;
+    if (mt < nm && warp_active) {
+      const bool valid = rho < GT;
+      const uint32_t lane_base = (uint32_t)(32 * wl) << 16;
+      uint8_t* prow = smem + OFF_P + mt * P_BYTES;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int b = j & 1;
+        mbar_wait(&s_full[2 * mt + b], (j >> 1) & 1);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b), sr);
+        tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b) + 32, sr + 32);
+        tmem_wait_ld();
+        const int nvalid = min(BN, key_end - (key_begin + j * BN));
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+          const float v = __uint_as_float(sr[c]) * LOG2E;
+          sr[c] = __float_as_uint(v);
+          if (c < nvalid) mx = fmaxf(mx, v);
+        }
+        float scale = 1.f;
+        bool rescale = false;
+        if (mx > m_used + TAU) {
+          scale = m_used == -INFINITY ? 0.f : ex2(m_used - mx);
+          rescale = j > 0;
+          m_used = mx;
+          l *= scale;
+        }
+        uint32_t pk[32];
+        float rs = 0.f;
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+          const float p0 = (c < nvalid && valid) ? ex2(__uint_as_float(sr[c]) - m_used) : 0.f;
+          const float p1 = (c + 1 < nvalid && valid) ? ex2(__uint_as_float(sr[c + 1]) - m_used) : 0.f;
+          rs += p0 + p1;
+          pk[c >> 1] = pack_bf16(p0, p1);
+        }
+        l += rs;
+        if (j > 0) mbar_wait(&o_done[mt], (j - 1) & 1);  // PV(j-1) done: P free, O stable
+        if (__any_sync(0xffffffffu, rescale)) {
+          tc_fence_after();
+#pragma unroll
+          for (int q4 = 0; q4 < 4; ++q4) {
+            uint32_t o[32];
+            const uint32_t ta = tmem + lane_base + COL_O + 128 * mt + 32 * q4;
+            tmem_ld32(ta, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * (rescale ? scale : 1.f));
+            tmem_st32(ta, o);
+          }
+          tmem_wait_st();
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(prow + sw128(row, c)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        fence_async_smem();
+        tc_fence_before();
+        mbar_arrive(&p_full[mt]);
+      }
+      // ---- epilogue: O / l, lse (natural log) ----
+      mbar_wait(&o_done[mt], (n_tiles - 1) & 1);
+      tc_fence_after();
+      const int t = rho / p.G, g = rho - t * p.G;
+      const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        uint32_t o[32];
+        tmem_ld32(tmem + lane_base + COL_O + 128 * mt + 32 * q4, o);
+        tmem_wait_ld();
+        if (valid) {
+          float4* dst = reinterpret_cast<float4*>(p.ws_o + oi * DH + 32 * q4);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            dst[c] = make_float4(__uint_as_float(o[4 * c]) * inv, __uint_as_float(o[4 * c + 1]) * inv,
+                                 __uint_as_float(o[4 * c + 2]) * inv, __uint_as_float(o[4 * c + 3]) * inv);
+        }
+      }
+      if (valid) p.ws_lse[oi] = l > 0.f ? (m_used + __log2f(l)) / LOG2E : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
+  }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------- host -----
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  }
+  return fn;
+}
+
+int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out) {
+  auto enc = get_encode();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SD_ECUDA;
+  }
+  CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
+  cuuint64_t dims[4] = {(cuuint64_t)dh, (cuuint64_t)cap, (cuuint64_t)Hk, (cuuint64_t)L};
+  cuuint64_t strides[3] = {(cuuint64_t)dh * 2, (cuuint64_t)cap * dh * 2, (cuuint64_t)Hk * cap * dh * 2};
+  cuuint32_t box[4] = {64, (cuuint32_t)tc::BN, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return SD_ECUDA;
+  }
+  return SD_OK;
+}
+
+int tc_n_chunks(int ctx, int Hk) {
+  // ~2 waves of one CTA per SM over (chunks x kv heads); >= 1 tile per chunk
+  int want = (2 * 148 + Hk - 1) / Hk;
+  const int max_by_tiles = (ctx + tc::BN - 1) / tc::BN;
+  if (want > max_by_tiles) want = max_by_tiles;
+  if (want > 64) want = 64;
+  return want < 1 ? 1 : want;
+}
+
+int tc_chunk_len(int ctx, int n) {
+  int c = (ctx + n - 1) / n;
+  return (c + tc::BN - 1) / tc::BN * tc::BN;
+}
+
+int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
+                     const int32_t* rows_dev, float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
+    attr_set = true;
+  }
+  tc::Params p;
+  p.q = (const __nv_bfloat16*)q;
+  p.T = T;
+  p.H = H;
+  p.G = H / Hk;
+  p.layer = layer;
+  p.ctx = ctx;
+  p.chunk = chunk;
+  p.rows_dev = rows_dev;
+  p.ws_o = ws_o;
+  p.ws_lse = ws_lse;
+  const int groups = (p.G * T + tc::ROWS - 1) / tc::ROWS;
+  dim3 grid(n_chunks, Hk, groups);
+  CUtensorMap mk, mv;
+  memcpy(&mk, tmap_k, sizeof(CUtensorMap));
+  memcpy(&mv, tmap_v, sizeof(CUtensorMap));
+  tc::verify_attn_tc_kernel<<<grid, tc::THREADS, tc::SMEM_ALLOC, st>>>(mk, mv, p);
+  return check_launch("sd_attention(tcgen05)");
+}
+
+}  // namespace sd

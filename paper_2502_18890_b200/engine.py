@@ -271,7 +271,7 @@ class Session:
             m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l, :, base:], F.k_rot[l, :, base:], F.v[l, :, base:],
                          F.head_stride, 0, rows_dev)
             m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                        F.v[l, :, base:], F.head_stride, bits, rows_dev, out)
+                        F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l)
             return out
 
         h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)

@@ -54,6 +54,14 @@ class FullCache:
         self.k_rot = torch.zeros(shape, dtype=dtype, device=self.device)
         self.v = torch.zeros(shape, dtype=dtype, device=self.device)
         self.positions: list[int] = []
+        self.tmaps = None
+        if dtype == torch.bfloat16 and head_dim == 128:
+            # TMA descriptors for the tensor-core verification path (sd_attention)
+            import ctypes
+            tk, tv = ctypes.create_string_buffer(128), ctypes.create_string_buffer(128)
+            L.call("sd_make_kv_tmap", L.ptr(self.k_rot), num_layers, num_kv_heads, capacity, head_dim, tk)
+            L.call("sd_make_kv_tmap", L.ptr(self.v), num_layers, num_kv_heads, capacity, head_dim, tv)
+            self.tmaps = (tk, tv)
 
     # strides in elements
     @property

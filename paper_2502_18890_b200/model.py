@@ -197,6 +197,7 @@ class TinyTransformer:
         self.rope_cos = torch.as_tensor(np.cos(ang).astype(np.float32), device=self.device).reshape(-1, half)
         self.rope_sin = torch.as_tensor(np.sin(ang).astype(np.float32), device=self.device).reshape(-1, half)
         self._ws = torch.empty(0, dtype=torch.uint8, device=self.device)
+        self.use_tc = True  # tcgen05 verification attention when the cache supports it
 
     # ------------------------------------------------------------ weights --
     def _load_weights(self, params, init):
@@ -298,15 +299,18 @@ class TinyTransformer:
         return all_gather_heads(o, self.world, self.group)
 
     def attention(self, q_rot, T, src_kind, k_cache, v_cache, head_stride, ctx, ranks, k_tree, v_tree,
-                  tree_head_stride, mask_bits, rows_dev, out):
+                  tree_head_stride, mask_bits, rows_dev, out, tmaps=None, layer=0):
+        """sd_attention; with `tmaps` (FullCache.tmaps) and bf16/dh=128 the cache
+        chunks run on the tcgen05 kernel of `layer`."""
         nbytes = L.load().sd_attention_workspace_bytes(T, self.H, self.dh, ctx)
         ws = self.workspace(nbytes)
         kd = L.dcode(self.dtype)
+        tk, tv = tmaps if (tmaps is not None and self.use_tc) else (None, None)
         L.call("sd_attention", L.ptr(q_rot), kd, T, self.H, self.Hk, self.dh, src_kind, L.ptr(k_cache),
                L.ptr(v_cache), kd, head_stride, ctx, L.ptr(ranks), L.ptr(self.rope_cos), L.ptr(self.rope_sin),
                L.ptr(k_tree), L.ptr(v_tree), tree_head_stride, L.ptr(mask_bits),
-               L.MASK_WORDS if mask_bits is not None else 0, L.ptr(rows_dev), L.ptr(out), kd, L.ptr(ws),
-               ws.numel(), L.stream())
+               L.MASK_WORDS if mask_bits is not None else 0, L.ptr(rows_dev), tk, tv, layer, L.ptr(out), kd,
+               L.ptr(ws), ws.numel(), L.stream())
 
     def rope_stage(self, qkv, T, positions_dev, q_rot, q_pre, k_raw, k_rot, v, head_stride, row_offset,
                    rows_dev=None):
@@ -406,13 +410,14 @@ class TinyTransformer:
                             cache.v[l, :, ctx:], cache.head_stride, 0)
             if bits is not None:
                 self.attention(q_rot, T, 0, cache.k_rot[l], cache.v[l], cache.head_stride, ctx, None,
-                               cache.k_rot[l, :, ctx:], cache.v[l, :, ctx:], cache.head_stride, bits, None, out)
+                               cache.k_rot[l, :, ctx:], cache.v[l, :, ctx:], cache.head_stride, bits, None, out,
+                               cache.tmaps, l)
             else:  # causal in blocks of <= 128 rows (model.py:301-305)
                 for b0 in range(0, T, 128):
                     tb = min(128, T - b0)
                     self.attention(q_rot[b0:], tb, 0, cache.k_rot[l], cache.v[l], cache.head_stride, ctx + b0,
                                    None, cache.k_rot[l, :, ctx + b0:], cache.v[l, :, ctx + b0:], cache.head_stride,
-                                   None, None, out[b0:])
+                                   None, None, out[b0:], cache.tmaps, l)
             return out
         return attend
 

@@ -75,7 +75,7 @@ def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, T, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, lib.ptr(bits), lib.MASK_WORDS,
-             None, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+             None, None, None, 0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
     # oracle on the same (rounded) inputs
     Kr = kt.double().cpu().numpy().transpose(1, 0, 2)
     Vr = vt.double().cpu().numpy().transpose(1, 0, 2)
@@ -87,6 +87,50 @@ def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
     got = out.double().cpu().numpy().reshape(T, H, dh)
     tol = 1e-5 if dtype == torch.float32 else 2e-2
     np.testing.assert_allclose(got, want, rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("ctx,T,H,Hk,layer", [(64, 1, 32, 8, 0), (100, 5, 32, 8, 1), (700, 41, 32, 8, 2),
+                                               (4096, 41, 32, 8, 0), (3000, 101, 32, 8, 1), (1500, 20, 40, 8, 2),
+                                               (20000, 41, 32, 8, 1), (900, 70, 32, 32, 0)])
+def test_verify_attention_tcgen05(lib, ctx, T, H, Hk, layer):
+    """tcgen05/TMA/TMEM path (bf16, dh=128) vs the fp64 oracle and vs the CUDA-core path."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200.model import mask_bits_from_bool
+    dev = torch.device("cuda")
+    g = np.random.default_rng(ctx * 7 + T)
+    dh, Lr = 128, 3
+    cap = ctx + T + 70
+    F = FullCache(Lr, Hk, dh, capacity=cap, dtype=torch.bfloat16)
+    assert F.tmaps is not None
+    F.k_rot.copy_(torch.as_tensor(g.normal(size=(Lr, Hk, cap, dh)), dtype=torch.bfloat16))
+    F.v.copy_(torch.as_tensor(g.normal(size=(Lr, Hk, cap, dh)), dtype=torch.bfloat16))
+    parent = [-1] + [int(g.integers(0, i)) for i in range(1, T)]
+    mask = np.zeros((T, T), dtype=bool)
+    for i in range(T):
+        j = i
+        while j >= 0:
+            mask[i, j] = True
+            j = parent[j]
+    bits = torch.as_tensor(mask_bits_from_bool(mask), device=dev)
+    qt = torch.as_tensor(g.normal(size=(T, H, dh)) * 2.0 / np.sqrt(dh), dtype=torch.bfloat16, device=dev)
+    outs = []
+    for tm in (F.tmaps, (None, None)):
+        out = torch.empty((T, H * dh), dtype=torch.bfloat16, device=dev)
+        ws = torch.empty(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
+        lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
+                 F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
+                 F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, tm[0], tm[1],
+                 layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
+        outs.append(out.double().cpu().numpy().reshape(T, H, dh))
+    Kr = F.k_rot[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
+    Vr = F.v[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
+    vis = np.zeros((T, ctx + T), dtype=bool)
+    vis[:, :ctx] = True
+    vis[:, ctx:] = mask
+    want = attend_oracle(qt.double().cpu().numpy(), Kr, Vr, vis)
+    np.testing.assert_allclose(outs[0], want, rtol=2e-2, atol=2e-2)
+    np.testing.assert_allclose(outs[0], outs[1], rtol=2e-2, atol=2e-2)
+    assert np.max(np.abs(outs[0] - want)) < 1.5e-2
 
 
 def test_attention_rows_dev_padding(lib):
@@ -105,7 +149,7 @@ def test_attention_rows_dev_padding(lib):
         ws = torch.empty(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 0, TT, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), 0, cap * dh, ctx, None,
                  None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, lib.ptr(rd),
-                 lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
+                 None, None, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
         outs.append(out)
     assert torch.equal(outs[0][:Tl], outs[1])
     assert torch.all(outs[0][Tl:] == 0)
