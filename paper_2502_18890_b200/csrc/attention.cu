@@ -410,11 +410,178 @@ static int dispatch_types(const AttnParams& p, int q_dtype, int kv_dtype, int ou
   return SD_EUNSUPPORTED;
 }
 
+
+// ------------------------------------------------------------------------
+// Single-row decode attention (draft over the partial cache, AR decode over
+// the full cache): T == 1, G <= 8 query heads per kv head. A CTA takes one
+// 64-key chunk of one kv head; each warp streams 16 keys with lanes over
+// head_dim (coalesced rows), 8 keys' loads in flight at a time, RoPE at the
+// slot's rank applied on load (kvcache.py:158-165), dot products reduced with
+// warp shuffles, online softmax per query head, then the 4 warps merge.
+constexpr int DEC_CHUNK = 64;
+
+template <int DH, typename QT, typename KT, bool ROT>
+__global__ void __launch_bounds__(128) decode_attn_kernel(AttnParams p, int chunk) {
+  constexpr int EPL = DH / 32;  // elements per lane (DH >= 64 -> even)
+  constexpr int NB = 8;         // keys per load batch
+  __shared__ float Sm[4][8], Sl[4][8], So[4][8][DH];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kvh = blockIdx.y, G = p.G;
+  const int cx = blockIdx.x;
+  const bool tree = cx == p.n_chunks;
+  const KT* K;
+  const KT* V;
+  int k_begin, k_end;
+  if (tree) {
+    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
+    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    k_begin = 0;
+    k_end = 1;
+  } else {
+    K = (const KT*)p.k_cache + kvh * p.head_stride;
+    V = (const KT*)p.v_cache + kvh * p.head_stride;
+    k_begin = cx * chunk;
+    k_end = min(p.ctx, k_begin + chunk);
+  }
+  // query rows of this kv head (T == 1): q[head = kvh*G + g]
+  float q[8][EPL];
+#pragma unroll
+  for (int g = 0; g < 8; ++g)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e)
+      q[g][e] = g < G ? to_f(((const QT*)p.q)[(int64_t)(kvh * G + g) * DH + lane * EPL + e]) : 0.f;
+  float m[8], l[8], acc[8][EPL];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
+  }
+  const int per_warp = (chunk + 3) / 4;
+  const int w0 = k_begin + warp * per_warp, w1 = min(k_end, w0 + per_warp);
+  for (int kb = w0; kb < w1; kb += NB) {
+    float kr[NB][EPL], vr[NB][EPL];
+    bool ok[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = kb + b;
+      ok[b] = k < w1;
+      int rk = 0;
+      if (ROT && !tree && ok[b]) {
+        rk = p.ranks[k];
+        ok[b] = rk >= 0;  // hole slot
+      }
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        kr[b][e] = ok[b] ? to_f(K[(int64_t)k * DH + lane * EPL + e]) : 0.f;
+        vr[b][e] = ok[b] ? to_f(V[(int64_t)k * DH + lane * EPL + e]) : 0.f;
+      }
+      if (ROT && !tree && ok[b]) {
+#pragma unroll
+        for (int e = 0; e < EPL; e += 2) {
+          const int i = (lane * EPL + e) >> 1;
+          const float c = p.cosT[(int64_t)rk * (DH / 2) + i], s = p.sinT[(int64_t)rk * (DH / 2) + i];
+          const float a = kr[b][e], bb = kr[b][e + 1];
+          kr[b][e] = a * c - bb * s;
+          kr[b][e + 1] = a * s + bb * c;
+        }
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (!__any_sync(0xffffffffu, ok[b])) continue;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) {
+        if (g >= G) break;
+        float s = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) s = fmaf(q[g][e], kr[b][e], s);
+        s = warp_sum(s);
+        if (!ok[b]) continue;  // uniform across the warp (ok depends on the key only)
+        const float mn = fmaxf(m[g], s);
+        const float corr = __expf(m[g] - mn), pw = __expf(s - mn);
+        l[g] = l[g] * corr + pw;
+        m[g] = mn;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[g][e] = fmaf(acc[g][e], corr, pw * vr[b][e]);
+      }
+    }
+  }
+  // merge the 4 warps
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    if (g >= G) break;
+    if (lane == 0) {
+      Sm[warp][g] = m[g];
+      Sl[warp][g] = l[g];
+    }
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) So[warp][g][lane * EPL + e] = acc[g][e];
+  }
+  __syncthreads();
+  for (int i = tid; i < G * DH; i += 128) {
+    const int g = i / DH, d = i - g * DH;
+    float M = -INFINITY;
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, Sm[w][g]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+      for (int w = 0; w < 4; ++w) {
+        const float sc = __expf(Sm[w][g] - M);
+        L += Sl[w][g] * sc;
+        O += So[w][g][d] * sc;
+      }
+    }
+    const int64_t oi = (int64_t)cx * p.H + kvh * G + g;  // T == 1
+    p.ws_o[oi * DH + d] = L > 0.f ? O / L : 0.f;
+    if (d == 0) p.ws_lse[oi] = L > 0.f ? M + __logf(L) : -INFINITY;
+  }
+}
+
+static inline int dec_chunk_for(int ctx) {
+  int c = (ctx + 255) / 256;
+  c = (c + DEC_CHUNK - 1) / DEC_CHUNK * DEC_CHUNK;
+  return c < DEC_CHUNK ? DEC_CHUNK : c;
+}
+
+template <int DH, typename QT, typename KT, typename OT>
+static int launch_decode(AttnParams p, int src_kind, void* out, cudaStream_t st) {
+  const int chunk = dec_chunk_for(p.ctx);
+  p.n_chunks = p.ctx > 0 ? (p.ctx + chunk - 1) / chunk : 0;
+  p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * p.H * DH;
+  dim3 grid(p.n_chunks + 1, p.Hk);
+  if (src_kind)
+    decode_attn_kernel<DH, QT, KT, true><<<grid, 128, 0, st>>>(p, chunk);
+  else
+    decode_attn_kernel<DH, QT, KT, false><<<grid, 128, 0, st>>>(p, chunk);
+  int rc = check_launch("sd_attention(decode)");
+  if (rc) return rc;
+  attn_merge_kernel<DH, OT><<<p.H, DH >= 128 ? 128 : DH, 0, st>>>(p.ws_o, p.ws_lse, p.n_chunks + 1, p.H, p.H,
+                                                                   p.rows_dev, (OT*)out);
+  return check_launch("sd_attention(decode merge)");
+}
+
+template <int DH>
+static int dispatch_decode(const AttnParams& p, int q_dtype, int kv_dtype, int out_dtype, int src_kind, void* out,
+                           cudaStream_t st) {
+  typedef __nv_bfloat16 bf;
+  if (q_dtype == SD_BF16 && kv_dtype == SD_BF16 && out_dtype == SD_BF16)
+    return launch_decode<DH, bf, bf, bf>(p, src_kind, out, st);
+  if (q_dtype == SD_F32 && kv_dtype == SD_F32 && out_dtype == SD_F32)
+    return launch_decode<DH, float, float, float>(p, src_kind, out, st);
+  set_error("sd_attention(decode): unsupported dtype combination");
+  return SD_EUNSUPPORTED;
+}
+
 int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
 int tc_n_chunks(int ctx, int Hk);
 int tc_chunk_len(int ctx, int n);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
-                     const int32_t* rows_dev, float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st);
+                     const int32_t* rows_dev, const uint32_t* mask, int mask_words, float* ws_o, float* ws_lse,
+                     int n_chunks, int chunk, cudaStream_t st);
+template <int DH, typename OT>
+__global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
+                                  int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out);
 
 // tensor-core path: all 16-bit, head_dim 128, full-cache source, >= one 64-key tile
 static bool use_tc(const void* tk, const void* tv, int q_dtype, int kv_dtype, int out_dtype, int dh, int src_kind,
@@ -431,7 +598,11 @@ extern "C" {
 
 size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
   int nc = n_chunks_for(ctx);
-  if (nc < 64) nc = 64;  // tensor-core chunking may use up to 64 chunks
+  if (nc < 148) nc = 148;  // tensor-core chunking may use up to 148 chunks
+  if (T == 1 && ctx > 0) {
+    const int dc = (ctx + dec_chunk_for(ctx) - 1) / dec_chunk_for(ctx);
+    if (dc > nc) nc = dc;
+  }
   return ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
 }
 
@@ -478,15 +649,22 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   p.x_base = 0;
   auto st = as_stream(stream);
   if (use_tc(tmap_k_host, tmap_v_host, q_dtype, kv_dtype, out_dtype, dh, src_kind, ctx)) {
-    // cache chunks on tcgen05, the masked tree chunk on CUDA cores, then the shared merge
-    p.n_chunks = tc_n_chunks(ctx, Hk);
-    p.chunk = tc_chunk_len(ctx, p.n_chunks);
-    p.n_chunks = (ctx + p.chunk - 1) / p.chunk;
-    p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
-    int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, p.ws_o, p.ws_lse,
-                              p.n_chunks, p.chunk, st);
+    // cache chunks + the masked tree rows on tcgen05, then the chunk merge
+    int nc = tc_n_chunks(ctx, Hk);
+    const int chunk = tc_chunk_len(ctx, nc);
+    nc = (ctx + chunk - 1) / chunk;
+    float* ws_lse = p.ws_o + (size_t)nc * T * H * dh;
+    int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, mask_bits, mask_words,
+                              p.ws_o, ws_lse, nc, chunk, st);
     if (rc) return rc;
-    return dispatch_types<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st, /*tree_only=*/true);
+    attn_merge_kernel<128, __nv_bfloat16><<<T * H, 128, 0, st>>>(p.ws_o, ws_lse, nc, T * H, H, rows_dev,
+                                                                  (__nv_bfloat16*)out);
+    return check_launch("sd_attention(tc merge)");
+  }
+  if (T == 1 && p.G <= 8 && (dh == 64 || dh == 128) && !rows_dev) {
+    // single-row decode (draft / AR): latency-tolerant streaming kernel
+    if (dh == 128) return dispatch_decode<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    return dispatch_decode<64>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
   }
   switch (dh) {
     case 8: return dispatch_types<8>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);

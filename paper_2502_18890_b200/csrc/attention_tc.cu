@@ -3,12 +3,13 @@
 // Same contract as the split-KV path in attention.cu (reference model.py:238-247,
 // 290-300): per kv head, the G*T query rows of the tree (query head j uses kv
 // head j / G) attend to the full-cache rows of one key chunk; the CTA writes
-// (o / l, lse) per row and sd_attention merges the chunks (plus the masked tree
-// chunk, done on CUDA cores) in fixed order.
+// (o / l, lse) per row and sd_attention merges the chunks in fixed order.
 //
-// One CTA = (key chunk, kv head, 256-row group), 12 warps:
-//   warp 0      TMA producer: K/V tiles of 64 keys x 128 dh (two 128-byte
-//               swizzled boxes each) into a 3-stage ring (mbarrier tx-count);
+// One CTA = (key chunk, kv head, 256-row group), 12 warps; the last chunk
+// also covers the T staged tree rows (keys ctx..ctx+T-1) under the tree mask.
+//   warp 0      TMA producer: K and V tiles of 64 keys x 128 dh (two 128-byte
+//               swizzled boxes each) into separate 4-deep rings (mbarrier
+//               tx-count); K slots free as soon as S = QK^T retires;
 //   warp 1      MMA issuer (one thread): S = Q K^T (M=128, N=64, K=16 steps)
 //               into TMEM, double-buffered, one tile ahead; O += P V (M=128,
 //               N=128, V consumed MN-major straight from the TMA layout);
@@ -28,7 +29,7 @@ namespace tc {
 
 constexpr int BN = 64;          // keys per tile
 constexpr int DH = 128;
-constexpr int ST = 3;           // K/V pipeline stages
+constexpr int ST = 4;           // K ring depth == V ring depth
 constexpr int THREADS = 384;
 constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
@@ -42,7 +43,7 @@ constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
 constexpr int OFF_P = OFF_V + ST * KV_TILE;
 constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
-constexpr int N_BAR = 3 * ST + 4 + 2 + 2;
+constexpr int N_BAR = 4 * ST + 4 + 2 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
@@ -54,8 +55,10 @@ constexpr uint32_t TMEM_COLS = 512;
 struct Params {
   const __nv_bfloat16* q;  // [T][H][128]
   int T, H, G;
-  int layer, ctx, chunk;
+  int layer, ctx, chunk, n_chunks;
   const int32_t* rows_dev;
+  const uint32_t* mask;    // [T][mask_words] tree rows (NULL = causal)
+  int mask_words;
   float* ws_o;
   float* ws_lse;
 };
@@ -153,6 +156,7 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
+
 __global__ void __launch_bounds__(THREADS, 1)
     verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                           Params p) {
@@ -161,8 +165,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
   uint64_t* k_full = bars;
   uint64_t* v_full = bars + ST;
-  uint64_t* kv_empty = bars + 2 * ST;
-  uint64_t* s_full = bars + 3 * ST;      // [mt][buf]
+  uint64_t* k_empty = bars + 2 * ST;
+  uint64_t* v_empty = bars + 3 * ST;
+  uint64_t* s_full = bars + 4 * ST;      // [mt][buf]
   uint64_t* p_full = s_full + 4;         // [mt]
   uint64_t* o_done = p_full + 2;         // [mt]
   uint32_t* tmem_slot = (uint32_t*)(o_done + 2);
@@ -173,10 +178,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int GT = p.G * T;
   const int rg = blockIdx.z * ROWS;
   if (rg >= GT) return;
+  const bool last = (int)blockIdx.x == p.n_chunks - 1;
   const int key_begin = blockIdx.x * p.chunk;
-  const int key_end = min(p.ctx, key_begin + p.chunk);
+  const int cache_end = min(p.ctx, key_begin + p.chunk);
+  const int key_end = last ? p.ctx + T : cache_end;  // the last chunk also takes the tree rows
   const int n_tiles = (key_end - key_begin + BN - 1) / BN;
-  // active warps per M-tile (rows beyond G*T are padding)
   int act[2];
   for (int mt = 0; mt < 2; ++mt) {
     int a = 0;
@@ -185,19 +191,29 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const int nm = act[1] > 0 ? 2 : 1;
 
-  // ---- stage Q (two M-tiles, K-major SW128) and zero P ----
+  // ---- stage Q (two M-tiles, K-major SW128): all loads in flight, then stores ----
   {
-    const int chunks = ROWS * (DH / 8);  // 16-byte chunks
-    for (int i = tid; i < chunks; i += THREADS) {
+    constexpr int PER = (ROWS * (DH / 8) + THREADS - 1) / THREADS;  // 16-byte chunks per thread
+    uint4 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * THREADS;
       const int row = i >> 4, c = i & 15;
       const int rho = rg + row;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (rho < GT) {
+      v[k] = make_uint4(0, 0, 0, 0);
+      if (i < ROWS * 16 && rho < GT) {
         const int t = rho / p.G, g = rho - t * p.G;
-        v = *reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8);
+        v[k] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8));
       }
-      const int mt = row >> 7, r = row & 127, half = c >> 3;
-      *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * THREADS;
+      if (i < ROWS * 16) {
+        const int row = i >> 4, c = i & 15;
+        const int mt = row >> 7, r = row & 127, half = c >> 3;
+        *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v[k];
+      }
     }
     for (int i = tid; i < 2 * P_BYTES / 16; i += THREADS)
       *reinterpret_cast<uint4*>(smem + OFF_P + i * 16) = make_uint4(0, 0, 0, 0);
@@ -206,7 +222,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < ST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&kv_empty[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_empty[s], 1);
     }
     for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int mt = 0; mt < 2; ++mt) {
@@ -228,19 +245,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ================= TMA producer =================
+    // ================= TMA producer: K(j), V(j) in order, separate rings =================
     if (lane == 0) {
       tma_prefetch(&tmap_k);
       tma_prefetch(&tmap_v);
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
-        if (j >= ST) mbar_wait(&kv_empty[s], ((j / ST) + 1) & 1);
         const int key0 = key_begin + j * BN;
+        if (j >= ST) mbar_wait(&k_empty[s], ((j / ST) + 1) & 1);
         uint8_t* kd = smem + OFF_K + s * KV_TILE;
-        uint8_t* vd = smem + OFF_V + s * KV_TILE;
         mbar_expect_tx(&k_full[s], KV_TILE);
         tma_load_4d(kd, &tmap_k, &k_full[s], 0, key0, kvh, p.layer);
         tma_load_4d(kd + KV_TILE / 2, &tmap_k, &k_full[s], 64, key0, kvh, p.layer);
+        if (j >= ST) mbar_wait(&v_empty[s], ((j / ST) + 1) & 1);
+        uint8_t* vd = smem + OFF_V + s * KV_TILE;
         mbar_expect_tx(&v_full[s], KV_TILE);
         tma_load_4d(vd, &tmap_v, &v_full[s], 0, key0, kvh, p.layer);
         tma_load_4d(vd + KV_TILE / 2, &tmap_v, &v_full[s], 64, key0, kvh, p.layer);
@@ -260,14 +278,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int mt = 0; mt < nm; ++mt) {
 #pragma unroll
           for (int ks = 0; ks < DH / 16; ++ks) {
-            const uint32_t koff = (ks >> 2) * 0, half = ks >> 2, in = (ks & 3) * 32;
-            (void)koff;
+            const uint32_t half = ks >> 2, in = (ks & 3) * 32;
             const uint64_t a = umma_desc(q_base + mt * 32768 + half * 16384 + in, 16, 1024);
             const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
             umma_bf16(tmem + COL_S + 64 * (2 * mt + b), a, bd, id_qk, ks > 0);
           }
           umma_commit(&s_full[2 * mt + b]);
         }
+        umma_commit(&k_empty[s]);  // K slot free once these MMAs retire
       };
       issue_qk(0);
       for (int j = 0; j < n_tiles; ++j) {
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
           umma_commit(&o_done[mt]);
         }
-        umma_commit(&kv_empty[s]);
+        umma_commit(&v_empty[s]);
       }
     }
   } else if (warp >= 4) {
@@ -299,8 +317,23 @@ __global__ void __launch_bounds__(THREADS, 1)
     const bool warp_active = (rg + 128 * mt + 32 * wl) < GT;
     if (mt < nm && warp_active) {
       const bool valid = rho < GT;
+      const int t = valid ? rho / p.G : 0;
       const uint32_t lane_base = (uint32_t)(32 * wl) << 16;
       uint8_t* prow = smem + OFF_P + mt * P_BYTES;
+      // tree-row visibility of this query row (ancestors + self; j <= t)
+      uint32_t tmask[SD_MASK_WORDS];
+#pragma unroll
+      for (int w = 0; w < SD_MASK_WORDS; ++w) {
+        uint32_t bits = 0u;
+        const int lo = 32 * w;
+        if (lo <= t) {
+          bits = p.mask ? (w < p.mask_words ? p.mask[(int64_t)t * p.mask_words + w] : 0u) : 0xffffffffu;
+          const int lim = t - lo;  // keep j <= t
+          if (lim < 31) bits &= (2u << lim) - 1u;
+          if (lim < 32) bits |= 1u << lim;  // self
+        }
+        tmask[w] = bits;
+      }
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
         const int b = j & 1;
@@ -310,14 +343,34 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b), sr);
         tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b) + 32, sr + 32);
         tmem_wait_ld();
-        const int nvalid = min(BN, key_end - (key_begin + j * BN));
+        const int key0 = key_begin + j * BN;
+        // visibility bits of the 64 keys of this tile
+        uint64_t vis;
+        if (key0 + BN <= cache_end) {
+          vis = ~0ull;
+        } else {
+          vis = 0ull;
+#pragma unroll 4
+          for (int c = 0; c < 64; ++c) {
+            const int k = key0 + c;
+            bool on;
+            if (k < cache_end) {
+              on = true;
+            } else if (last && k < key_end) {
+              const int jt = k - p.ctx;
+              on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
+            } else {
+              on = false;
+            }
+            vis |= (uint64_t)on << c;
+          }
+        }
+        if (!valid) vis = 0ull;
         float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-          const float v = __uint_as_float(sr[c]) * LOG2E;
-          sr[c] = __float_as_uint(v);
-          if (c < nvalid) mx = fmaxf(mx, v);
-        }
+        for (int c = 0; c < 64; ++c)
+          if ((vis >> c) & 1ull) mx = fmaxf(mx, __uint_as_float(sr[c]));
+        mx *= LOG2E;
         float scale = 1.f;
         bool rescale = false;
         if (mx > m_used + TAU) {
@@ -328,10 +381,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         uint32_t pk[32];
         float rs = 0.f;
+        const float nm_used = -m_used;
 #pragma unroll
         for (int c = 0; c < 64; c += 2) {
-          const float p0 = (c < nvalid && valid) ? ex2(__uint_as_float(sr[c]) - m_used) : 0.f;
-          const float p1 = (c + 1 < nvalid && valid) ? ex2(__uint_as_float(sr[c + 1]) - m_used) : 0.f;
+          const float p0 = ((vis >> c) & 1ull) ? ex2(fmaf(__uint_as_float(sr[c]), LOG2E, nm_used)) : 0.f;
+          const float p1 = ((vis >> (c + 1)) & 1ull) ? ex2(fmaf(__uint_as_float(sr[c + 1]), LOG2E, nm_used)) : 0.f;
           rs += p0 + p1;
           pk[c >> 1] = pack_bf16(p0, p1);
         }
@@ -362,7 +416,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- epilogue: O / l, lse (natural log) ----
       mbar_wait(&o_done[mt], (n_tiles - 1) & 1);
       tc_fence_after();
-      const int t = rho / p.G, g = rho - t * p.G;
+      const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
       const float inv = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll
@@ -426,11 +480,11 @@ int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out)
 }
 
 int tc_n_chunks(int ctx, int Hk) {
-  // ~2 waves of one CTA per SM over (chunks x kv heads); >= 1 tile per chunk
-  int want = (2 * 148 + Hk - 1) / Hk;
+  // one wave of one CTA per SM over (chunks x kv heads); >= one tile per chunk
+  int want = 148 / Hk;
   const int max_by_tiles = (ctx + tc::BN - 1) / tc::BN;
   if (want > max_by_tiles) want = max_by_tiles;
-  if (want > 64) want = 64;
+  if (want > 148) want = 148;
   return want < 1 ? 1 : want;
 }
 
@@ -440,7 +494,8 @@ int tc_chunk_len(int ctx, int n) {
 }
 
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
-                     const int32_t* rows_dev, float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st) {
+                     const int32_t* rows_dev, const uint32_t* mask, int mask_words, float* ws_o, float* ws_lse,
+                     int n_chunks, int chunk, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
@@ -454,7 +509,10 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   p.layer = layer;
   p.ctx = ctx;
   p.chunk = chunk;
+  p.n_chunks = n_chunks;
   p.rows_dev = rows_dev;
+  p.mask = mask;
+  p.mask_words = mask_words;
   p.ws_o = ws_o;
   p.ws_lse = ws_lse;
   const int groups = (p.G * T + tc::ROWS - 1) / tc::ROWS;

@@ -156,13 +156,13 @@ def test_attention_rows_dev_padding(lib):
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
-def test_draft_attention_rank_rope_with_holes(lib, dtype):
+@pytest.mark.parametrize("H,Hk,dh,cap,hi", [(8, 2, 32, 300, 260), (32, 8, 128, 4200, 4100), (40, 8, 128, 700, 650),
+                                            (16, 16, 64, 300, 290)])
+def test_draft_attention_rank_rope_with_holes(lib, dtype, H, Hk, dh, cap, hi):
     dev = torch.device("cuda")
     g = np.random.default_rng(11)
-    H, Hk, dh, cap = 8, 2, 32, 300
-    hi = 260
     ranks = -np.ones(hi, dtype=np.int32)
-    live = np.sort(g.choice(hi, size=200, replace=False))
+    live = np.sort(g.choice(hi, size=int(hi * 0.8), replace=False))
     perm = g.permutation(len(live))
     ranks[live] = perm  # arbitrary rank per live slot
     Kraw = g.normal(size=(Hk, cap, dh))
@@ -192,6 +192,30 @@ def test_draft_attention_rank_rope_with_holes(lib, dtype):
     Kall = np.concatenate([Krot, kt.double().cpu().numpy().transpose(1, 0, 2)])
     Vall = np.concatenate([Vr, vt.double().cpu().numpy().transpose(1, 0, 2)])
     want = attend_oracle(qt.double().cpu().numpy(), Kall, Vall, np.ones((1, m + 1), dtype=bool))
+    tol = 1e-5 if dtype == torch.float32 else 2e-2
+    np.testing.assert_allclose(out.double().cpu().numpy().reshape(1, H, dh), want, rtol=tol, atol=tol)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("ctx", [1, 63, 5000, 54000])
+def test_decode_attention_full_cache(lib, dtype, ctx):
+    """T == 1 over the full cache (AR decode path) vs the oracle."""
+    dev = torch.device("cuda")
+    g = np.random.default_rng(ctx)
+    H, Hk, dh = 32, 8, 128
+    cap = ctx + 4
+    kt = torch.as_tensor(g.normal(size=(Hk, cap, dh)), dtype=dtype, device=dev)
+    vt = torch.as_tensor(g.normal(size=(Hk, cap, dh)), dtype=dtype, device=dev)
+    qt = torch.as_tensor(g.normal(size=(1, H, dh)) * 2 / np.sqrt(dh), dtype=dtype, device=dev)
+    out = torch.empty((1, H * dh), dtype=dtype, device=dev)
+    ws = torch.empty(lib.load().sd_attention_workspace_bytes(1, H, dh, ctx), dtype=torch.uint8, device=dev)
+    kd = lib.dcode(dtype)
+    lib.call("sd_attention", lib.ptr(qt), kd, 1, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
+             None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, None, None, None, 0,
+             lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+    Kr = kt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]
+    Vr = vt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]
+    want = attend_oracle(qt.double().cpu().numpy(), Kr, Vr, np.ones((1, ctx + 1), dtype=bool))
     tol = 1e-5 if dtype == torch.float32 else 2e-2
     np.testing.assert_allclose(out.double().cpu().numpy().reshape(1, H, dh), want, rtol=tol, atol=tol)
 
