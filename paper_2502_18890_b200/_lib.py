@@ -57,6 +57,7 @@ _SIGS = {
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P,
                            P, P, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
+    "sd_debug_tc_trace": (INT, [P]),
     "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
     "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
     "sd_select_workspace_bytes": (SZ, [INT, INT]),
@@ -115,7 +116,7 @@ def require_cuda():
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
-              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap"}
+              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_debug_tc_trace"}
 launch_count = 0
 
 

@@ -347,27 +347,46 @@ __global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
   }
 }
 
-// merge chunk partials in ascending chunk order -> out [T][H][DH]
+// merge chunk partials in ascending chunk order -> out [T][H][DH]. One CTA per
+// (t, head) row: the split weights exp(lse_c - max) are computed once into
+// shared memory, then every thread accumulates its dims with independent loads.
+constexpr int MERGE_MAX = 1024;
 template <int DH, typename OT>
 __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
                                   int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out) {
+  __shared__ float wsh[MERGE_MAX];
+  __shared__ float red[32];
   const int row = blockIdx.x;  // t * H + head
   if (rows_dev && row / H >= *rows_dev) {  // padded row: defined zeros
     for (int d = threadIdx.x; d < DH; d += blockDim.x) out[(int64_t)row * DH + d] = from_f<OT>(0.f);
     return;
   }
-  float M = -INFINITY;
-  for (int c = 0; c < nsplit; ++c) M = fmaxf(M, ws_lse[(int64_t)c * TH + row]);
+  float lm = -INFINITY;
+  for (int c = threadIdx.x; c < nsplit; c += blockDim.x) {
+    const float v = ws_lse[(int64_t)c * TH + row];
+    wsh[c] = v;
+    lm = fmaxf(lm, v);
+  }
+  const float M = block_reduce(lm, red, [](float a, float b) { return fmaxf(a, b); });
+  float ls = 0.f;
+  for (int c = threadIdx.x; c < nsplit; c += blockDim.x) {
+    const float w = wsh[c] == -INFINITY ? 0.f : __expf(wsh[c] - M);
+    wsh[c] = w;
+    ls += w;
+  }
+  const float L = block_reduce(ls, red, [](float a, float b) { return a + b; });  // syncs: wsh visible
+  const float inv = L > 0.f ? 1.f / L : 0.f;
   for (int d = threadIdx.x; d < DH; d += blockDim.x) {
-    float L = 0.f, O = 0.f;
-    for (int c = 0; c < nsplit; ++c) {
-      const float lse = ws_lse[(int64_t)c * TH + row];
-      if (lse == -INFINITY) continue;
-      const float w = __expf(lse - M);
-      L += w;
-      O += w * ws_o[((int64_t)c * TH + row) * DH + d];
+    float O0 = 0.f, O1 = 0.f, O2 = 0.f, O3 = 0.f;
+    int c = 0;
+    for (; c + 4 <= nsplit; c += 4) {
+      O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
+      O1 = fmaf(wsh[c + 1], ws_o[((int64_t)(c + 1) * TH + row) * DH + d], O1);
+      O2 = fmaf(wsh[c + 2], ws_o[((int64_t)(c + 2) * TH + row) * DH + d], O2);
+      O3 = fmaf(wsh[c + 3], ws_o[((int64_t)(c + 3) * TH + row) * DH + d], O3);
     }
-    out[(int64_t)row * DH + d] = from_f<OT>(L > 0.f ? O / L : 0.f);
+    for (; c < nsplit; ++c) O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
+    out[(int64_t)row * DH + d] = from_f<OT>(((O0 + O1) + (O2 + O3)) * inv);
   }
 }
 
@@ -414,17 +433,35 @@ static int dispatch_types(const AttnParams& p, int q_dtype, int kv_dtype, int ou
 // ------------------------------------------------------------------------
 // Single-row decode attention (draft over the partial cache, AR decode over
 // the full cache): T == 1, G <= 8 query heads per kv head. A CTA takes one
-// 64-key chunk of one kv head; each warp streams 16 keys with lanes over
-// head_dim (coalesced rows), 8 keys' loads in flight at a time, RoPE at the
-// slot's rank applied on load (kvcache.py:158-165), dot products reduced with
-// warp shuffles, online softmax per query head, then the 4 warps merge.
+// 64-key chunk of one kv head; each of its 4 warps streams 16 keys with lanes
+// over head_dim: the warp's ranks arrive in one coalesced load and are
+// broadcast by shuffles, then all 8 keys of a batch issue their K / V / cos /
+// sin loads (8-byte vectors) before any math, so a warp has one memory
+// round trip per batch. RoPE at the slot's rank is applied on load
+// (kvcache.py:158-165); dots are reduced with warp shuffles; online softmax
+// per query head; the 4 warps merge through shared memory.
 constexpr int DEC_CHUNK = 64;
 
-template <int DH, typename QT, typename KT, bool ROT>
-__global__ void __launch_bounds__(128) decode_attn_kernel(AttnParams p, int chunk) {
-  constexpr int EPL = DH / 32;  // elements per lane (DH >= 64 -> even)
-  constexpr int NB = 8;         // keys per load batch
-  __shared__ float Sm[4][8], Sl[4][8], So[4][8][DH];
+template <typename KT> struct Vec4;  // 4 consecutive elements
+template <> struct Vec4<__nv_bfloat16> {
+  using T = uint2;
+  __device__ static void unpack(const T& v, float* f) {
+    const __nv_bfloat162 a = *reinterpret_cast<const __nv_bfloat162*>(&v.x);
+    const __nv_bfloat162 b = *reinterpret_cast<const __nv_bfloat162*>(&v.y);
+    f[0] = __low2float(a); f[1] = __high2float(a); f[2] = __low2float(b); f[3] = __high2float(b);
+  }
+};
+template <> struct Vec4<float> {
+  using T = float4;
+  __device__ static void unpack(const T& v, float* f) { f[0] = v.x; f[1] = v.y; f[2] = v.z; f[3] = v.w; }
+};
+
+template <int DH, typename QT, typename KT, bool ROT, int GM>
+__global__ void __launch_bounds__(128, (GM == 4 && sizeof(KT) == 2) ? 4 : 2) decode_attn_kernel(AttnParams p, int chunk) {
+  static_assert(DH == 128, "decode kernel: lanes hold 4 consecutive elements");
+  constexpr int NB = 8;  // keys per load batch
+  using V4 = typename Vec4<KT>::T;
+  __shared__ float Sm[4][GM], Sl[4][GM], So[4][GM][DH];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kvh = blockIdx.y, G = p.G;
   const int cx = blockIdx.x;
@@ -443,89 +480,108 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(AttnParams p, int chun
     k_begin = cx * chunk;
     k_end = min(p.ctx, k_begin + chunk);
   }
-  // query rows of this kv head (T == 1): q[head = kvh*G + g]
-  float q[8][EPL];
+  const int per_warp = chunk / 4;
+  const int w0 = k_begin + warp * per_warp, w1 = min(k_end, w0 + per_warp);
+  // ranks of this warp's keys (<= 32 per warp)
+  int my_rank = 0;
+  if (ROT && !tree && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
+  float q[GM][4];
 #pragma unroll
-  for (int g = 0; g < 8; ++g)
+  for (int g = 0; g < GM; ++g) {
+    if (g < G) {
+      const QT* qp = (const QT*)p.q + (int64_t)(kvh * G + g) * DH + lane * 4;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e)
-      q[g][e] = g < G ? to_f(((const QT*)p.q)[(int64_t)(kvh * G + g) * DH + lane * EPL + e]) : 0.f;
-  float m[8], l[8], acc[8][EPL];
+      for (int e = 0; e < 4; ++e) q[g][e] = to_f(qp[e]);
+    } else {
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
+      for (int e = 0; e < 4; ++e) q[g][e] = 0.f;
+    }
+  }
+  float m[GM], l[GM], acc[GM][4];
+#pragma unroll
+  for (int g = 0; g < GM; ++g) {
     m[g] = -INFINITY;
     l[g] = 0.f;
 #pragma unroll
-    for (int e = 0; e < EPL; ++e) acc[g][e] = 0.f;
+    for (int e = 0; e < 4; ++e) acc[g][e] = 0.f;
   }
-  const int per_warp = (chunk + 3) / 4;
-  const int w0 = k_begin + warp * per_warp, w1 = min(k_end, w0 + per_warp);
   for (int kb = w0; kb < w1; kb += NB) {
-    float kr[NB][EPL], vr[NB][EPL];
+    V4 kv[NB], vv[NB];
+    float2 cs[NB][2];
     bool ok[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int k = kb + b;
-      ok[b] = k < w1;
-      int rk = 0;
-      if (ROT && !tree && ok[b]) {
-        rk = p.ranks[k];
-        ok[b] = rk >= 0;  // hole slot
-      }
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        kr[b][e] = ok[b] ? to_f(K[(int64_t)k * DH + lane * EPL + e]) : 0.f;
-        vr[b][e] = ok[b] ? to_f(V[(int64_t)k * DH + lane * EPL + e]) : 0.f;
-      }
-      if (ROT && !tree && ok[b]) {
-#pragma unroll
-        for (int e = 0; e < EPL; e += 2) {
-          const int i = (lane * EPL + e) >> 1;
-          const float c = p.cosT[(int64_t)rk * (DH / 2) + i], s = p.sinT[(int64_t)rk * (DH / 2) + i];
-          const float a = kr[b][e], bb = kr[b][e + 1];
-          kr[b][e] = a * c - bb * s;
-          kr[b][e + 1] = a * s + bb * c;
-        }
+      const int rk = __shfl_sync(0xffffffffu, my_rank, (k - w0) & 31);
+      ok[b] = k < w1 && (!ROT || tree || rk >= 0);
+      const int kk = k < w1 ? k : w0;  // in-bounds address for masked keys
+      kv[b] = *reinterpret_cast<const V4*>(K + (int64_t)kk * DH + lane * 4);
+      vv[b] = *reinterpret_cast<const V4*>(V + (int64_t)kk * DH + lane * 4);
+      if (ROT && !tree) {
+        const int64_t r = rk > 0 ? rk : 0;
+        cs[b][0] = *reinterpret_cast<const float2*>(p.cosT + r * (DH / 2) + lane * 2);
+        cs[b][1] = *reinterpret_cast<const float2*>(p.sinT + r * (DH / 2) + lane * 2);
       }
     }
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-      if (!__any_sync(0xffffffffu, ok[b])) continue;
+      float kf[4], vf[4];
+      Vec4<KT>::unpack(kv[b], kf);
+      Vec4<KT>::unpack(vv[b], vf);
+      if (ROT && !tree) {  // pairs (0,1) and (2,3) of this lane
+        const float a0 = kf[0], b0 = kf[1], a1 = kf[2], b1 = kf[3];
+        kf[0] = a0 * cs[b][0].x - b0 * cs[b][1].x;
+        kf[1] = a0 * cs[b][1].x + b0 * cs[b][0].x;
+        kf[2] = a1 * cs[b][0].y - b1 * cs[b][1].y;
+        kf[3] = a1 * cs[b][1].y + b1 * cs[b][0].y;
+      }
+      float sg[GM];
 #pragma unroll
-      for (int g = 0; g < 8; ++g) {
-        if (g >= G) break;
-        float s = 0.f;
+      for (int g = 0; g < GM; ++g) {
+        float s = q[g][0] * kf[0];
+        s = fmaf(q[g][1], kf[1], s);
+        s = fmaf(q[g][2], kf[2], s);
+        s = fmaf(q[g][3], kf[3], s);
+        sg[g] = s;
+      }
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) s = fmaf(q[g][e], kr[b][e], s);
-        s = warp_sum(s);
-        if (!ok[b]) continue;  // uniform across the warp (ok depends on the key only)
-        const float mn = fmaxf(m[g], s);
-        const float corr = __expf(m[g] - mn), pw = __expf(s - mn);
-        l[g] = l[g] * corr + pw;
-        m[g] = mn;
+      for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[g][e] = fmaf(acc[g][e], corr, pw * vr[b][e]);
+        for (int g = 0; g < GM; ++g) sg[g] += __shfl_xor_sync(0xffffffffu, sg[g], o);
+      if (!ok[b]) continue;  // warp-uniform
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        if (g < G) {
+          const float mn = fmaxf(m[g], sg[g]);
+          const float corr = __expf(m[g] - mn), pw = __expf(sg[g] - mn);
+          l[g] = l[g] * corr + pw;
+          m[g] = mn;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[g][e] = fmaf(acc[g][e], corr, pw * vf[e]);
+        }
       }
     }
   }
-  // merge the 4 warps
 #pragma unroll
-  for (int g = 0; g < 8; ++g) {
-    if (g >= G) break;
-    if (lane == 0) {
-      Sm[warp][g] = m[g];
-      Sl[warp][g] = l[g];
+  for (int g = 0; g < GM; ++g) {
+    if (g < G) {
+      if (lane == 0) {
+        Sm[warp][g] = m[g];
+        Sl[warp][g] = l[g];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) So[warp][g][lane * 4 + e] = acc[g][e];
     }
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) So[warp][g][lane * EPL + e] = acc[g][e];
   }
   __syncthreads();
   for (int i = tid; i < G * DH; i += 128) {
     const int g = i / DH, d = i - g * DH;
     float M = -INFINITY;
+#pragma unroll
     for (int w = 0; w < 4; ++w) M = fmaxf(M, Sm[w][g]);
     float L = 0.f, O = 0.f;
     if (M != -INFINITY) {
+#pragma unroll
       for (int w = 0; w < 4; ++w) {
         const float sc = __expf(Sm[w][g] - M);
         L += Sl[w][g] * sc;
@@ -550,10 +606,17 @@ static int launch_decode(AttnParams p, int src_kind, void* out, cudaStream_t st)
   p.n_chunks = p.ctx > 0 ? (p.ctx + chunk - 1) / chunk : 0;
   p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * p.H * DH;
   dim3 grid(p.n_chunks + 1, p.Hk);
-  if (src_kind)
-    decode_attn_kernel<DH, QT, KT, true><<<grid, 128, 0, st>>>(p, chunk);
-  else
-    decode_attn_kernel<DH, QT, KT, false><<<grid, 128, 0, st>>>(p, chunk);
+  if (p.G <= 4) {
+    if (src_kind)
+      decode_attn_kernel<DH, QT, KT, true, 4><<<grid, 128, 0, st>>>(p, chunk);
+    else
+      decode_attn_kernel<DH, QT, KT, false, 4><<<grid, 128, 0, st>>>(p, chunk);
+  } else {
+    if (src_kind)
+      decode_attn_kernel<DH, QT, KT, true, 8><<<grid, 128, 0, st>>>(p, chunk);
+    else
+      decode_attn_kernel<DH, QT, KT, false, 8><<<grid, 128, 0, st>>>(p, chunk);
+  }
   int rc = check_launch("sd_attention(decode)");
   if (rc) return rc;
   attn_merge_kernel<DH, OT><<<p.H, DH >= 128 ? 128 : DH, 0, st>>>(p.ws_o, p.ws_lse, p.n_chunks + 1, p.H, p.H,
@@ -574,6 +637,7 @@ static int dispatch_decode(const AttnParams& p, int q_dtype, int kv_dtype, int o
 }
 
 int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
+int tc_set_trace(void* dev_ptr);
 int tc_n_chunks(int ctx, int Hk);
 int tc_chunk_len(int ctx, int n);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
@@ -606,6 +670,8 @@ size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
   return ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
 }
 
+int sd_debug_tc_trace(void* trace_dev) { return tc_set_trace(trace_dev); }
+
 int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host) {
   SD_REQUIRE(base && tmap_out_host && dh == 128 && L > 0 && Hk > 0 && cap > 0, "sd_make_kv_tmap: args");
   return tc_make_kv_tmap(base, L, Hk, cap, dh, tmap_out_host);
@@ -623,6 +689,7 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   SD_REQUIRE(!mask_bits || mask_words * 32 >= T, "sd_attention: mask words");
   SD_REQUIRE(src_kind == 0 || (ranks && rope_cos && rope_sin), "sd_attention: partial source needs ranks/rope");
   SD_REQUIRE(workspace_bytes >= sd_attention_workspace_bytes(T, H, dh, ctx), "sd_attention: workspace too small");
+  SD_REQUIRE(ctx <= 256 * 8192, "sd_attention: ctx too large for the merge split limit");
   AttnParams p;
   p.q = q;
   p.T = T;
@@ -661,10 +728,9 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
                                                                   (__nv_bfloat16*)out);
     return check_launch("sd_attention(tc merge)");
   }
-  if (T == 1 && p.G <= 8 && (dh == 64 || dh == 128) && !rows_dev) {
+  if (T == 1 && p.G <= 8 && dh == 128 && !rows_dev) {
     // single-row decode (draft / AR): latency-tolerant streaming kernel
-    if (dh == 128) return dispatch_decode<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
-    return dispatch_decode<64>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
+    return dispatch_decode<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
   }
   switch (dh) {
     case 8: return dispatch_types<8>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);

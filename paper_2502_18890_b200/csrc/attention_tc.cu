@@ -65,6 +65,15 @@ struct Params {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+// Debug-only event timeline of CTA (0, 0, 0) (sd_debug_tc_trace); NULL in production.
+__device__ int64_t* g_tc_trace = nullptr;
+constexpr int TR_TILES = 64, TR_EV = 8;
+__device__ __forceinline__ void trace(int role, int j, int ev) {
+  int64_t* t = g_tc_trace;
+  if (t && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TR_TILES)
+    t[(role * TR_TILES + j) * TR_EV + ev] = clock64();
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -252,12 +261,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
         const int key0 = key_begin + j * BN;
+        trace(0, j, 0);
         if (j >= ST) mbar_wait(&k_empty[s], ((j / ST) + 1) & 1);
+        trace(0, j, 1);
         uint8_t* kd = smem + OFF_K + s * KV_TILE;
         mbar_expect_tx(&k_full[s], KV_TILE);
         tma_load_4d(kd, &tmap_k, &k_full[s], 0, key0, kvh, p.layer);
         tma_load_4d(kd + KV_TILE / 2, &tmap_k, &k_full[s], 64, key0, kvh, p.layer);
         if (j >= ST) mbar_wait(&v_empty[s], ((j / ST) + 1) & 1);
+        trace(0, j, 2);
         uint8_t* vd = smem + OFF_V + s * KV_TILE;
         mbar_expect_tx(&v_full[s], KV_TILE);
         tma_load_4d(vd, &tmap_v, &v_full[s], 0, key0, kvh, p.layer);
@@ -272,7 +284,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t q_base = smem_u32(smem + OFF_Q);
       auto issue_qk = [&](int j) {
         const int s = j % ST, b = j & 1;
+        trace(1, j, 0);
         mbar_wait(&k_full[s], (j / ST) & 1);
+        trace(1, j, 1);
         tc_fence_after();
         const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
         for (int mt = 0; mt < nm; ++mt) {
@@ -291,10 +305,13 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < n_tiles; ++j) {
         if (j + 1 < n_tiles) issue_qk(j + 1);
         const int s = j % ST;
+        trace(1, j, 2);
         mbar_wait(&v_full[s], (j / ST) & 1);
+        trace(1, j, 3);
         const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
         for (int mt = 0; mt < nm; ++mt) {
           mbar_wait(&p_full[mt], j & 1);
+          trace(1, j, 4 + mt);
           tc_fence_after();
           const uint32_t p_base = smem_u32(smem + OFF_P + mt * P_BYTES);
 #pragma unroll
@@ -337,7 +354,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
         const int b = j & 1;
+        const int role = (lane == 0 && wl == 0) ? 2 + mt : 99;
+        if (role < 4) trace(role, j, 0);
         mbar_wait(&s_full[2 * mt + b], (j >> 1) & 1);
+        if (role < 4) trace(role, j, 1);
         tc_fence_after();
         uint32_t sr[64];
         tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b), sr);
@@ -390,7 +410,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           pk[c >> 1] = pack_bf16(p0, p1);
         }
         l += rs;
+        if (role < 4) trace(role, j, 2);
         if (j > 0) mbar_wait(&o_done[mt], (j - 1) & 1);  // PV(j-1) done: P free, O stable
+        if (role < 4) trace(role, j, 3);
         if (__any_sync(0xffffffffu, rescale)) {
           tc_fence_after();
 #pragma unroll
@@ -412,6 +434,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         fence_async_smem();
         tc_fence_before();
         mbar_arrive(&p_full[mt]);
+        if (role < 4) trace(role, j, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
       mbar_wait(&o_done[mt], (n_tiles - 1) & 1);
@@ -477,6 +500,11 @@ int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out)
     return SD_ECUDA;
   }
   return SD_OK;
+}
+
+int tc_set_trace(void* dev_ptr) {
+  cudaError_t e = cudaMemcpyToSymbol(tc::g_tc_trace, &dev_ptr, sizeof(void*));
+  return e == cudaSuccess ? SD_OK : SD_ECUDA;
 }
 
 int tc_n_chunks(int ctx, int Hk) {

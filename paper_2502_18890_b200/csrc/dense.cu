@@ -32,10 +32,59 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const T* __restric
   for (int i = threadIdx.x; i < d; i += blockDim.x) h[(int64_t)t * d + i] = to_f(row[i]);
 }
 
-// one block per row: h += delta; x = h * gain / sqrt(mean(h^2) + eps)
+// one block per row: h += delta; x = h * gain / sqrt(mean(h^2) + eps).
+// float4 vectors: every thread issues its loads before the reduction.
 template <typename XT>
+__device__ __forceinline__ void store4(XT* x, int64_t i, float a, float b, float c, float d);
+template <>
+__device__ __forceinline__ void store4<float>(float* x, int64_t i, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(x + i) = make_float4(a, b, c, d);
+}
+template <>
+__device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* x, int64_t i, float a, float b, float c,
+                                                      float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 v;
+  v.x = *reinterpret_cast<uint32_t*>(&lo);
+  v.y = *reinterpret_cast<uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(x + i) = v;
+}
+
+template <typename XT, int PER>
 __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
                                    const float* __restrict__ gain, float eps, XT* __restrict__ x) {
+  __shared__ float red[32];
+  const int64_t base = (int64_t)blockIdx.x * d;
+  float4 v[PER];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = (threadIdx.x + k * blockDim.x) * 4;
+    if (i < d) {
+      v[k] = *reinterpret_cast<const float4*>(h + base + i);
+      if (delta) {
+        const float4 dd = *reinterpret_cast<const float4*>(delta + base + i);
+        v[k].x += dd.x; v[k].y += dd.y; v[k].z += dd.z; v[k].w += dd.w;
+        *reinterpret_cast<float4*>(h + base + i) = v[k];
+      }
+      ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+    }
+  }
+  ss = block_reduce(ss, red, [](float a, float b) { return a + b; });
+  const float inv = rsqrtf(ss / (float)d + eps);
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = (threadIdx.x + k * blockDim.x) * 4;
+    if (i < d) {
+      const float4 g = *reinterpret_cast<const float4*>(gain + i);
+      store4<XT>(x, base + i, v[k].x * (g.x * inv), v[k].y * (g.y * inv), v[k].z * (g.z * inv), v[k].w * (g.w * inv));
+    }
+  }
+}
+
+template <typename XT>
+__global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
+                                          const float* __restrict__ gain, float eps, XT* __restrict__ x) {
   __shared__ float red[32];
   const int64_t base = (int64_t)blockIdx.x * d;
   float ss = 0.f;
@@ -70,7 +119,19 @@ __global__ void add_cast_kernel(const float* __restrict__ a, const float* __rest
   }
 }
 
-// grid: T rows; threads over (head, pair) for H q-heads + 2 Hk kv-heads.
+// grid: T rows; each thread rotates 2 adjacent pairs (4 elements) of one
+// q/k head, or copies 4 elements of v.
+template <typename T>
+__device__ __forceinline__ void put2(T* p, float a, float b);
+template <>
+__device__ __forceinline__ void put2<float>(float* p, float a, float b) {
+  *reinterpret_cast<float2*>(p) = make_float2(a, b);
+}
+template <>
+__device__ __forceinline__ void put2<__nv_bfloat16>(__nv_bfloat16* p, float a, float b) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(a, b);
+}
+
 template <typename QT, typename KT>
 __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, int dh,
                                   const int32_t* __restrict__ positions, const float* __restrict__ cosT,
@@ -84,37 +145,36 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   const int width = (H + 2 * Hk) * dh;
   const float* row = qkv + (int64_t)t * width;
   const int64_t pos = positions[t];
-  const float* cs = cosT + pos * half;
-  const float* sn = sinT + pos * half;
   const int64_t dst_row = row_offset + t;
-  const int pairs = (H + Hk) * half;  // rotated heads (q then k)
-  for (int i = threadIdx.x; i < pairs; i += blockDim.x) {
-    const int head = i / half, j = i - head * half;
-    const float a = row[head * dh + 2 * j], b = row[head * dh + 2 * j + 1];
-    const float c = cs[j], s = sn[j];
-    const float ra = a * c - b * s, rb = a * s + b * c;
-    if (head < H) {
-      const int64_t o = ((int64_t)t * H + head) * dh + 2 * j;
-      q_rot[o] = from_f<QT>(ra * q_scale);
-      q_rot[o + 1] = from_f<QT>(rb * q_scale);
-      if (q_pre) {
-        q_pre[o] = a;
-        q_pre[o + 1] = b;
+  const int quads_rot = (H + Hk) * dh / 4, quads_all = width / 4;
+  for (int u = threadIdx.x; u < quads_all; u += blockDim.x) {
+    const float4 x = *reinterpret_cast<const float4*>(row + 4 * u);
+    const int col = 4 * u, head = col / dh, e = col - head * dh;
+    if (u < quads_rot) {
+      const int j = e >> 1;  // pair index of x.x/x.y; x.z/x.w is j + 1
+      const float2 c = *reinterpret_cast<const float2*>(cosT + pos * half + j);
+      const float2 s = *reinterpret_cast<const float2*>(sinT + pos * half + j);
+      const float r0 = x.x * c.x - x.y * s.x, r1 = x.x * s.x + x.y * c.x;
+      const float r2 = x.z * c.y - x.w * s.y, r3 = x.z * s.y + x.w * c.y;
+      if (head < H) {
+        const int64_t o = ((int64_t)t * H + head) * dh + e;
+        put2<QT>(q_rot + o, r0 * q_scale, r1 * q_scale);
+        put2<QT>(q_rot + o + 2, r2 * q_scale, r3 * q_scale);
+        if (q_pre) *reinterpret_cast<float4*>(q_pre + o) = x;
+      } else {
+        const int64_t o = (head - H) * head_stride + dst_row * dh + e;
+        put2<KT>(k_rot + o, r0, r1);
+        put2<KT>(k_rot + o + 2, r2, r3);
+        if (k_raw) {
+          put2<KT>(k_raw + o, x.x, x.y);
+          put2<KT>(k_raw + o + 2, x.z, x.w);
+        }
       }
     } else {
-      const int kh = head - H;
-      const int64_t o = kh * head_stride + dst_row * dh + 2 * j;
-      k_rot[o] = from_f<KT>(ra);
-      k_rot[o + 1] = from_f<KT>(rb);
-      if (k_raw) {
-        k_raw[o] = from_f<KT>(a);
-        k_raw[o + 1] = from_f<KT>(b);
-      }
+      const int64_t o = (head - H - Hk) * head_stride + dst_row * dh + e;
+      put2<KT>(v + o, x.x, x.y);
+      put2<KT>(v + o + 2, x.z, x.w);
     }
-  }
-  for (int i = threadIdx.x; i < Hk * dh; i += blockDim.x) {
-    const int kh = i / dh, e = i - kh * dh;
-    v[kh * head_stride + dst_row * dh + e] = from_f<KT>(row[(H + Hk) * dh + i]);
   }
 }
 
@@ -148,14 +208,26 @@ int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, 
 int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain, float eps, void* x, int x_dtype,
                    sd_stream_t stream) {
   SD_REQUIRE(T > 0 && d > 0, "sd_add_rmsnorm: bad sizes");
+  SD_REQUIRE(x_dtype == SD_BF16 || x_dtype == SD_F32, "sd_add_rmsnorm: dtype");
   auto st = as_stream(stream);
-  const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
-  if (x_dtype == SD_BF16)
-    add_rmsnorm_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x);
-  else if (x_dtype == SD_F32)
-    add_rmsnorm_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x);
-  else
-    SD_REQUIRE(false, "sd_add_rmsnorm: dtype");
+  if (d % 4 == 0 && d <= 4 * 1024 * 2) {
+    const int quads = d / 4;
+    const int threads = quads >= 1024 ? 1024 : ((quads + 31) / 32) * 32;
+    const bool two = quads > threads;
+#define SD_NORM(XT, PER) add_rmsnorm_kernel<XT, PER><<<T, threads, 0, st>>>(h, delta, d, gain, eps, (XT*)x)
+    if (x_dtype == SD_BF16) {
+      if (two) SD_NORM(__nv_bfloat16, 2); else SD_NORM(__nv_bfloat16, 1);
+    } else {
+      if (two) SD_NORM(float, 2); else SD_NORM(float, 1);
+    }
+#undef SD_NORM
+  } else {
+    const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
+    if (x_dtype == SD_BF16)
+      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x);
+    else
+      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x);
+  }
   return check_launch("sd_add_rmsnorm");
 }
 
@@ -184,10 +256,10 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
                   const float* rope_sin, float q_scale, void* q_rot, int q_dtype, float* q_pre, void* k_raw,
                   void* k_rot, void* v, int kv_dtype, int64_t head_stride, int64_t row_offset,
                   const int32_t* rows_dev, sd_stream_t stream) {
-  SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 2) == 0, "sd_rope_stage: bad sizes");
+  SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 4) == 0, "sd_rope_stage: head_dim must be a multiple of 4");
   auto st = as_stream(stream);
 #define SD_RS(QT, KT)                                                                                          \
-  rope_stage_kernel<QT, KT><<<T, 256, 0, st>>>(qkv, H, Hk, dh, positions, rope_cos, rope_sin, q_scale, (QT*)q_rot, \
+  rope_stage_kernel<QT, KT><<<T, 512, 0, st>>>(qkv, H, Hk, dh, positions, rope_cos, rope_sin, q_scale, (QT*)q_rot, \
                                               q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev)
   if (q_dtype == SD_F32 && kv_dtype == SD_F32)
     SD_RS(float, float);

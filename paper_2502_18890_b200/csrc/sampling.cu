@@ -196,9 +196,29 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   auto max_op = [](double x, double y) { return fmax(x, y); };
 
   // ---- penalised softmax (or given probabilities) ----
-  double m = 0.0, Z = 1.0;
+  // fp64 logits (API path): fp64 throughout, like the reference.
+  // fp32 logits (engine path): fp32 scaled logits and expf, fp64 sums.
+  constexpr bool FAST = IN == SD_IN_LOGITS_F32;
+  double m = 0.0, Z = 1.0, invZ = 1.0;
+  float mf = 0.f;
+  const float inv_t = (float)(1.0 / a.temperature), inv_tt = (float)(1.0 / (a.temperature * a.theta));
+  const float th = (float)a.theta;
+  auto scaled_f = [&](int v) -> float {
+    const float l = ((const float*)in)[base + v];
+    if (!is_member(a, rc, row, v)) return l * inv_t;
+    if (a.ctrl_style) return (l < 0.f ? l * th : l / th) * inv_t;
+    return l * inv_tt;
+  };
   const bool is_probs = IN == SD_IN_PROBS_F64;
-  if (!is_probs) {
+  if (FAST) {
+    float lm = -INFINITY;
+    for (int v = tid; v < V; v += SMP_THREADS) lm = fmaxf(lm, scaled_f(v));
+    mf = block_reduce(lm, (float*)dred, [](float x, float y) { return fmaxf(x, y); });
+    double lz = 0.0;
+    for (int v = tid; v < V; v += SMP_THREADS) lz += (double)expf(scaled_f(v) - mf);
+    Z = block_reduce(lz, dred, sum_op);
+    invZ = 1.0 / Z;
+  } else if (!is_probs) {
     double lm = -INFINITY;
     for (int v = tid; v < V; v += SMP_THREADS) lm = fmax(lm, scaled(load_in<IN>(in, base + v), is_member(a, rc, row, v), a));
     m = block_reduce(lm, dred, max_op);
@@ -208,6 +228,7 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   }
   auto prob = [&](int v) -> double {
     if (is_probs) return load_in<IN>(in, base + v);
+    if (FAST) return (double)expf(scaled_f(v) - mf) * invZ;
     const double s = scaled(load_in<IN>(in, base + v), is_member(a, rc, row, v), a);
     const double e = exp(s - m);
     return e / Z;
@@ -222,7 +243,10 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   double pstar = -1.0;
   int vcut = -1, only = -1;
   const int tk = a.trunc_kind;
-  if (tk == SD_TRUNC_MIN_P || tk == SD_TRUNC_ETA || tk == SD_TRUNC_TOP_P) {
+  if (tk == SD_TRUNC_MIN_P && !is_probs) {
+    // p_max = exp(0) / Z: no pass needed (sampling.py:207)
+    thr = a.trunc_value * (FAST ? invZ : 1.0 / Z);
+  } else if (tk == SD_TRUNC_MIN_P || tk == SD_TRUNC_ETA || tk == SD_TRUNC_TOP_P) {
     // pmax and argmax (lowest index)
     DI best{-1.0, 0x7fffffff};
     for (int v = tid; v < V; v += SMP_THREADS) best = better(best, DI{prob(v), v});
@@ -371,48 +395,65 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   }
 }
 
-// draft per-head top-w: one CTA per head; rank by exp(s - m) (the penalised
-// probability up to the shared 1/Z), ties to the lower id.
+// draft per-head top-w (engine.py:207-215): one CTA per head, one pass over
+// the vocabulary. Candidates are ranked by the penalised scaled logit s
+// (exp(s - m) / Z is monotone in s), ties to the lower id. Each thread keeps a
+// sorted top-W list; W rounds of block argmax then pick the head's top-w.
+template <int W>
 __global__ void __launch_bounds__(SMP_THREADS) draft_topw_kernel(const float* __restrict__ logits, int V,
                                                                  const int32_t* __restrict__ cnt, double t,
-                                                                 double theta, int ctrl, SampleDev a0, int off0,
-                                                                 int w0, int w1, int w2, int w3, int w4, int w5,
-                                                                 int w6, int w7, int32_t* __restrict__ out) {
-  __shared__ double dred[32];
+                                                                 double theta, int ctrl, int w0, int w1, int w2,
+                                                                 int w3, int w4, int w5, int w6, int w7,
+                                                                 int32_t* __restrict__ out) {
   __shared__ DI ared[32];
-  __shared__ int chosen[16];
   const int head = blockIdx.x, tid = threadIdx.x;
   const int ws[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
   int off = 0;
   for (int k = 0; k < head; ++k) off += ws[k];
   const int w = ws[head];
   const float* row = logits + (int64_t)head * V;
-  SampleDev a = a0;
-  a.temperature = t;
-  a.theta = theta;
-  a.ctrl_style = ctrl;
-  auto s_of = [&](int v) -> double {
-    const bool mem = cnt != nullptr && cnt[v] > 0;
-    return scaled((double)row[v], mem, a);
-  };
-  double lm = -INFINITY;
-  for (int v = tid; v < V; v += SMP_THREADS) lm = fmax(lm, s_of(v));
-  const double m = block_reduce(lm, dred, [](double x, double y) { return fmax(x, y); });
-  for (int j = 0; j < w; ++j) {
-    DI best{-1.0, 0x7fffffff};
-    for (int v = tid; v < V; v += SMP_THREADS) {
-      bool taken = false;
-      for (int i = 0; i < j; ++i) taken |= chosen[i] == v;
-      if (!taken) best = better(best, DI{exp(s_of(v) - m), v});
-    }
-    best = block_argmax(best, ared);
-    if (tid == 0) {
-      chosen[j] = best.i;
-      out[off + j] = best.i;
-    }
-    __syncthreads();
+  const double inv_t = 1.0 / t, inv_tt = 1.0 / (t * theta);
+  double bv[W];
+  int bi[W];
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    bv[k] = -INFINITY;
+    bi[k] = 0x7fffffff;
   }
-  (void)off0;
+  for (int v = tid; v < V; v += SMP_THREADS) {
+    const double l = (double)row[v];
+    const bool mem = cnt != nullptr && cnt[v] > 0;
+    double sv;
+    if (!mem) sv = l * inv_t;
+    else if (ctrl) sv = (l < 0.0 ? l * theta : l / theta) * inv_t;
+    else sv = l * inv_tt;
+    // v increases within a thread: ties keep the earlier (lower) id
+    if (sv > bv[W - 1]) {
+      double cv = sv;
+      int ci = v;
+#pragma unroll
+      for (int k = 0; k < W; ++k) {
+        if (cv > bv[k]) {
+          const double tv = bv[k];
+          const int ti = bi[k];
+          bv[k] = cv;
+          bi[k] = ci;
+          cv = tv;
+          ci = ti;
+        }
+      }
+    }
+  }
+  int head_pos = 0;
+  for (int j = 0; j < w; ++j) {
+    DI mine{-INFINITY, 0x7fffffff};
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (k == head_pos) mine = DI{bv[k], bi[k]};
+    const DI best = block_argmax(mine, ared);
+    if (best.i == mine.i && best.v == mine.v) ++head_pos;
+    if (tid == 0) out[off + j] = best.i;
+  }
 }
 
 static SampleDev to_dev(const sd_sample_args& h) {
@@ -473,14 +514,18 @@ int sd_draft_topw(const float* logits, int heads, int V, const int32_t* win_coun
                   int ctrl_style, const int32_t* widths_host, int32_t* out, sd_stream_t stream) {
   SD_REQUIRE(heads > 0 && heads <= SD_TREE_MAX_DEPTH && V > 0, "sd_draft_topw: sizes");
   int w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int wmax = 0;
   for (int k = 0; k < heads; ++k) {
     SD_REQUIRE(widths_host[k] >= 1 && widths_host[k] <= 16 && widths_host[k] <= V, "sd_draft_topw: width");
     w[k] = widths_host[k];
+    wmax = w[k] > wmax ? w[k] : wmax;
   }
-  SampleDev a{};
-  draft_topw_kernel<<<heads, SMP_THREADS, 0, as_stream(stream)>>>(logits, V, win_count, temperature, theta,
-                                                                  ctrl_style, a, 0, w[0], w[1], w[2], w[3], w[4],
-                                                                  w[5], w[6], w[7], out);
+  auto st = as_stream(stream);
+#define SD_TOPW(W) draft_topw_kernel<W><<<heads, SMP_THREADS, 0, st>>>(logits, V, win_count, temperature, theta, \
+                                                                       ctrl_style, w[0], w[1], w[2], w[3], w[4], \
+                                                                       w[5], w[6], w[7], out)
+  if (wmax <= 4) SD_TOPW(4); else if (wmax <= 8) SD_TOPW(8); else SD_TOPW(16);
+#undef SD_TOPW
   return check_launch("sd_draft_topw");
 }
 

@@ -1,0 +1,57 @@
+"""Debug: event timeline of the tcgen05 verification kernel's first CTA.
+
+    python tools/tc_trace.py [ctx] [T]
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2502_18890_b200 import FullCache, _lib as L  # noqa: E402
+from paper_2502_18890_b200.model import mask_bits_from_bool  # noqa: E402
+
+ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 54096
+T = int(sys.argv[2]) if len(sys.argv) > 2 else 41
+H, Hk, dh = 32, 8, 128
+F = FullCache(1, Hk, dh, capacity=ctx + T + 64, dtype=torch.bfloat16)
+F.k_rot.normal_()
+F.v.normal_()
+q = (torch.randn((T, H, dh), device="cuda") * 0.1).to(torch.bfloat16)
+bits = torch.as_tensor(mask_bits_from_bool(np.tril(np.ones((T, T), dtype=bool))), device="cuda")
+out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
+ws = torch.empty(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+tr = torch.zeros((4, 64, 8), dtype=torch.int64, device="cuda")
+
+
+def run():
+    L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
+           None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
+           L.MASK_WORDS, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
+
+
+for _ in range(3):
+    run()
+L.call("sd_debug_tc_trace", L.ptr(tr))
+run()
+torch.cuda.synchronize()
+L.call("sd_debug_tc_trace", None)
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(10):
+    run()
+e1.record()
+torch.cuda.synchronize()
+print(f"ctx={ctx} T={T}: {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call")
+t = tr.cpu().numpy()
+base = t[t > 0].min()
+names = {0: ["k_empty?", "k_empty ok", "v_empty ok"], 1: ["qk wait", "k_full ok", "v wait", "v_full ok", "p0 ok", "p1 ok"],
+         2: ["s wait", "s ok", "exp done", "o_done ok", "p arrive"], 3: ["s wait", "s ok", "exp done", "o_done ok", "p arrive"]}
+for j in list(range(0, 6)) + list(range(20, 24)):
+    row = []
+    for role in range(4):
+        for ev, nm in enumerate(names[role]):
+            v = t[role, j, ev]
+            if v:
+                row.append(f"{['P', 'M', 'S0', 'S1'][role]}.{nm}={v - base}")
+    print(f"tile {j:2d}: " + "  ".join(row))
