@@ -10,15 +10,18 @@
 //   warp 0      TMA producer: K and V tiles of 64 keys x 128 dh (two 128-byte
 //               swizzled boxes each) into separate 4-deep rings (mbarrier
 //               tx-count); K slots free as soon as S = QK^T retires;
-//   warp 1      MMA issuer (one thread): S = Q K^T (M=128, N=64, K=16 steps)
-//               into TMEM, double-buffered, one tile ahead; O += P V (M=128,
-//               N=128, V consumed MN-major straight from the TMA layout);
-//   warp 2      TMEM allocator (512 columns: S[2 mtiles][2 bufs] x 64 + O[2] x 128);
+//   warp 1      MMA issuer (one thread), per 32-key sub-tile u and M-tile:
+//               S[u%2] = Q K^T (M=128, N=32, A = Q from TMEM, B = K from
+//               smem) issued one sub-tile ahead; O += P V (M=128, N=128,
+//               A = P from TMEM, B = V from smem, MN-major straight from the
+//               TMA layout). Only one operand of each MMA is read from
+//               shared memory, so the tensor core is not smem-bound;
+//   warp 2      TMEM allocator (512 columns);
 //   warps 4-11  two softmax warpgroups, one per 128-row M-tile: thread = row =
-//               TMEM lane; online softmax in base 2 with lazy rescale (O in
-//               TMEM is rescaled only when the row max grows by > 2^8), P
-//               written to shared memory in the UMMA K-major SW128 layout.
-// Q (pre-rotated, pre-scaled by 1/sqrt(dh)) is staged once per CTA.
+//               TMEM lane; Q staged into TMEM once; online softmax in base 2
+//               with lazy rescale (O in TMEM is rescaled only when the row
+//               max grows by > 2^8); P written back into TMEM (tcgen05.st).
+// Q is pre-rotated and pre-scaled by 1/sqrt(dh).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -35,21 +38,21 @@ constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 
-constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][half][128 rows][128 B]
-constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [half][64 rows][128 B]
-constexpr int P_BYTES = 128 * BN * 2;           // 16 KB per M-tile: [128 rows][128 B]
-constexpr int OFF_Q = 0;
-constexpr int OFF_K = OFF_Q + Q_BYTES;
+constexpr int SUB = 32;         // keys per MMA sub-tile (S double-buffered per M-tile)
+constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [dh half][64 rows][128 B]
+constexpr int OFF_K = 0;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
-constexpr int OFF_P = OFF_V + ST * KV_TILE;
-constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+constexpr int OFF_BAR = OFF_V + ST * KV_TILE;
 constexpr int N_BAR = 4 * ST + 4 + 2 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
-// TMEM columns
-constexpr uint32_t COL_S = 0;    // S[mt][buf] at 64 * (2 mt + buf)
-constexpr uint32_t COL_O = 256;  // O[mt] at 256 + 128 mt
+// TMEM columns (512): O[mt] fp32 128 each, Q[mt] bf16x2 64 each (TMEM A
+// operand), S[mt][buf] fp32 32 each; P[mt][buf] (bf16x2, TMEM A operand of
+// O += P V) overwrites the first 16 columns of the S buffer it came from.
+constexpr uint32_t COL_O = 0;
+constexpr uint32_t COL_Q = 256;
+constexpr uint32_t COL_S = 384;
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
@@ -134,6 +137,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t 
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// A operand from TMEM (K-major: row = lane, 2 bf16 per 32-bit column)
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc,
+                                             uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
@@ -166,6 +178,12 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
 }
 
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+               : "memory");
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                           Params p) {
@@ -192,6 +210,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int cache_end = min(p.ctx, key_begin + p.chunk);
   const int key_end = last ? p.ctx + T : cache_end;  // the last chunk also takes the tree rows
   const int n_tiles = (key_end - key_begin + BN - 1) / BN;
+  const int n_sub = (key_end - key_begin + SUB - 1) / SUB;
   int act[2];
   for (int mt = 0; mt < 2; ++mt) {
     int a = 0;
@@ -200,33 +219,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const int nm = act[1] > 0 ? 2 : 1;
 
-  // ---- stage Q (two M-tiles, K-major SW128): all loads in flight, then stores ----
-  {
-    constexpr int PER = (ROWS * (DH / 8) + THREADS - 1) / THREADS;  // 16-byte chunks per thread
-    uint4 v[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = tid + k * THREADS;
-      const int row = i >> 4, c = i & 15;
-      const int rho = rg + row;
-      v[k] = make_uint4(0, 0, 0, 0);
-      if (i < ROWS * 16 && rho < GT) {
-        const int t = rho / p.G, g = rho - t * p.G;
-        v[k] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = tid + k * THREADS;
-      if (i < ROWS * 16) {
-        const int row = i >> 4, c = i & 15;
-        const int mt = row >> 7, r = row & 127, half = c >> 3;
-        *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v[k];
-      }
-    }
-    for (int i = tid; i < 2 * P_BYTES / 16; i += THREADS)
-      *reinterpret_cast<uint4*>(smem + OFF_P + i * 16) = make_uint4(0, 0, 0, 0);
-  }
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&k_full[s], 1);
@@ -247,11 +239,33 @@ __global__ void __launch_bounds__(THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+
+  // ---- softmax threads stage their query row into TMEM (A operand of S = Q K^T) ----
+  if (warp >= 4) {
+    const int mt = (warp - 4) >> 2, wl = warp & 3;
+    const int rho = rg + 128 * mt + 32 * wl + lane;
+    uint4 qv[16];
+    if (rho < GT) {
+      const int t = rho / p.G, g = rho - t * p.G;
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH);
+#pragma unroll
+      for (int c = 0; c < 16; ++c) qv[c] = __ldg(src + c);
+    } else {
+#pragma unroll
+      for (int c = 0; c < 16; ++c) qv[c] = make_uint4(0, 0, 0, 0);
+    }
+    const uint32_t ta = tmem + ((uint32_t)(32 * wl) << 16) + COL_Q + 64 * mt;
+    tmem_st32(ta, reinterpret_cast<const uint32_t*>(qv));
+    tmem_st32(ta + 32, reinterpret_cast<const uint32_t*>(qv + 8));
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {
     // ================= TMA producer: K(j), V(j) in order, separate rings =================
@@ -277,53 +291,54 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer =================
+    // ================= MMA issuer (32-key sub-tiles u) =================
     if (lane == 0) {
-      const uint32_t id_qk = idesc_bf16(BN, false);
+      const uint32_t id_qk = idesc_bf16(SUB, false);
       const uint32_t id_pv = idesc_bf16(DH, true);
-      const uint32_t q_base = smem_u32(smem + OFF_Q);
-      auto issue_qk = [&](int j) {
-        const int s = j % ST, b = j & 1;
-        trace(1, j, 0);
-        mbar_wait(&k_full[s], (j / ST) & 1);
-        trace(1, j, 1);
-        tc_fence_after();
-        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
+      auto issue_qk = [&](int u) {
+        const int j = u >> 1, h = u & 1, s = j % ST, b = u & 1;
+        if (h == 0) {
+          trace(1, j, 0);
+          mbar_wait(&k_full[s], (j / ST) & 1);
+          trace(1, j, 1);
+          tc_fence_after();
+        }
+        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE) + h * SUB * 128;
         for (int mt = 0; mt < nm; ++mt) {
 #pragma unroll
           for (int ks = 0; ks < DH / 16; ++ks) {
             const uint32_t half = ks >> 2, in = (ks & 3) * 32;
-            const uint64_t a = umma_desc(q_base + mt * 32768 + half * 16384 + in, 16, 1024);
             const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
-            umma_bf16(tmem + COL_S + 64 * (2 * mt + b), a, bd, id_qk, ks > 0);
+            umma_bf16_ts(tmem + COL_S + 64 * mt + 32 * b, tmem + COL_Q + 64 * mt + 8 * ks, bd, id_qk, ks > 0);
           }
           umma_commit(&s_full[2 * mt + b]);
         }
-        umma_commit(&k_empty[s]);  // K slot free once these MMAs retire
+        if (h == 1 || u + 1 == n_sub) umma_commit(&k_empty[s]);  // K slot free once these retire
       };
       issue_qk(0);
-      for (int j = 0; j < n_tiles; ++j) {
-        if (j + 1 < n_tiles) issue_qk(j + 1);
-        const int s = j % ST;
-        trace(1, j, 2);
-        mbar_wait(&v_full[s], (j / ST) & 1);
-        trace(1, j, 3);
-        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
+      for (int u = 0; u < n_sub; ++u) {
+        if (u + 1 < n_sub) issue_qk(u + 1);
+        const int j = u >> 1, h = u & 1, s = j % ST, b = u & 1;
+        if (h == 0) {
+          trace(1, j, 2);
+          mbar_wait(&v_full[s], (j / ST) & 1);
+          trace(1, j, 3);
+        }
+        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE) + h * SUB * 128;
         for (int mt = 0; mt < nm; ++mt) {
-          mbar_wait(&p_full[mt], j & 1);
-          trace(1, j, 4 + mt);
+          mbar_wait(&p_full[mt], u & 1);
+          if (h == 0) trace(1, j, 4 + mt);
           tc_fence_after();
-          const uint32_t p_base = smem_u32(smem + OFF_P + mt * P_BYTES);
 #pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks) {
-            const uint64_t a = umma_desc(p_base + ks * 32, 16, 1024);
-            // V tile is [keys][dh] (MN-major for B): dh halves are LBO apart, 8-key groups SBO apart
+          for (int ks = 0; ks < SUB / 16; ++ks) {
+            // V sub-tile is [32 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
             const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-            umma_bf16(tmem + COL_O + 128 * mt, a, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + COL_O + 128 * mt, tmem + COL_S + 64 * mt + 32 * b + 8 * ks, bd, id_pv,
+                         (u > 0 || ks > 0) ? 1u : 0u);
           }
           umma_commit(&o_done[mt]);
         }
-        umma_commit(&v_empty[s]);
+        if (h == 1 || u + 1 == n_sub) umma_commit(&v_empty[s]);
       }
     }
   } else if (warp >= 4) {
@@ -336,7 +351,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const bool valid = rho < GT;
       const int t = valid ? rho / p.G : 0;
       const uint32_t lane_base = (uint32_t)(32 * wl) << 16;
-      uint8_t* prow = smem + OFF_P + mt * P_BYTES;
       // tree-row visibility of this query row (ancestors + self; j <= t)
       uint32_t tmask[SD_MASK_WORDS];
 #pragma unroll
@@ -352,67 +366,74 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmask[w] = bits;
       }
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int b = j & 1;
-        const int role = (lane == 0 && wl == 0) ? 2 + mt : 99;
-        if (role < 4) trace(role, j, 0);
-        mbar_wait(&s_full[2 * mt + b], (j >> 1) & 1);
-        if (role < 4) trace(role, j, 1);
+      for (int u = 0; u < n_sub; ++u) {
+        const int b = u & 1;
+        const int role = (lane == 0 && wl == 0 && (u & 1) == 0) ? 2 + mt : 99;
+        if (role < 4) trace(role, u >> 1, 0);
+        mbar_wait(&s_full[2 * mt + b], (u >> 1) & 1);
+        if (role < 4) trace(role, u >> 1, 1);
         tc_fence_after();
-        uint32_t sr[64];
-        tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b), sr);
-        tmem_ld32(tmem + lane_base + COL_S + 64 * (2 * mt + b) + 32, sr + 32);
+        const uint32_t s_addr = tmem + lane_base + COL_S + 64 * mt + 32 * b;
+        uint32_t sr[32];
+        tmem_ld32(s_addr, sr);
         tmem_wait_ld();
-        const int key0 = key_begin + j * BN;
-        // visibility bits of the 64 keys of this tile
-        uint64_t vis;
-        if (key0 + BN <= cache_end) {
-          vis = ~0ull;
-        } else {
-          vis = 0ull;
+        const int key0 = key_begin + u * SUB;
+        const bool full = valid && key0 + SUB <= cache_end;
+        uint32_t vis = 0xffffffffu;
+        if (!full) {
+          vis = 0u;
+          if (valid) {
 #pragma unroll 4
-          for (int c = 0; c < 64; ++c) {
-            const int k = key0 + c;
-            bool on;
-            if (k < cache_end) {
-              on = true;
-            } else if (last && k < key_end) {
-              const int jt = k - p.ctx;
-              on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
-            } else {
-              on = false;
+            for (int c = 0; c < 32; ++c) {
+              const int k = key0 + c;
+              bool on;
+              if (k < cache_end) {
+                on = true;
+              } else if (last && k < key_end) {
+                const int jt = k - p.ctx;
+                on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
+              } else {
+                on = false;
+              }
+              vis |= (uint32_t)on << c;
             }
-            vis |= (uint64_t)on << c;
           }
-        }
-        if (!valid) vis = 0ull;
-        float mx = -INFINITY;
 #pragma unroll
-        for (int c = 0; c < 64; ++c)
-          if ((vis >> c) & 1ull) mx = fmaxf(mx, __uint_as_float(sr[c]));
-        mx *= LOG2E;
+          for (int c = 0; c < 32; ++c)
+            if (!((vis >> c) & 1u)) sr[c] = __float_as_uint(-INFINITY);
+        }
+        // tree max (short dependency chain)
+        float mx8[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          mx8[c] = fmaxf(fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 8])),
+                         fmaxf(__uint_as_float(sr[c + 16]), __uint_as_float(sr[c + 24])));
+        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * LOG2E;
         float scale = 1.f;
         bool rescale = false;
         if (mx > m_used + TAU) {
           scale = m_used == -INFINITY ? 0.f : ex2(m_used - mx);
-          rescale = j > 0;
+          rescale = u > 0;
           m_used = mx;
           l *= scale;
         }
-        uint32_t pk[32];
-        float rs = 0.f;
-        const float nm_used = -m_used;
+        uint32_t pk[16];
+        float rs8[8];
+        const float nm_used = m_used == -INFINITY ? 0.f : -m_used;
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float p0 = ((vis >> c) & 1ull) ? ex2(fmaf(__uint_as_float(sr[c]), LOG2E, nm_used)) : 0.f;
-          const float p1 = ((vis >> (c + 1)) & 1ull) ? ex2(fmaf(__uint_as_float(sr[c + 1]), LOG2E, nm_used)) : 0.f;
-          rs += p0 + p1;
+        for (int c = 0; c < 8; ++c) rs8[c] = 0.f;
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          const float p0 = ex2(fmaf(__uint_as_float(sr[c]), LOG2E, nm_used));
+          const float p1 = ex2(fmaf(__uint_as_float(sr[c + 1]), LOG2E, nm_used));
+          rs8[(c >> 1) & 7] += p0 + p1;
           pk[c >> 1] = pack_bf16(p0, p1);
         }
-        l += rs;
-        if (role < 4) trace(role, j, 2);
-        if (j > 0) mbar_wait(&o_done[mt], (j - 1) & 1);  // PV(j-1) done: P free, O stable
-        if (role < 4) trace(role, j, 3);
+        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        if (role < 4) trace(role, u >> 1, 2);
+        if (u > 0) mbar_wait(&o_done[mt], (u - 1) & 1);  // PV(u-1) done: O stable, P buffer free
+        if (role < 4) trace(role, u >> 1, 3);
         if (__any_sync(0xffffffffu, rescale)) {
           tc_fence_after();
 #pragma unroll
@@ -425,19 +446,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * (rescale ? scale : 1.f));
             tmem_st32(ta, o);
           }
-          tmem_wait_st();
         }
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(prow + sw128(row, c)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        fence_async_smem();
+        tmem_st16(s_addr, pk);  // P (bf16x2) over the consumed S columns
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[mt]);
-        if (role < 4) trace(role, j, 4);
+        if (role < 4) trace(role, u >> 1, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
-      mbar_wait(&o_done[mt], (n_tiles - 1) & 1);
+      mbar_wait(&o_done[mt], (n_sub - 1) & 1);
       tc_fence_after();
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
