@@ -106,8 +106,9 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
 int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host);
 /* DEBUG ONLY (the one piece of global state): route clock64 event stamps of
  * the tensor-core kernel's first CTA to int64 [4][64][8] at trace_dev (NULL
- * disables). Not used by the product path. */
-int sd_debug_tc_trace(void* trace_dev);
+ * disables); force_chunks > 0 overrides the chunk count. Not used by the
+ * product path. */
+int sd_debug_tc_trace(void* trace_dev, int force_chunks);
 
 /* ---- Eq. 2 importance (kvcache.py:243-265) ----
  * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),

@@ -57,7 +57,7 @@ _SIGS = {
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P,
                            P, P, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
-    "sd_debug_tc_trace": (INT, [P]),
+    "sd_debug_tc_trace": (INT, [P, INT]),
     "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
     "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
     "sd_select_workspace_bytes": (SZ, [INT, INT]),

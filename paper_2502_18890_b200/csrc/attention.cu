@@ -637,7 +637,7 @@ static int dispatch_decode(const AttnParams& p, int q_dtype, int kv_dtype, int o
 }
 
 int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
-int tc_set_trace(void* dev_ptr);
+int tc_set_trace(void* dev_ptr, int force_chunks);
 int tc_n_chunks(int ctx, int Hk);
 int tc_chunk_len(int ctx, int n);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
@@ -670,7 +670,7 @@ size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
   return ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
 }
 
-int sd_debug_tc_trace(void* trace_dev) { return tc_set_trace(trace_dev); }
+int sd_debug_tc_trace(void* trace_dev, int force_chunks) { return tc_set_trace(trace_dev, force_chunks); }
 
 int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host) {
   SD_REQUIRE(base && tmap_out_host && dh == 128 && L > 0 && Hk > 0 && cap > 0, "sd_make_kv_tmap: args");

@@ -10,18 +10,18 @@
 //   warp 0      TMA producer: K and V tiles of 64 keys x 128 dh (two 128-byte
 //               swizzled boxes each) into separate 4-deep rings (mbarrier
 //               tx-count); K slots free as soon as S = QK^T retires;
-//   warp 1      MMA issuer (one thread), per 32-key sub-tile u and M-tile:
-//               S[u%2] = Q K^T (M=128, N=32, A = Q from TMEM, B = K from
-//               smem) issued one sub-tile ahead; O += P V (M=128, N=128,
-//               A = P from TMEM, B = V from smem, MN-major straight from the
-//               TMA layout). Only one operand of each MMA is read from
-//               shared memory, so the tensor core is not smem-bound;
+//   warp 1      MMA issuer (one thread): S[u%2] = Q K^T (M=128, N=64, both
+//               operands in smem) issued two tiles ahead; O += P V (M=128,
+//               N=128, A = P from TMEM, B = V from smem, MN-major straight
+//               from the TMA layout); the two M-tiles' chains interleaved;
 //   warp 2      TMEM allocator (512 columns);
 //   warps 4-11  two softmax warpgroups, one per 128-row M-tile: thread = row =
-//               TMEM lane; Q staged into TMEM once; online softmax in base 2
-//               with lazy rescale (O in TMEM is rescaled only when the row
-//               max grows by > 2^8); P written back into TMEM (tcgen05.st).
-// Q is pre-rotated and pre-scaled by 1/sqrt(dh).
+//               TMEM lane; online softmax in base 2 with lazy rescale (O is
+//               rescaled in TMEM only when the row max grows by > 2^8, and
+//               only then does softmax wait for the previous O += P V); P is
+//               written back into TMEM (tcgen05.st).
+// Measured on B200 (tools/mma_bench.cu): an M=128 tcgen05.mma costs >= ~45
+// cycles whatever N, so S tiles are 64 keys wide; Q stays in smem.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -38,21 +38,21 @@ constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 
-constexpr int SUB = 32;         // keys per MMA sub-tile (S double-buffered per M-tile)
+constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
 constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [dh half][64 rows][128 B]
-constexpr int OFF_K = 0;
+constexpr int OFF_Q = 0;
+constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
 constexpr int OFF_BAR = OFF_V + ST * KV_TILE;
-constexpr int N_BAR = 4 * ST + 4 + 2 + 2;
+constexpr int N_BAR = 4 * ST + 4 + 4 + 2 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
-// TMEM columns (512): O[mt] fp32 128 each, Q[mt] bf16x2 64 each (TMEM A
-// operand), S[mt][buf] fp32 32 each; P[mt][buf] (bf16x2, TMEM A operand of
-// O += P V) overwrites the first 16 columns of the S buffer it came from.
+// TMEM columns (512): O[mt] fp32 128 each; S[mt][buf] fp32 64 each (double
+// buffered); P[mt][buf] (bf16x2, the TMEM A operand of O += P V) overwrites
+// the first 32 columns of the S buffer it was computed from.
 constexpr uint32_t COL_O = 0;
-constexpr uint32_t COL_Q = 256;
-constexpr uint32_t COL_S = 384;
+constexpr uint32_t COL_S = 256;
 constexpr uint32_t TMEM_COLS = 512;
 
 struct Params {
@@ -69,12 +69,20 @@ struct Params {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // Debug-only event timeline of CTA (0, 0, 0) (sd_debug_tc_trace); NULL in production.
+// Compiled in only with -DSD_TC_TRACE (tools/tc_trace.py builds that variant):
+// production kernels carry no instrumentation on the MMA critical path.
 __device__ int64_t* g_tc_trace = nullptr;
 constexpr int TR_TILES = 64, TR_EV = 8;
 __device__ __forceinline__ void trace(int role, int j, int ev) {
+#ifdef SD_TC_TRACE
   int64_t* t = g_tc_trace;
   if (t && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && j < TR_TILES)
     t[(role * TR_TILES + j) * TR_EV + ev] = clock64();
+#else
+  (void)role;
+  (void)j;
+  (void)ev;
+#endif
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -86,14 +94,29 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+__device__ int64_t* g_tc_stuck = nullptr;  // debug watchdog report (SD_TC_TRACE builds)
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done;
+#ifdef SD_TC_TRACE
+  long long spins = 0;
+#endif
   do {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
         : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+#ifdef SD_TC_TRACE
+    if (!done && ++spins > (1ll << 22)) {
+      int64_t* st = g_tc_stuck;
+      if (st) {
+        const int slot = atomicAdd((unsigned long long*)st, 1ull) & 63;
+        st[1 + slot] = ((int64_t)blockIdx.x << 48) | ((int64_t)blockIdx.y << 40) | ((int64_t)threadIdx.x << 24) |
+                       ((int64_t)(smem_u32(bar) & 0xFFFFF) << 1) | parity;
+      }
+      return;  // give up: the kernel finishes with garbage so the report can be read
+    }
+#endif
   } while (!done);
 }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -150,6 +173,11 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}" : "=r"(pred));
+  return pred != 0;
+}
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ float ex2(float x) {
@@ -184,6 +212,7 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
+
 __global__ void __launch_bounds__(THREADS, 1)
     verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                           Params p) {
@@ -195,9 +224,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* k_empty = bars + 2 * ST;
   uint64_t* v_empty = bars + 3 * ST;
   uint64_t* s_full = bars + 4 * ST;      // [mt][buf]
-  uint64_t* p_full = s_full + 4;         // [mt]
-  uint64_t* o_done = p_full + 2;         // [mt]
-  uint32_t* tmem_slot = (uint32_t*)(o_done + 2);
+  uint64_t* p_full = s_full + 4;         // [mt][buf]: per S buffer, so a softmax running two tiles
+                                         // ahead of the MMA issuer cannot alias a barrier phase
+  uint64_t* o_done = p_full + 4;         // [mt]: one phase per tile's O += P V
+  uint64_t* o_final = o_done + 2;        // [mt]: single phase, after the last O += P V. The
+                                         // epilogue cannot use o_done's parity: the softmax may
+                                         // finish while o_done is still two phases behind.
+  uint32_t* tmem_slot = (uint32_t*)(o_final + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kvh = blockIdx.y;
@@ -210,7 +243,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int cache_end = min(p.ctx, key_begin + p.chunk);
   const int key_end = last ? p.ctx + T : cache_end;  // the last chunk also takes the tree rows
   const int n_tiles = (key_end - key_begin + BN - 1) / BN;
-  const int n_sub = (key_end - key_begin + SUB - 1) / SUB;
   int act[2];
   for (int mt = 0; mt < 2; ++mt) {
     int a = 0;
@@ -219,6 +251,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const int nm = act[1] > 0 ? 2 : 1;
 
+  // ---- stage Q (M-tiles, K-major SW128): all loads in flight, then stores ----
+  {
+    constexpr int PER = (ROWS * (DH / 8) + THREADS - 1) / THREADS;  // 16-byte chunks per thread
+    uint4 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * THREADS;
+      const int row = i >> 4, c = i & 15;
+      const int rho = rg + row;
+      v[k] = make_uint4(0, 0, 0, 0);
+      if (i < ROWS * 16 && rho < GT) {
+        const int t = rho / p.G, g = rho - t * p.G;
+        v[k] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = tid + k * THREADS;
+      if (i < ROWS * 16) {
+        const int row = i >> 4, c = i & 15;
+        const int mt = row >> 7, r = row & 127, half = c >> 3;
+        *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v[k];
+      }
+    }
+  }
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&k_full[s], 1);
@@ -228,8 +285,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int mt = 0; mt < 2; ++mt) {
-      mbar_init(&p_full[mt], 32 * (act[mt] > 0 ? act[mt] : 1));
+      mbar_init(&p_full[2 * mt], 32 * (act[mt] > 0 ? act[mt] : 1));
+      mbar_init(&p_full[2 * mt + 1], 32 * (act[mt] > 0 ? act[mt] : 1));
       mbar_init(&o_done[mt], 1);
+      mbar_init(&o_final[mt], 1);
     }
     fence_barrier_init();
   }
@@ -239,33 +298,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  fence_async_smem();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-
-  // ---- softmax threads stage their query row into TMEM (A operand of S = Q K^T) ----
-  if (warp >= 4) {
-    const int mt = (warp - 4) >> 2, wl = warp & 3;
-    const int rho = rg + 128 * mt + 32 * wl + lane;
-    uint4 qv[16];
-    if (rho < GT) {
-      const int t = rho / p.G, g = rho - t * p.G;
-      const uint4* src = reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH);
-#pragma unroll
-      for (int c = 0; c < 16; ++c) qv[c] = __ldg(src + c);
-    } else {
-#pragma unroll
-      for (int c = 0; c < 16; ++c) qv[c] = make_uint4(0, 0, 0, 0);
-    }
-    const uint32_t ta = tmem + ((uint32_t)(32 * wl) << 16) + COL_Q + 64 * mt;
-    tmem_st32(ta, reinterpret_cast<const uint32_t*>(qv));
-    tmem_st32(ta + 32, reinterpret_cast<const uint32_t*>(qv + 8));
-    tmem_wait_st();
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
 
   if (warp == 0) {
     // ================= TMA producer: K(j), V(j) in order, separate rings =================
@@ -291,54 +328,70 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer (32-key sub-tiles u) =================
+    // ================= MMA issuer =================
     if (lane == 0) {
-      const uint32_t id_qk = idesc_bf16(SUB, false);
+      const uint32_t id_qk = idesc_bf16(BN, false);
       const uint32_t id_pv = idesc_bf16(DH, true);
-      auto issue_qk = [&](int u) {
-        const int j = u >> 1, h = u & 1, s = j % ST, b = u & 1;
-        if (h == 0) {
-          trace(1, j, 0);
-          mbar_wait(&k_full[s], (j / ST) & 1);
-          trace(1, j, 1);
-          tc_fence_after();
-        }
-        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE) + h * SUB * 128;
-        for (int mt = 0; mt < nm; ++mt) {
+      const uint32_t q_base = smem_u32(smem + OFF_Q);
+      // S[mt][j%2] = Q K(j)^T for one M-tile (8 dependent K=16 steps)
+      auto issue_qk_mt = [&](int j, int mt) {
+        const int s = j % ST, b = j & 1;
+        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
 #pragma unroll
-          for (int ks = 0; ks < DH / 16; ++ks) {
-            const uint32_t half = ks >> 2, in = (ks & 3) * 32;
-            const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
-            umma_bf16_ts(tmem + COL_S + 64 * mt + 32 * b, tmem + COL_Q + 64 * mt + 8 * ks, bd, id_qk, ks > 0);
-          }
-          umma_commit(&s_full[2 * mt + b]);
+        for (int ks = 0; ks < DH / 16; ++ks) {
+          const uint32_t half = ks >> 2, in = (ks & 3) * 32;
+          const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
+          const uint64_t a = umma_desc(q_base + mt * 32768 + half * 16384 + in, 16, 1024);
+          umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
         }
-        if (h == 1 || u + 1 == n_sub) umma_commit(&k_empty[s]);  // K slot free once these retire
+        umma_commit(&s_full[2 * mt + b]);
       };
-      issue_qk(0);
-      for (int u = 0; u < n_sub; ++u) {
-        if (u + 1 < n_sub) issue_qk(u + 1);
-        const int j = u >> 1, h = u & 1, s = j % ST, b = u & 1;
-        if (h == 0) {
-          trace(1, j, 2);
-          mbar_wait(&v_full[s], (j / ST) & 1);
-          trace(1, j, 3);
-        }
-        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE) + h * SUB * 128;
+      auto wait_k = [&](int j) {
+        trace(1, j, 0);
+        mbar_wait(&k_full[j % ST], (j / ST) & 1);
+        trace(1, j, 1);
+        tc_fence_after();
+      };
+      for (int j0 = 0; j0 < 2 && j0 < n_tiles; ++j0) {
+        wait_k(j0);
+        for (int mt = 0; mt < nm; ++mt) issue_qk_mt(j0, mt);
+        umma_commit(&k_empty[j0 % ST]);
+        trace(1, j0, 2);
+      }
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % ST, b = j & 1;
+        trace(1, j, 3);
+        mbar_wait(&v_full[s], (j / ST) & 1);
+        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
+        // O += P(j) V(j), per M-tile as soon as its P is in TMEM
         for (int mt = 0; mt < nm; ++mt) {
-          mbar_wait(&p_full[mt], u & 1);
-          if (h == 0) trace(1, j, 4 + mt);
+          mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
+          trace(1, j, 4 + mt);
           tc_fence_after();
 #pragma unroll
-          for (int ks = 0; ks < SUB / 16; ++ks) {
-            // V sub-tile is [32 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
+          for (int ks = 0; ks < BN / 16; ++ks) {
+            // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
             const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-            umma_bf16_ts(tmem + COL_O + 128 * mt, tmem + COL_S + 64 * mt + 32 * b + 8 * ks, bd, id_pv,
-                         (u > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_ts(tmem + COL_O + 128 * mt, tmem + COL_S + 128 * mt + 64 * b + 8 * ks, bd, id_pv,
+                         (j > 0 || ks > 0) ? 1u : 0u);
           }
           umma_commit(&o_done[mt]);
+          if (j == n_tiles - 1) umma_commit(&o_final[mt]);
         }
-        if (h == 1 || u + 1 == n_sub) umma_commit(&v_empty[s]);
+        umma_commit(&v_empty[s]);
+        trace(1, j, 6);
+        // S(j+2) reuses buffer b: it may only be written once O += P(j) V has
+        // read P(j) (the tensor pipe does not order that WAR on TMEM). Waiting
+        // per M-tile keeps the pipe busy with the other tile's PV meanwhile.
+        if (j + 2 < n_tiles) {
+          wait_k(j + 2);
+          for (int mt = 0; mt < nm; ++mt) {
+            mbar_wait(&o_done[mt], j & 1);
+            tc_fence_after();
+            issue_qk_mt(j + 2, mt);
+          }
+          umma_commit(&k_empty[(j + 2) % ST]);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -366,75 +419,76 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmask[w] = bits;
       }
       float m_used = -INFINITY, l = 0.f;
-      for (int u = 0; u < n_sub; ++u) {
-        const int b = u & 1;
-        const int role = (lane == 0 && wl == 0 && (u & 1) == 0) ? 2 + mt : 99;
-        if (role < 4) trace(role, u >> 1, 0);
-        mbar_wait(&s_full[2 * mt + b], (u >> 1) & 1);
-        if (role < 4) trace(role, u >> 1, 1);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int b = j & 1;
+        const int role = (lane == 0 && wl == 0) ? 2 + mt : 99;
+        if (role < 4) trace(role, j, 0);
+        mbar_wait(&s_full[2 * mt + b], (j >> 1) & 1);
+        if (role < 4) trace(role, j, 1);
         tc_fence_after();
-        const uint32_t s_addr = tmem + lane_base + COL_S + 64 * mt + 32 * b;
-        uint32_t sr[32];
+        const uint32_t s_addr = tmem + lane_base + COL_S + 128 * mt + 64 * b;
+        uint32_t sr[64];
         tmem_ld32(s_addr, sr);
+        tmem_ld32(s_addr + 32, sr + 32);
         tmem_wait_ld();
-        const int key0 = key_begin + u * SUB;
-        const bool full = valid && key0 + SUB <= cache_end;
-        uint32_t vis = 0xffffffffu;
+        const int key0 = key_begin + j * BN;
+        const bool full = valid && key0 + BN <= cache_end;
         if (!full) {
-          vis = 0u;
+          uint64_t vis = 0ull;  // built without indexing sr[] (keeps it in registers)
           if (valid) {
-#pragma unroll 4
-            for (int c = 0; c < 32; ++c) {
+            for (int c = 0; c < 64; ++c) {
               const int k = key0 + c;
-              bool on;
+              bool on = false;
               if (k < cache_end) {
                 on = true;
               } else if (last && k < key_end) {
                 const int jt = k - p.ctx;
                 on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
-              } else {
-                on = false;
               }
-              vis |= (uint32_t)on << c;
+              vis |= (uint64_t)on << c;
             }
           }
 #pragma unroll
-          for (int c = 0; c < 32; ++c)
-            if (!((vis >> c) & 1u)) sr[c] = __float_as_uint(-INFINITY);
+          for (int c = 0; c < 64; ++c)
+            if (!((vis >> c) & 1ull)) sr[c] = __float_as_uint(-INFINITY);
         }
         // tree max (short dependency chain)
         float mx8[8];
 #pragma unroll
-        for (int c = 0; c < 8; ++c)
-          mx8[c] = fmaxf(fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 8])),
-                         fmaxf(__uint_as_float(sr[c + 16]), __uint_as_float(sr[c + 24])));
+        for (int c = 0; c < 8; ++c) {
+          const float a0 = fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 8]));
+          const float a1 = fmaxf(__uint_as_float(sr[c + 16]), __uint_as_float(sr[c + 24]));
+          const float a2 = fmaxf(__uint_as_float(sr[c + 32]), __uint_as_float(sr[c + 40]));
+          const float a3 = fmaxf(__uint_as_float(sr[c + 48]), __uint_as_float(sr[c + 56]));
+          mx8[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+        }
         const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
                                fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * LOG2E;
         float scale = 1.f;
         bool rescale = false;
         if (mx > m_used + TAU) {
           scale = m_used == -INFINITY ? 0.f : ex2(m_used - mx);
-          rescale = u > 0;
+          rescale = j > 0;
           m_used = mx;
           l *= scale;
         }
-        uint32_t pk[16];
+        uint32_t pk[32];
         float rs8[8];
         const float nm_used = m_used == -INFINITY ? 0.f : -m_used;
 #pragma unroll
         for (int c = 0; c < 8; ++c) rs8[c] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 32; c += 2) {
+        for (int c = 0; c < 64; c += 2) {
           const float p0 = ex2(fmaf(__uint_as_float(sr[c]), LOG2E, nm_used));
           const float p1 = ex2(fmaf(__uint_as_float(sr[c + 1]), LOG2E, nm_used));
           rs8[(c >> 1) & 7] += p0 + p1;
           pk[c >> 1] = pack_bf16(p0, p1);
         }
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-        if (role < 4) trace(role, u >> 1, 2);
-        if (u > 0) mbar_wait(&o_done[mt], (u - 1) & 1);  // PV(u-1) done: O stable, P buffer free
-        if (role < 4) trace(role, u >> 1, 3);
+        if (role < 4) trace(role, j, 2);
         if (__any_sync(0xffffffffu, rescale)) {
+          // O must be stable: wait for every earlier O += P V of this M-tile
+          if (j > 0) mbar_wait(&o_done[mt], (j - 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -447,14 +501,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             tmem_st32(ta, o);
           }
         }
-        tmem_st16(s_addr, pk);  // P (bf16x2) over the consumed S columns
+        if (role < 4) trace(role, j, 3);
+        tmem_st32(s_addr, pk);  // P (bf16x2) over the consumed S columns
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[mt]);
-        if (role < 4) trace(role, u >> 1, 4);
+        mbar_arrive(&p_full[2 * mt + b]);
+        if (role < 4) trace(role, j, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
-      mbar_wait(&o_done[mt], (n_sub - 1) & 1);
+      mbar_wait(&o_final[mt], 0);
       tc_fence_after();
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
@@ -519,12 +574,20 @@ int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out)
   return SD_OK;
 }
 
-int tc_set_trace(void* dev_ptr) {
+static int g_force_chunks = 0;  // debug only (sd_debug_tc_trace)
+
+int tc_set_trace(void* dev_ptr, int force_chunks) {
+  g_force_chunks = force_chunks;
+  if (dev_ptr) {  // watchdog report area just past the trace block
+    void* stuck = (char*)dev_ptr + 4 * 64 * 8 * sizeof(int64_t);
+    cudaMemcpyToSymbol(tc::g_tc_stuck, &stuck, sizeof(void*));
+  }
   cudaError_t e = cudaMemcpyToSymbol(tc::g_tc_trace, &dev_ptr, sizeof(void*));
   return e == cudaSuccess ? SD_OK : SD_ECUDA;
 }
 
 int tc_n_chunks(int ctx, int Hk) {
+  if (g_force_chunks > 0) return g_force_chunks;
   // one wave of one CTA per SM over (chunks x kv heads); >= one tile per chunk
   int want = 148 / Hk;
   const int max_by_tiles = (ctx + tc::BN - 1) / tc::BN;

@@ -13,7 +13,9 @@ from paper_2502_18890_b200.model import mask_bits_from_bool  # noqa: E402
 
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 54096
 T = int(sys.argv[2]) if len(sys.argv) > 2 else 41
-H, Hk, dh = 32, 8, 128
+Hk = int(sys.argv[3]) if len(sys.argv) > 3 else 8
+force = int(sys.argv[4]) if len(sys.argv) > 4 else 0
+H, dh = 4 * Hk, 128
 F = FullCache(1, Hk, dh, capacity=ctx + T + 64, dtype=torch.bfloat16)
 F.k_rot.normal_()
 F.v.normal_()
@@ -30,12 +32,13 @@ def run():
            L.MASK_WORDS, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
 
 
+L.call("sd_debug_tc_trace", None, force)
 for _ in range(3):
     run()
-L.call("sd_debug_tc_trace", L.ptr(tr))
+L.call("sd_debug_tc_trace", L.ptr(tr), force)
 run()
 torch.cuda.synchronize()
-L.call("sd_debug_tc_trace", None)
+L.call("sd_debug_tc_trace", None, force)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
 for _ in range(10):
@@ -45,8 +48,8 @@ torch.cuda.synchronize()
 print(f"ctx={ctx} T={T}: {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call")
 t = tr.cpu().numpy()
 base = t[t > 0].min()
-names = {0: ["k_empty?", "k_empty ok", "v_empty ok"], 1: ["qk wait", "k_full ok", "v wait", "v_full ok", "p0 ok", "p1 ok"],
-         2: ["s wait", "s ok", "exp done", "o_done ok", "p arrive"], 3: ["s wait", "s ok", "exp done", "o_done ok", "p arrive"]}
+names = {0: ["k_empty?", "k_empty ok", "v_empty ok"], 1: ["qk wait", "k_full ok", "qk issued", "v wait", "p0 ok", "p1 ok", "pv issued"],
+         2: ["s wait", "s ok", "exp done", "rescaled", "p arrive"], 3: ["s wait", "s ok", "exp done", "rescaled", "p arrive"]}
 for j in list(range(0, 6)) + list(range(20, 24)):
     row = []
     for role in range(4):
@@ -55,3 +58,4 @@ for j in list(range(0, 6)) + list(range(20, 24)):
             if v:
                 row.append(f"{['P', 'M', 'S0', 'S1'][role]}.{nm}={v - base}")
     print(f"tile {j:2d}: " + "  ".join(row))
+

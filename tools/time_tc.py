@@ -1,0 +1,24 @@
+import sys, torch, numpy as np
+sys.path.insert(0, '.')
+from paper_2502_18890_b200 import FullCache, _lib as L
+from paper_2502_18890_b200.model import mask_bits_from_bool
+for (ctx, T, Hk) in [(54096, 41, 8), (54096, 20, 8), (54096, 101, 8), (4096, 41, 8)]:
+    H, dh = 4 * Hk, 128
+    F = FullCache(1, Hk, dh, capacity=ctx + T + 64, dtype=torch.bfloat16)
+    F.k_rot.normal_(); F.v.normal_()
+    q = (torch.randn((T, H, dh), device="cuda") * 0.1).to(torch.bfloat16)
+    bits = torch.as_tensor(mask_bits_from_bool(np.tril(np.ones((T, T), dtype=bool))), device="cuda")
+    out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+    def run():
+        L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
+               None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
+               L.MASK_WORDS, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
+    for _ in range(3): run()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(); e0.record()
+    for _ in range(20): run()
+    e1.record(); torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / 20 * 1000
+    byt = 2 * ctx * Hk * dh * 2
+    print(f"ctx={ctx} T={T} Hk={Hk}: {us:.1f} us  {byt / us / 1e3:.0f} GB/s")
