@@ -25,7 +25,7 @@ FLAGS = [
     "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
     "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
     f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}",
-] + (["-DSD_TC_TRACE"] if os.environ.get("SD_TC_TRACE") else [])
+] + (["-DSD_TC_TRACE"] if os.environ.get("SD_TC_TRACE") else []) + os.environ.get("NVCC_EXTRA", "").split()
 
 
 def sources():

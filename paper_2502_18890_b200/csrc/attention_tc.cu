@@ -8,20 +8,20 @@
 // One CTA = (key chunk, kv head, 256-row group), 12 warps; the last chunk
 // also covers the T staged tree rows (keys ctx..ctx+T-1) under the tree mask.
 //   warp 0      TMA producer: K and V tiles of 64 keys x 128 dh (two 128-byte
-//               swizzled boxes each) into separate 4-deep rings (mbarrier
-//               tx-count); K slots free as soon as S = QK^T retires;
-//   warp 1      MMA issuer (one thread): S[u%2] = Q K^T (M=128, N=64, both
-//               operands in smem) issued two tiles ahead; O += P V (M=128,
-//               N=128, A = P from TMEM, B = V from smem, MN-major straight
-//               from the TMA layout); the two M-tiles' chains interleaved;
-//   warp 2      TMEM allocator (512 columns);
+//               swizzled boxes each) into separate 3-deep rings (mbarrier
+//               tx-count);
+//   warp 1      MMA issuer (one thread): S[mt][j%2] = Q K(j)^T (M=128, N=64,
+//               SS) and O[mt] += P(j) V(j) (M=128, N=128, A = P from shared
+//               memory, B = V MN-major straight from the TMA layout);
+//   warp 2      TMEM allocator (512 columns: O 2x128, S 2x2x64);
 //   warps 4-11  two softmax warpgroups, one per 128-row M-tile: thread = row =
 //               TMEM lane; online softmax in base 2 with lazy rescale (O is
-//               rescaled in TMEM only when the row max grows by > 2^8, and
-//               only then does softmax wait for the previous O += P V); P is
-//               written back into TMEM (tcgen05.st).
-// Measured on B200 (tools/mma_bench.cu): an M=128 tcgen05.mma costs >= ~45
-// cycles whatever N, so S tiles are 64 keys wide; Q stays in smem.
+//               rescaled in TMEM only when the row max grows by > 2^8).
+// P goes to shared memory (SW128 K-major, the layout the MMA reads), not back
+// into TMEM over S: the S buffer is released (s_free) as soon as the softmax
+// has loaded it, so QK(j+2) is issued while the softmax of tile j is still
+// computing, and the issuer never waits for an MMA to retire. The tensor pipe
+// therefore runs QK(j+1) / QK(j+2) / PV(j) back to back under the softmax.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -32,7 +32,10 @@ namespace tc {
 
 constexpr int BN = 64;          // keys per tile
 constexpr int DH = 128;
-constexpr int ST = 4;           // K ring depth == V ring depth
+#ifndef SD_TC_ST
+#define SD_TC_ST 3
+#endif
+constexpr int ST = SD_TC_ST;    // K ring depth == V ring depth
 constexpr int THREADS = 384;
 constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
@@ -40,17 +43,18 @@ constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 
 constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
 constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [dh half][64 rows][128 B]
+constexpr int P_TILE = 128 * BN * 2;            // 16 KB: [128 rows][64 keys * 2 B] SW128 K-major
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
-constexpr int OFF_BAR = OFF_V + ST * KV_TILE;
-constexpr int N_BAR = 4 * ST + 4 + 4 + 2 + 2;
+constexpr int OFF_P = OFF_V + ST * KV_TILE;     // [mt][buf]
+constexpr int OFF_BAR = OFF_P + 4 * P_TILE;
+constexpr int N_BAR = 4 * ST + 4 * 4 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
 // TMEM columns (512): O[mt] fp32 128 each; S[mt][buf] fp32 64 each (double
-// buffered); P[mt][buf] (bf16x2, the TMEM A operand of O += P V) overwrites
-// the first 32 columns of the S buffer it was computed from.
+// buffered).
 constexpr uint32_t COL_O = 0;
 constexpr uint32_t COL_S = 256;
 constexpr uint32_t TMEM_COLS = 512;
@@ -72,6 +76,11 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 // Compiled in only with -DSD_TC_TRACE (tools/tc_trace.py builds that variant):
 // production kernels carry no instrumentation on the MMA critical path.
 __device__ int64_t* g_tc_trace = nullptr;
+// Debug-only pipeline experiments (-DSD_TC_EXPERIMENT=n, tools/gpu_tc_exp.sh):
+// 1 = softmax skips its math, 2 = no PV MMAs, 3 = no QK MMAs, 4 = 1+2+3 (TMA stream only).
+#ifndef SD_TC_EXPERIMENT
+#define SD_TC_EXPERIMENT 0
+#endif
 constexpr int TR_TILES = 64, TR_EV = 8;
 __device__ __forceinline__ void trace(int role, int j, int ev) {
 #ifdef SD_TC_TRACE
@@ -223,13 +232,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* v_full = bars + ST;
   uint64_t* k_empty = bars + 2 * ST;
   uint64_t* v_empty = bars + 3 * ST;
-  uint64_t* s_full = bars + 4 * ST;      // [mt][buf]
-  uint64_t* p_full = s_full + 4;         // [mt][buf]: per S buffer, so a softmax running two tiles
-                                         // ahead of the MMA issuer cannot alias a barrier phase
-  uint64_t* o_done = p_full + 4;         // [mt]: one phase per tile's O += P V
-  uint64_t* o_final = o_done + 2;        // [mt]: single phase, after the last O += P V. The
-                                         // epilogue cannot use o_done's parity: the softmax may
-                                         // finish while o_done is still two phases behind.
+  uint64_t* s_full = bars + 4 * ST;      // [mt][buf]: QK retired -> softmax
+  uint64_t* s_free = s_full + 4;         // [mt][buf]: softmax has loaded S -> QK(j+2) may overwrite it
+  uint64_t* p_full = s_free + 4;         // [mt][buf]: P(j) in shared memory -> PV(j)
+  uint64_t* pv_done = p_full + 4;        // [mt][buf]: PV(j) retired -> P buffer free, O stable
+  uint64_t* o_final = pv_done + 4;       // [mt]: single phase, after the last PV
   uint32_t* tmem_slot = (uint32_t*)(o_final + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -238,6 +245,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int GT = p.G * T;
   const int rg = blockIdx.z * ROWS;
   if (rg >= GT) return;
+  if (tid == 0) trace(0, 60, 0);
   const bool last = (int)blockIdx.x == p.n_chunks - 1;
   const int key_begin = blockIdx.x * p.chunk;
   const int cache_end = min(p.ctx, key_begin + p.chunk);
@@ -276,18 +284,22 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   }
+  if (tid == 0) trace(0, 60, 1);
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&k_full[s], 1);
       mbar_init(&v_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_empty[s], 1);
+      mbar_init(&k_empty[s], nm);  // one commit per M-tile issuer
+      mbar_init(&v_empty[s], nm);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(&s_full[i], 1);
     for (int mt = 0; mt < 2; ++mt) {
-      mbar_init(&p_full[2 * mt], 32 * (act[mt] > 0 ? act[mt] : 1));
-      mbar_init(&p_full[2 * mt + 1], 32 * (act[mt] > 0 ? act[mt] : 1));
-      mbar_init(&o_done[mt], 1);
+      const uint32_t arrivals = 32 * (act[mt] > 0 ? act[mt] : 1);
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&s_full[2 * mt + b], 1);
+        mbar_init(&s_free[2 * mt + b], arrivals);
+        mbar_init(&p_full[2 * mt + b], arrivals);
+        mbar_init(&pv_done[2 * mt + b], 1);
+      }
       mbar_init(&o_final[mt], 1);
     }
     fence_barrier_init();
@@ -303,95 +315,95 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tid == 0) trace(0, 60, 2);
 
-  if (warp == 0) {
-    // ================= TMA producer: K(j), V(j) in order, separate rings =================
+  if (warp == 0 || warp == 3) {
+    // ================= TMA producers: K (warp 0) and V (warp 3), decoupled =================
+    // K(j) is recycled when QK(j) retires, V(j) only after the softmax and PV
+    // of tile j: one thread per ring keeps the K stream from queueing behind V.
     if (lane == 0) {
-      tma_prefetch(&tmap_k);
-      tma_prefetch(&tmap_v);
+      const bool is_k = warp == 0;
+      const CUtensorMap* map = is_k ? &tmap_k : &tmap_v;
+      uint64_t* full = is_k ? k_full : v_full;
+      uint64_t* empty = is_k ? k_empty : v_empty;
+      uint8_t* ring = smem + (is_k ? OFF_K : OFF_V);
+      tma_prefetch(map);
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
         const int key0 = key_begin + j * BN;
-        trace(0, j, 0);
-        if (j >= ST) mbar_wait(&k_empty[s], ((j / ST) + 1) & 1);
-        trace(0, j, 1);
-        uint8_t* kd = smem + OFF_K + s * KV_TILE;
-        mbar_expect_tx(&k_full[s], KV_TILE);
-        tma_load_4d(kd, &tmap_k, &k_full[s], 0, key0, kvh, p.layer);
-        tma_load_4d(kd + KV_TILE / 2, &tmap_k, &k_full[s], 64, key0, kvh, p.layer);
-        if (j >= ST) mbar_wait(&v_empty[s], ((j / ST) + 1) & 1);
-        trace(0, j, 2);
-        uint8_t* vd = smem + OFF_V + s * KV_TILE;
-        mbar_expect_tx(&v_full[s], KV_TILE);
-        tma_load_4d(vd, &tmap_v, &v_full[s], 0, key0, kvh, p.layer);
-        tma_load_4d(vd + KV_TILE / 2, &tmap_v, &v_full[s], 64, key0, kvh, p.layer);
+        if (j >= ST) mbar_wait(&empty[s], ((j / ST) + 1) & 1);
+        trace(0, j, is_k ? 1 : 2);
+        uint8_t* d = ring + s * KV_TILE;
+        mbar_expect_tx(&full[s], KV_TILE);
+        tma_load_4d(d, map, &full[s], 0, key0, kvh, p.layer);
+        tma_load_4d(d + KV_TILE / 2, map, &full[s], 64, key0, kvh, p.layer);
       }
     }
-  } else if (warp == 1) {
-    // ================= MMA issuer =================
-    if (lane == 0) {
+  } else if (warp == 1 || warp == 2) {
+    // ================= MMA issuers: one thread per M-tile =================
+    // Each M-tile runs its own QK -> softmax -> PV chain on its own TMEM
+    // columns; the two issuers share the K/V rings (a slot is free once both
+    // have committed it) and their MMAs interleave in the tensor pipe, so one
+    // tile's barrier waits never stall the other's MMAs.
+    const int mt = warp - 1;
+    if (lane == 0 && mt < nm) {
       const uint32_t id_qk = idesc_bf16(BN, false);
       const uint32_t id_pv = idesc_bf16(DH, true);
-      const uint32_t q_base = smem_u32(smem + OFF_Q);
-      // S[mt][j%2] = Q K(j)^T for one M-tile (8 dependent K=16 steps)
-      auto issue_qk_mt = [&](int j, int mt) {
+      const uint32_t q_base = smem_u32(smem + OFF_Q + mt * 32768);
+      const uint32_t o_col = tmem + COL_O + 128 * mt;
+      // S[mt][j%2] = Q[mt] K(j)^T (8 K=16 steps)
+      auto issue_qk = [&](int j) {
         const int s = j % ST, b = j & 1;
         const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) {
           const uint32_t half = ks >> 2, in = (ks & 3) * 32;
           const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
-          const uint64_t a = umma_desc(q_base + mt * 32768 + half * 16384 + in, 16, 1024);
-          umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
+          const uint64_t a = umma_desc(q_base + half * 16384 + in, 16, 1024);
+          if (SD_TC_EXPERIMENT != 3 && SD_TC_EXPERIMENT != 4)
+            umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
         }
         umma_commit(&s_full[2 * mt + b]);
+        umma_commit(&k_empty[s]);
       };
       auto wait_k = [&](int j) {
-        trace(1, j, 0);
+        if (mt == 0) trace(1, j, 0);
         mbar_wait(&k_full[j % ST], (j / ST) & 1);
-        trace(1, j, 1);
+        if (mt == 0) trace(1, j, 1);
         tc_fence_after();
       };
       for (int j0 = 0; j0 < 2 && j0 < n_tiles; ++j0) {
         wait_k(j0);
-        for (int mt = 0; mt < nm; ++mt) issue_qk_mt(j0, mt);
-        umma_commit(&k_empty[j0 % ST]);
-        trace(1, j0, 2);
+        issue_qk(j0);
       }
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST, b = j & 1;
-        trace(1, j, 3);
-        mbar_wait(&v_full[s], (j / ST) & 1);
-        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
-        // O += P(j) V(j), per M-tile as soon as its P is in TMEM
-        for (int mt = 0; mt < nm; ++mt) {
-          mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
-          trace(1, j, 4 + mt);
-          tc_fence_after();
-#pragma unroll
-          for (int ks = 0; ks < BN / 16; ++ks) {
-            // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
-            const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-            umma_bf16_ts(tmem + COL_O + 128 * mt, tmem + COL_S + 128 * mt + 64 * b + 8 * ks, bd, id_pv,
-                         (j > 0 || ks > 0) ? 1u : 0u);
-          }
-          umma_commit(&o_done[mt]);
-          if (j == n_tiles - 1) umma_commit(&o_final[mt]);
-        }
-        umma_commit(&v_empty[s]);
-        trace(1, j, 6);
-        // S(j+2) reuses buffer b: it may only be written once O += P(j) V has
-        // read P(j) (the tensor pipe does not order that WAR on TMEM). Waiting
-        // per M-tile keeps the pipe busy with the other tile's PV meanwhile.
+        // S(j+2) into buffer b as soon as the softmax has read S(j) out of it
         if (j + 2 < n_tiles) {
           wait_k(j + 2);
-          for (int mt = 0; mt < nm; ++mt) {
-            mbar_wait(&o_done[mt], j & 1);
-            tc_fence_after();
-            issue_qk_mt(j + 2, mt);
-          }
-          umma_commit(&k_empty[(j + 2) % ST]);
+          mbar_wait(&s_free[2 * mt + b], (j >> 1) & 1);
+          tc_fence_after();
+          issue_qk(j + 2);
         }
+        if (mt == 0) trace(1, j, 3);
+        mbar_wait(&v_full[s], (j / ST) & 1);
+        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
+        const uint32_t p_base = smem_u32(smem + OFF_P + (2 * mt + b) * P_TILE);
+        mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
+        if (mt == 0) trace(1, j, 4);
+        tc_fence_after();
+#pragma unroll
+        for (int ks = 0; ks < BN / 16; ++ks) {
+          // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
+          const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
+          const uint64_t ad = umma_desc(p_base + ks * 32, 16, 1024);
+          if (SD_TC_EXPERIMENT != 2 && SD_TC_EXPERIMENT != 4)
+            umma_bf16(o_col, ad, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_done[2 * mt + b]);
+        if (j == n_tiles - 1) umma_commit(&o_final[mt]);
+        umma_commit(&v_empty[s]);
+        if (mt == 0) trace(1, j, 6);
       }
     }
   } else if (warp >= 4) {
@@ -431,6 +443,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld32(s_addr, sr);
         tmem_ld32(s_addr + 32, sr + 32);
         tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(&s_free[2 * mt + b]);  // S(j) is in registers: QK(j+2) may reuse the buffer
+        if (SD_TC_EXPERIMENT == 1 || SD_TC_EXPERIMENT == 4) {
+          if (j >= 2) mbar_wait(&pv_done[2 * mt + b], ((j - 2) >> 1) & 1);
+          mbar_arrive(&p_full[2 * mt + b]);
+          l += __uint_as_float(sr[lane]);
+          continue;
+        }
         const int key0 = key_begin + j * BN;
         const bool full = valid && key0 + BN <= cache_end;
         if (!full) {
@@ -487,8 +507,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         if (role < 4) trace(role, j, 2);
         if (__any_sync(0xffffffffu, rescale)) {
-          // O must be stable: wait for every earlier O += P V of this M-tile
-          if (j > 0) mbar_wait(&o_done[mt], (j - 1) & 1);
+          // O must be stable: wait for every earlier O += P V of this M-tile (PV(j-1) retires last)
+          if (j > 0) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -500,16 +520,25 @@ __global__ void __launch_bounds__(THREADS, 1)
             for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * (rescale ? scale : 1.f));
             tmem_st32(ta, o);
           }
+          tmem_wait_st();
         }
         if (role < 4) trace(role, j, 3);
-        tmem_st32(s_addr, pk);  // P (bf16x2) over the consumed S columns
-        tmem_wait_st();
+        // P(j) -> shared memory buffer b (free once PV(j-2) has retired)
+        if (j >= 2) mbar_wait(&pv_done[2 * mt + b], ((j - 2) >> 1) & 1);
+        uint8_t* prow = smem + OFF_P + (2 * mt + b) * P_TILE;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(prow + sw128(row, c)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        fence_async_smem();  // generic-proxy stores -> visible to the tensor pipe
         tc_fence_before();
         mbar_arrive(&p_full[2 * mt + b]);
         if (role < 4) trace(role, j, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
+      if (row == 0 && mt == 0) trace(0, 60, 3);
       mbar_wait(&o_final[mt], 0);
+      if (row == 0 && mt == 0) trace(0, 60, 4);
       tc_fence_after();
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
@@ -528,10 +557,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
       }
       if (valid) p.ws_lse[oi] = l > 0.f ? (m_used + __log2f(l)) / LOG2E : -INFINITY;
+      if (row == 0 && mt == 0) trace(0, 60, 5);
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) trace(0, 60, 6);
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");

@@ -186,9 +186,12 @@ int main() {
   long long* d;
   cudaMalloc(&d, 64);
   cudaMalloc(&g_src, 512 * 16384 + 16384);
-  run<true, 32, 2, 0, false, 1>(d, 1);
-  run<true, 32, 2, 7, false, 1>(d, 1);
-  run<true, 32, 2, 8, false, 1>(d, 1);
-  run<true, 32, 2, 7, true, 1>(d, 148);
+  // dependent chains (acc=1) vs independent accumulators
+  run<false, 64, 1, 0, true, 1>(d, 148);
+  run<false, 64, 2, 0, true, 1>(d, 148);
+  run<false, 64, 4, 0, true, 1>(d, 148);
+  run<false, 128, 1, 0, true, 1>(d, 148);
+  run<false, 128, 2, 0, true, 1>(d, 148);
+  run<true, 128, 1, 0, true, 1>(d, 148);
   return 0;
 }

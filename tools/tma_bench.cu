@@ -1,0 +1,150 @@
+// Microbenchmark: HBM streaming rate of a TMA ring per SM as a function of ring
+// depth and box shape, with the verify kernel's access pattern ([L][Hk][cap][128]
+// bf16, one contiguous key chunk per CTA, K and V tiles of 64 keys).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/tma_bench.cu -lcuda -o /tmp/tma_bench
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdint>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(c) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t ph) {
+  uint32_t done;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                 : "=r"(done) : "r"(smem_u32(b)), "r"(ph) : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+               "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void tma5(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+               "l"((uint64_t)m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4) : "memory");
+}
+__device__ __forceinline__ void bulk1d(void* dst, const void* src, uint32_t n, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+               "l"((uint64_t)src), "r"(n), "r"(smem_u32(bar)) : "memory");
+}
+
+// MODE 0: 2 x 4D boxes (64 dh x 64 rows) per 16 KB tile; 1: one 5D box (64 x 64 rows x 2 halves);
+// 2: one 1D bulk copy of the contiguous 16 KB
+template <int MODE>
+__global__ void __launch_bounds__(128, 1) stream(const __grid_constant__ CUtensorMap mk, const __grid_constant__ CUtensorMap mv,
+                                                 const __grid_constant__ CUtensorMap mk5, const __grid_constant__ CUtensorMap mv5,
+                                                 const uint8_t* kbase, const uint8_t* vbase, int cap, int chunk, int layer, int depth,
+                                                 long long* sink) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[16];
+  const int kvh = blockIdx.y, key_begin = blockIdx.x * chunk;
+  const int n_tiles = chunk / 64;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < depth; ++i) mbar_init(&full[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  auto issue = [&](int j) {
+    const int s = j % depth, key0 = key_begin + j * 64;
+    uint8_t* d = sm + s * 32768;
+    mbar_expect_tx(&full[s], 32768);
+    if (MODE == 0) {
+      tma4(d, &mk, &full[s], 0, key0, kvh, layer);
+      tma4(d + 8192, &mk, &full[s], 64, key0, kvh, layer);
+      tma4(d + 16384, &mv, &full[s], 0, key0, kvh, layer);
+      tma4(d + 24576, &mv, &full[s], 64, key0, kvh, layer);
+    } else if (MODE == 1) {
+      tma5(d, &mk5, &full[s], 0, key0, 0, kvh, layer);
+      tma5(d + 16384, &mv5, &full[s], 0, key0, 0, kvh, layer);
+    } else {
+      const size_t off = (((size_t)layer * gridDim.y + kvh) * cap + key0) * 256;
+      bulk1d(d, kbase + off, 16384, &full[s]);
+      bulk1d(d + 16384, vbase + off, 16384, &full[s]);
+    }
+  };
+  for (int j = 0; j < depth && j < n_tiles; ++j) issue(j);
+  long long acc = 0;
+  for (int j = 0; j < n_tiles; ++j) {
+    const int s = j % depth;
+    mbar_wait(&full[s], (j / depth) & 1);
+    acc += sm[s * 32768 + (j & 1023)];
+    if (j + depth < n_tiles) issue(j + depth);
+  }
+  if (acc == 123456789) sink[0] = acc;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 enc() {
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+  return (PFN_cuTensorMapEncodeTiled_v12000)f;
+}
+
+int main() {
+  const int L = 4, Hk = 8, cap = 54096 + 256, dh = 128;
+  const size_t bytes = (size_t)L * Hk * cap * dh * 2;
+  uint8_t *k, *v;
+  cudaMalloc(&k, bytes);
+  cudaMalloc(&v, bytes);
+  cudaMemset(k, 1, bytes);
+  cudaMemset(v, 1, bytes);
+  long long* sink;
+  cudaMalloc(&sink, 8);
+  auto e = enc();
+  CUtensorMap mk, mv, mk5, mv5;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)dh, (cuuint64_t)cap, (cuuint64_t)Hk, (cuuint64_t)L};
+    cuuint64_t str[3] = {(cuuint64_t)dh * 2, (cuuint64_t)cap * dh * 2, (cuuint64_t)Hk * cap * dh * 2};
+    cuuint32_t box[4] = {64, 64, 1, 1}, es[4] = {1, 1, 1, 1};
+    e(&mk, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, k, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    e(&mv, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, v, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  {
+    cuuint64_t dims[5] = {64, (cuuint64_t)cap, 2, (cuuint64_t)Hk, (cuuint64_t)L};
+    cuuint64_t str[4] = {(cuuint64_t)dh * 2, 128, (cuuint64_t)cap * dh * 2, (cuuint64_t)Hk * cap * dh * 2};
+    cuuint32_t box[5] = {64, 64, 2, 1, 1}, es[5] = {1, 1, 1, 1, 1};
+    CUresult r1 = e(&mk5, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, k, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    e(&mv5, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, v, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    printf("5D map encode: %d\n", (int)r1);
+  }
+  const int ctx = 54096, nch = 18, chunk = (ctx / nch + 63) / 64 * 64;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int mode = 0; mode < 3; ++mode) {
+    for (int depth : {2, 3, 4, 5, 6}) {
+      const int smem = depth * 32768 + 1024;
+      auto kern = mode == 0 ? stream<0> : (mode == 1 ? stream<1> : stream<2>);
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      dim3 grid(nch, Hk);
+      float best = 1e9;
+      for (int rep = 0; rep < 8; ++rep) {
+        const int layer = rep % L;
+        cudaEventRecord(a);
+        kern<<<grid, 128, smem>>>(mk, mv, mk5, mv5, k, v, cap, chunk, layer, depth, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (rep >= 2 && ms < best) best = ms;
+      }
+      const double byt = 2.0 * nch * chunk * Hk * 256;
+      printf("mode %d depth %d (%3d KB in flight/SM): %7.1f us  %6.0f GB/s  %s\n", mode, depth, depth * 32, best * 1e3,
+             byt / (best * 1e-3) / 1e9, cudaGetErrorString(cudaGetLastError()));
+    }
+  }
+  return 0;
+}
