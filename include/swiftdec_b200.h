@@ -70,7 +70,9 @@ int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int 
  * positions[t] from fp64-derived cos/sin tables [max_pos][dh/2] (f32).
  * q_rot = rope(q) * q_scale -> [T][H][dh] (q_dtype); q_pre = q (f32, nullable).
  * k_raw (nullable), k_rot, v written at row (row_offset + t) of each kv head.
- * rows_dev (nullable): rows t >= *rows_dev are skipped. */
+ * rows_dev (nullable): rows t >= *rows_dev are skipped. row_offset < 0: rows go
+ * to positions[0] + t (device-resident offset; k_raw / k_rot / v then point
+ * at row 0 of the layer). */
 int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t* positions,
                   const float* rope_cos, const float* rope_sin, float q_scale,
                   void* q_rot, int q_dtype, float* q_pre,
@@ -89,13 +91,19 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
  * T <= SD_TREE_MAX_ROWS. rows_dev (nullable): live row count <= T read on
  * device (rows beyond it produce zeros), so a padded verify forward needs no
  * host round trip. Partial-cache slots with rank < 0 are holes and skipped.
- * Split boundaries depend on ctx only (bitwise identical across GPU counts). */
+ * ctx_dev (nullable, src_kind 0): live cache length read on device; `ctx` is
+ * then an upper bound that sizes the grid and workspace, and the tree rows are
+ * taken from k_cache / v_cache right after the live rows (k_tree / v_tree are
+ * ignored). With ctx_dev every argument is step-invariant, so the call can be
+ * captured once in a CUDA graph and replayed as the cache grows.
+ * CUDA-core split boundaries depend on ctx only (bitwise identical across GPU
+ * counts); the tensor-core path splits by SM count. */
 size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx);
 int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
                  int src_kind, const void* k_cache, const void* v_cache, int kv_dtype, int64_t head_stride,
                  int ctx, const int32_t* ranks, const float* rope_cos, const float* rope_sin,
                  const void* k_tree, const void* v_tree, int64_t tree_head_stride,
-                 const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
+                 const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev, const int32_t* ctx_dev,
                  const void* tmap_k_host, const void* tmap_v_host, int layer,
                  void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
 /* 128-byte TMA descriptor (CUtensorMap) over a whole [L][Hk][cap][128] bf16
@@ -227,6 +235,7 @@ int sd_draft_tree(const void* ngram_table, int k, const int32_t* per_head, const
 #define SD_ST_HIST_LEN 2
 #define SD_ST_PENDING 3
 #define SD_ST_ERROR 4
+#define SD_ST_BASE 5        /* committed length n-1 (device-maintained by sd_accept_commit) */
 /* step result (int32[32]) slots */
 #define SD_RES_ACCEPTED 0
 #define SD_RES_BEST 1
@@ -235,6 +244,7 @@ int sd_draft_tree(const void* ngram_table, int k, const int32_t* per_head, const
 #define SD_RES_ROWS 4
 #define SD_RES_PATHS 5
 #define SD_RES_PENDING 6   /* int32 copy of the pending token (next draft input) */
+#define SD_RES_BASE 7      /* n-1 of the step (the verify rows' cache offset) */
 #define SD_RES_YS 8
 #define SD_RES_KEEP 16
 

@@ -19,8 +19,9 @@ TREE_MAX_ROWS, TREE_MAX_PATHS, TREE_MAX_DEPTH, MASK_WORDS = 256, 512, 8, 8
 MEMBER_NONE, MEMBER_MASK, MEMBER_WINDOW, MEMBER_TREE = 0, 1, 2, 3
 TRUNC_NONE, TRUNC_TOP_P, TRUNC_MIN_P, TRUNC_ETA = 0, 1, 2, 3
 IN_LOGITS_F32, IN_LOGITS_F64, IN_PROBS_F64 = 0, 1, 2
-ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR = 0, 1, 2, 3, 4
-RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_YS, RES_KEEP = 0, 1, 2, 3, 4, 5, 6, 8, 16
+ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR, ST_BASE = 0, 1, 2, 3, 4, 5
+RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_BASE = 0, 1, 2, 3, 4, 5, 6, 7
+RES_YS, RES_KEEP = 8, 16
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -54,7 +55,7 @@ _SIGS = {
     "sd_add_cast": (INT, [P, P, P, P, INT, SZ, P]),
     "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, P]),
     "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),
-    "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P,
+    "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P, P,
                            P, P, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
     "sd_debug_tc_trace": (INT, [P, INT]),

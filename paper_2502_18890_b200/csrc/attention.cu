@@ -34,8 +34,24 @@ struct AttnParams {
   float* ws_o;
   float* ws_lse;
   const int32_t* rows_dev;  // nullable: live row count (<= T) read on device
+  const int32_t* ctx_dev;   // nullable: live cache length (<= ctx) read on device; the tree
+                            // rows then sit right after it in k_cache / v_cache
   int x_base;               // chunk index of blockIdx.x == 0 (tree-only launches)
 };
+
+// live cache length and tree-row base pointers of kv head `kvh`
+template <int DH, typename KT>
+__device__ __forceinline__ int resolve_ctx(const AttnParams& p, int kvh, const KT*& Kt, const KT*& Vt) {
+  if (p.ctx_dev) {
+    const int c = *p.ctx_dev;
+    Kt = (const KT*)p.k_cache + kvh * p.head_stride + (int64_t)c * DH;
+    Vt = (const KT*)p.v_cache + kvh * p.head_stride + (int64_t)c * DH;
+    return c;
+  }
+  Kt = (const KT*)p.k_tree + kvh * p.tree_head_stride;
+  Vt = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+  return p.ctx;
+}
 
 __device__ __forceinline__ int live_rows(const AttnParams& p) {
   if (!p.rows_dev) return p.T;
@@ -182,16 +198,18 @@ __global__ void __launch_bounds__(256) attn_rows_kernel(AttnParams p) {
   const KT* K;
   const KT* V;
   int k_begin, k_end;
+  const KT *Kt, *Vt;
+  const int ctx = resolve_ctx<DH, KT>(p, kvh, Kt, Vt);
   if (tree) {
-    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
-    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    K = Kt;
+    V = Vt;
     k_begin = 0;
     k_end = Tl;
   } else {
     K = (const KT*)p.k_cache + kvh * p.head_stride;
     V = (const KT*)p.v_cache + kvh * p.head_stride;
     k_begin = cx * p.chunk;
-    k_end = min(p.ctx, k_begin + p.chunk);
+    k_end = min(ctx, k_begin + p.chunk);
   }
   float m[RPW], l[RPW], acc[RPW][EPL];
   const float* qrow[RPW];
@@ -268,16 +286,18 @@ __global__ void __launch_bounds__(128) attn_keys_kernel(AttnParams p) {
   const KT* K;
   const KT* V;
   int k_begin, k_end;
+  const KT *Kt, *Vt;
+  const int ctx = resolve_ctx<DH, KT>(p, kvh, Kt, Vt);
   if (tree) {
-    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
-    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    K = Kt;
+    V = Vt;
     k_begin = 0;
     k_end = Tl;
   } else {
     K = (const KT*)p.k_cache + kvh * p.head_stride;
     V = (const KT*)p.v_cache + kvh * p.head_stride;
     k_begin = cx * p.chunk;
-    k_end = min(p.ctx, k_begin + p.chunk);
+    k_end = min(ctx, k_begin + p.chunk);
   }
   float m[RPW], l[RPW], acc[RPW][EPL];
   const float* qrow[RPW];
@@ -379,13 +399,16 @@ __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* _
   for (int d = threadIdx.x; d < DH; d += blockDim.x) {
     float O0 = 0.f, O1 = 0.f, O2 = 0.f, O3 = 0.f;
     int c = 0;
+    // zero-weight splits (empty chunks past a device-resident context) are
+    // skipped: their partial slots are not written
     for (; c + 4 <= nsplit; c += 4) {
-      O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
-      O1 = fmaf(wsh[c + 1], ws_o[((int64_t)(c + 1) * TH + row) * DH + d], O1);
-      O2 = fmaf(wsh[c + 2], ws_o[((int64_t)(c + 2) * TH + row) * DH + d], O2);
-      O3 = fmaf(wsh[c + 3], ws_o[((int64_t)(c + 3) * TH + row) * DH + d], O3);
+      if (wsh[c] != 0.f) O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
+      if (wsh[c + 1] != 0.f) O1 = fmaf(wsh[c + 1], ws_o[((int64_t)(c + 1) * TH + row) * DH + d], O1);
+      if (wsh[c + 2] != 0.f) O2 = fmaf(wsh[c + 2], ws_o[((int64_t)(c + 2) * TH + row) * DH + d], O2);
+      if (wsh[c + 3] != 0.f) O3 = fmaf(wsh[c + 3], ws_o[((int64_t)(c + 3) * TH + row) * DH + d], O3);
     }
-    for (; c < nsplit; ++c) O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
+    for (; c < nsplit; ++c)
+      if (wsh[c] != 0.f) O0 = fmaf(wsh[c], ws_o[((int64_t)c * TH + row) * DH + d], O0);
     out[(int64_t)row * DH + d] = from_f<OT>(((O0 + O1) + (O2 + O3)) * inv);
   }
 }
@@ -469,16 +492,18 @@ __global__ void __launch_bounds__(128, (GM == 4 && sizeof(KT) == 2) ? 4 : 2) dec
   const KT* K;
   const KT* V;
   int k_begin, k_end;
+  const KT *Kt, *Vt;
+  const int ctx = resolve_ctx<DH, KT>(p, kvh, Kt, Vt);
   if (tree) {
-    K = (const KT*)p.k_tree + kvh * p.tree_head_stride;
-    V = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    K = Kt;
+    V = Vt;
     k_begin = 0;
     k_end = 1;
   } else {
     K = (const KT*)p.k_cache + kvh * p.head_stride;
     V = (const KT*)p.v_cache + kvh * p.head_stride;
     k_begin = cx * chunk;
-    k_end = min(p.ctx, k_begin + chunk);
+    k_end = min(ctx, k_begin + chunk);
   }
   const int per_warp = chunk / 4;
   const int w0 = k_begin + warp * per_warp, w1 = min(k_end, w0 + per_warp);
@@ -641,8 +666,8 @@ int tc_set_trace(void* dev_ptr, int force_chunks);
 int tc_n_chunks(int ctx, int Hk);
 int tc_chunk_len(int ctx, int n);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
-                     const int32_t* rows_dev, const uint32_t* mask, int mask_words, float* ws_o, float* ws_lse,
-                     int n_chunks, int chunk, cudaStream_t st);
+                     const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
+                     float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st);
 template <int DH, typename OT>
 __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
                                   int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out);
@@ -681,13 +706,15 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
                  const void* v_cache, int kv_dtype, int64_t head_stride, int ctx, const int32_t* ranks,
                  const float* rope_cos, const float* rope_sin, const void* k_tree, const void* v_tree,
                  int64_t tree_head_stride, const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
-                 const void* tmap_k_host, const void* tmap_v_host, int layer,
+                 const int32_t* ctx_dev, const void* tmap_k_host, const void* tmap_v_host, int layer,
                  void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
   SD_REQUIRE(T > 0 && T <= SD_TREE_MAX_ROWS, "sd_attention: T=%d out of range", T);
   SD_REQUIRE(H > 0 && Hk > 0 && H % Hk == 0, "sd_attention: heads");
   SD_REQUIRE(ctx >= 0, "sd_attention: ctx");
   SD_REQUIRE(!mask_bits || mask_words * 32 >= T, "sd_attention: mask words");
   SD_REQUIRE(src_kind == 0 || (ranks && rope_cos && rope_sin), "sd_attention: partial source needs ranks/rope");
+  SD_REQUIRE(!ctx_dev || (src_kind == 0 && tree_head_stride == head_stride),
+             "sd_attention: ctx_dev needs the full-cache source with the tree rows in the cache arrays");
   SD_REQUIRE(workspace_bytes >= sd_attention_workspace_bytes(T, H, dh, ctx), "sd_attention: workspace too small");
   SD_REQUIRE(ctx <= 256 * 8192, "sd_attention: ctx too large for the merge split limit");
   AttnParams p;
@@ -713,6 +740,7 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   p.ws_o = (float*)workspace;
   p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
   p.rows_dev = rows_dev;
+  p.ctx_dev = ctx_dev;
   p.x_base = 0;
   auto st = as_stream(stream);
   if (use_tc(tmap_k_host, tmap_v_host, q_dtype, kv_dtype, out_dtype, dh, src_kind, ctx)) {
@@ -721,14 +749,18 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     const int chunk = tc_chunk_len(ctx, nc);
     nc = (ctx + chunk - 1) / chunk;
     float* ws_lse = p.ws_o + (size_t)nc * T * H * dh;
-    int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, mask_bits, mask_words,
-                              p.ws_o, ws_lse, nc, chunk, st);
+    if (ctx_dev) {  // device-resident context: fixed grid, chunking resolved in the kernel
+      nc = tc_n_chunks(ctx, Hk);
+      ws_lse = p.ws_o + (size_t)nc * T * H * dh;
+    }
+    int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, ctx_dev, mask_bits,
+                              mask_words, p.ws_o, ws_lse, nc, chunk, st);
     if (rc) return rc;
     attn_merge_kernel<128, __nv_bfloat16><<<T * H, 128, 0, st>>>(p.ws_o, ws_lse, nc, T * H, H, rows_dev,
                                                                   (__nv_bfloat16*)out);
     return check_launch("sd_attention(tc merge)");
   }
-  if (T == 1 && p.G <= 8 && dh == 128 && !rows_dev) {
+  if (T == 1 && p.G <= 8 && dh == 128 && !rows_dev && !ctx_dev) {
     // single-row decode (draft / AR): latency-tolerant streaming kernel
     return dispatch_decode<128>(p, q_dtype, kv_dtype, out_dtype, src_kind, out, st);
   }

@@ -64,6 +64,7 @@ struct Params {
   int T, H, G;
   int layer, ctx, chunk, n_chunks;
   const int32_t* rows_dev;
+  const int32_t* ctx_dev;  // nullable: live cache length (chunking resolved per launch on device)
   const uint32_t* mask;    // [T][mask_words] tree rows (NULL = causal)
   int mask_words;
   float* ws_o;
@@ -246,10 +247,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int rg = blockIdx.z * ROWS;
   if (rg >= GT) return;
   if (tid == 0) trace(0, 60, 0);
-  const bool last = (int)blockIdx.x == p.n_chunks - 1;
-  const int key_begin = blockIdx.x * p.chunk;
-  const int cache_end = min(p.ctx, key_begin + p.chunk);
-  const int key_end = last ? p.ctx + T : cache_end;  // the last chunk also takes the tree rows
+  int ctx = p.ctx, chunk = p.chunk, n_live = p.n_chunks;
+  if (p.ctx_dev) {  // device-resident context: chunk the live length over the fixed grid
+    ctx = *p.ctx_dev;
+    chunk = (ctx + p.n_chunks - 1) / p.n_chunks;
+    chunk = chunk < BN ? BN : (chunk + BN - 1) / BN * BN;
+    n_live = ctx > 0 ? (ctx + chunk - 1) / chunk : 1;
+    if ((int)blockIdx.x >= n_live) {  // empty split: weight 0 in the merge
+      for (int r = tid; r < ROWS; r += THREADS) {
+        const int rho = rg + r;
+        if (rho < GT) {
+          const int t = rho / p.G, g = rho - t * p.G;
+          p.ws_lse[((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g] = -INFINITY;
+        }
+      }
+      return;
+    }
+  }
+  const bool last = (int)blockIdx.x == n_live - 1;
+  const int key_begin = blockIdx.x * chunk;
+  const int cache_end = min(ctx, key_begin + chunk);
+  const int key_end = last ? ctx + T : cache_end;  // the last chunk also takes the tree rows
   const int n_tiles = (key_end - key_begin + BN - 1) / BN;
   int act[2];
   for (int mt = 0; mt < 2; ++mt) {
@@ -462,7 +480,7 @@ __global__ void __launch_bounds__(THREADS, 1)
               if (k < cache_end) {
                 on = true;
               } else if (last && k < key_end) {
-                const int jt = k - p.ctx;
+                const int jt = k - ctx;
                 on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
               }
               vis |= (uint64_t)on << c;
@@ -633,8 +651,8 @@ int tc_chunk_len(int ctx, int n) {
 }
 
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
-                     const int32_t* rows_dev, const uint32_t* mask, int mask_words, float* ws_o, float* ws_lse,
-                     int n_chunks, int chunk, cudaStream_t st) {
+                     const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
+                     float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
@@ -650,6 +668,7 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   p.chunk = chunk;
   p.n_chunks = n_chunks;
   p.rows_dev = rows_dev;
+  p.ctx_dev = ctx_dev;
   p.mask = mask;
   p.mask_words = mask_words;
   p.ws_o = ws_o;

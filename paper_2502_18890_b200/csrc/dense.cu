@@ -145,7 +145,9 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   const int width = (H + 2 * Hk) * dh;
   const float* row = qkv + (int64_t)t * width;
   const int64_t pos = positions[t];
-  const int64_t dst_row = row_offset + t;
+  // row_offset < 0: rows go to positions[0] + t (verify rows staged after the
+  // committed cache; device-resident step under graph replay)
+  const int64_t dst_row = (row_offset >= 0 ? row_offset : (int64_t)positions[0]) + t;
   const int quads_rot = (H + Hk) * dh / 4, quads_all = width / 4;
   for (int u = threadIdx.x; u < quads_all; u += blockDim.x) {
     const float4 x = *reinterpret_cast<const float4*>(row + 4 * u);

@@ -281,6 +281,7 @@ __global__ void reconcile_kernel(const int32_t* __restrict__ result, int base, u
   extern __shared__ uint32_t buf[];  // [3][depth][row_w]
   const int layer = blockIdx.x, h = blockIdx.y;
   const int a = result[SD_RES_ACCEPTED];
+  if (base < 0) base = result[SD_RES_BASE];  // device-resident step (graph replay)
   const int64_t off = layer * layer_w + h * head_w;
   uint32_t* arrs[3] = {k_raw, k_rot, v};
   const int per = a * row_w;

@@ -78,7 +78,8 @@ __device__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
   if (a.positions) {
     rc.pos = a.positions[row];
   } else {
-    rc.pos = row == 0 ? a.n : a.n + a.tree[tree_off::NDEPTH + row - 1] + 1;
+    const int64_t n = a.n >= 0 ? a.n : a.state[SD_ST_BASE] + 1;  // n < 0: device-resident step
+    rc.pos = row == 0 ? n : n + a.tree[tree_off::NDEPTH + row - 1] + 1;
   }
   if (a.member_kind != SD_MEMBER_TREE || a.window <= 0 || row == 0) return;
   const int W = a.window;

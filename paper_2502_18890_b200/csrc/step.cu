@@ -296,6 +296,7 @@ __device__ void tree_build_dev(const int32_t* per_head, const Widths& W, int K, 
 __global__ void tree_build_kernel(const int32_t* per_head, Widths W, int K, const int32_t* grams,
                                   const int32_t* n_grams_dev, int n_grams_host, const int64_t* state,
                                   int64_t base_pos, int32_t* tree) {
+  if (base_pos < 0) base_pos = state[SD_ST_BASE];
   if (threadIdx.x || blockIdx.x) return;
   const int ng = n_grams_dev ? *n_grams_dev : n_grams_host;
   const int pending = state ? (int)state[SD_ST_PENDING] : -1;
@@ -304,6 +305,7 @@ __global__ void tree_build_kernel(const int32_t* per_head, Widths W, int K, cons
 
 __global__ void draft_tree_kernel(const void* ngram, int k, const int32_t* per_head, Widths W, int K,
                                   const int64_t* state, int64_t base_pos, int32_t* grams, int32_t* tree) {
+  if (base_pos < 0) base_pos = state[SD_ST_BASE];
   if (threadIdx.x || blockIdx.x) return;
   int ng = 0;
   if (ngram && k > 0) ng = ng_retrieve_dev(ngram, per_head[0], k, grams);
@@ -334,6 +336,7 @@ __global__ void accept_commit_kernel(const int32_t* __restrict__ tr, const int32
   using namespace tree_off;
   __shared__ int best[SD_TREE_MAX_PATHS];
   if (threadIdx.x || blockIdx.x) return;
+  if (n < 0) n = state[SD_ST_BASE] + 1;  // device-resident step (graph replay)
   const int P = tr[NPATHS];
   int best_v = -1, nb = 0;
   for (int p = 0; p < P; ++p) {
@@ -368,6 +371,7 @@ __global__ void accept_commit_kernel(const int32_t* __restrict__ tr, const int32
   result[SD_RES_ORIGIN] = tr[PORIGIN + pick];
   result[SD_RES_ROWS] = tr[tree_off::T];
   result[SD_RES_PATHS] = P;
+  result[SD_RES_BASE] = (int32_t)(n - 1);
   for (int j = 0; j < SD_TREE_MAX_DEPTH; ++j) {
     result[SD_RES_YS + j] = j < a ? ys[j] : -1;
     result[SD_RES_KEEP + j] = j < a ? keep[j] : -1;
@@ -383,6 +387,7 @@ __global__ void accept_commit_kernel(const int32_t* __restrict__ tr, const int32
     window_push_dev(ys[j], state, ring, cnt, W);
   }
   state[SD_ST_HIST_LEN] = hl + a;
+  state[SD_ST_BASE] = n - 1 + a;
   state[SD_ST_PENDING] = ys[a - 1];
   result[SD_RES_PENDING] = ys[a - 1];
   if (ngram) ng_update_dev(ngram, seq, tail, a);

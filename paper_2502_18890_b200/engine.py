@@ -16,6 +16,15 @@ Session.step() is Algorithm 1 (engine.py:185-302) with every stage on device:
 The only host round trip per step is that result copy; refresh decisions and
 slot bookkeeping are integer arithmetic on host scalars that mirror the
 device state exactly.
+
+Graph mode (default): every launch from the draft forward to the result copy
+takes only step-invariant arguments — the committed length lives on device
+(state[SD_ST_BASE], advanced by sd_accept_commit; the verify rows' cache
+offset and the attention context are read from the tree record), the draft
+attention scans the whole slot range (holes are masked by rank < 0) — so the
+step is captured once as a CUDA graph and replayed; per step the host issues
+one fill (draft position), one graph launch, and after the result copy the
+partial-cache admit/evict launch (plus a refresh every B - S tokens).
 """
 
 from __future__ import annotations
@@ -92,7 +101,7 @@ class Session:
     """One speculative generation run; owns its device caches and tables."""
 
     def __init__(self, model: TinyTransformer, prompt: list[int], config: EngineConfig,
-                 capacity: int | None = None, prefill: bool = True):
+                 capacity: int | None = None, prefill: bool = True, graph: bool = True):
         c = model.config
         gamma = c.gamma
         config.validate(gamma)
@@ -140,7 +149,11 @@ class Session:
         self.partial: PartialCache | None = None
         self.result[L.RES_PENDING] = self.tokens[-1]
         self.state[L.ST_PENDING] = self.tokens[-1]
+        self.state[L.ST_BASE] = len(self.tokens) - 1
         self._ev = torch.cuda.Event()
+        self.use_graph = graph
+        self._graph: torch.cuda.CUDAGraph | None = None
+        self._eager_steps = 0
         if prefill:
             t0 = time.perf_counter()
             self._prefill()
@@ -198,6 +211,7 @@ class Session:
         self.q_sum.normal_(0.0, 1.0, generator=g)
         self.result[L.RES_PENDING] = self.tokens[-1]
         self.state[L.ST_PENDING] = self.tokens[-1]
+        self.state[L.ST_BASE] = len(self.tokens) - 1
         self.partial = self._build_partial(ctx)
 
     # -------------------------------------------------------- partial cache --
@@ -227,17 +241,17 @@ class Session:
     def done(self) -> bool:
         return len(self.emitted) >= self.config.target_length
 
-    def _draft(self, n: int) -> int:
-        """Draft forward + penalised per-head top-w + n-gram tree (engine.py:199-217)."""
+    def _draft(self, n: int, graph: bool = False) -> None:
+        """Draft forward + penalised per-head top-w + n-gram tree (engine.py:199-217).
+        graph: step-invariant arguments only (whole slot range, base from state)."""
         m, cfg, smp = self.model, self.config, self.config.sampler
         part = self.partial
-        dm = part.count
-        self.draft_pos.fill_(dm)
         q_rot, kt, vt, out = self.q_rot_d, self.kt, self.vt, self.attn_out_d
+        hi = part.slot_cap if graph else part.hi
 
         def attend(l, qkv, q_pre):
             m.rope_stage(qkv, 1, self.draft_pos, q_rot, None, None, kt, vt, m.dh, 0)
-            m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, part.hi, part.prank[l], kt, vt,
+            m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt,
                         m.dh, None, None, out)
             return out
 
@@ -249,12 +263,13 @@ class Session:
         L.call("sd_draft_topw", L.ptr(logits), self.depth, m.config.vocab_size, L.ptr(win), smp.temperature,
                smp.theta, int(smp.ctrl_style), L.host_i32(cfg.tree.widths), L.ptr(self.per_head), L.stream())
         L.call("sd_draft_tree", self.ngrams.handle, cfg.k, L.ptr(self.per_head), L.host_i32(cfg.tree.widths),
-               self.depth, L.ptr(self.state), n - 1, L.ptr(self.grams), L.ptr(self.tree_rec), L.stream())
-        return dm
+               self.depth, L.ptr(self.state), -1 if graph else n - 1, L.ptr(self.grams), L.ptr(self.tree_rec),
+               L.stream())
 
-    def _verify(self, n: int) -> None:
+    def _verify(self, n: int, graph: bool = False) -> None:
         """Masked tree verification over the full cache + sampling + accept
-        + commit + reconcile (engine.py:221-290)."""
+        + commit + reconcile (engine.py:221-290). graph: the cache offset and
+        context come from the tree record / state on device."""
         m, cfg, smp = self.model, self.config, self.config.sampler
         F = self.full
         base = n - 1
@@ -267,12 +282,22 @@ class Session:
         bits = rec[lay["MASK"]:lay["MASK"] + T * L.MASK_WORDS]
         q_rot, out = self.q_rot_v, self.attn_out_v
 
-        def attend(l, qkv, q_pre):
-            m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l, :, base:], F.k_rot[l, :, base:], F.v[l, :, base:],
-                         F.head_stride, 0, rows_dev)
-            m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                        F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l)
-            return out
+        if graph:
+            ctx_max = F.capacity - T
+            ctx_dev = pos[0:1]  # tree record POS[0] = n - 1 = live cache length
+
+            def attend(l, qkv, q_pre):
+                m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l], F.k_rot[l], F.v[l], F.head_stride, -1, rows_dev)
+                m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, ctx_max, None, None, None,
+                            F.head_stride, bits, rows_dev, out, F.tmaps, l, ctx_dev=ctx_dev)
+                return out
+        else:
+            def attend(l, qkv, q_pre):
+                m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l, :, base:], F.k_rot[l, :, base:],
+                             F.v[l, :, base:], F.head_stride, 0, rows_dev)
+                m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
+                            F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l)
+                return out
 
         h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
         logits = m.lm_logits(h0)
@@ -284,13 +309,13 @@ class Session:
         a.win_count, a.win_ring, a.state = L.ptr(self.window.count), L.ptr(self.window.ring), L.ptr(self.state)
         a.window = smp.window
         a.tree, a.depth = L.ptr(rec), self.depth
-        a.positions, a.n = None, n
+        a.positions, a.n = None, -1 if graph else n
         a.token_out = L.ptr(self.y)
         L.call("sd_sample_rows", L.ptr(logits), a, L.stream())
-        L.call("sd_accept_commit", L.ptr(rec), L.ptr(self.y), self.select_seed, n, self.depth, int(cfg.bonus),
-               L.ptr(self.state), L.ptr(self.window.ring), L.ptr(self.window.count), smp.window,
+        L.call("sd_accept_commit", L.ptr(rec), L.ptr(self.y), self.select_seed, -1 if graph else n, self.depth,
+               int(cfg.bonus), L.ptr(self.state), L.ptr(self.window.ring), L.ptr(self.window.count), smp.window,
                L.ptr(self.history), self.ngrams.handle, L.ptr(self.result), L.stream())
-        F.reconcile_device(base, self.result, self.q_pre, T, m.H, self.q_sum)
+        F.reconcile_device(-1 if graph else base, self.result, self.q_pre, T, m.H, self.q_sum)
 
     def step(self) -> IterationRecord:
         if self.done:
@@ -303,16 +328,25 @@ class Session:
         if refreshed:
             self.partial = self._build_partial(len(self.full))
         t0 = time.perf_counter()
-        draft_ctx = self._draft(n)
-        self.forward_counts["draft"] += 1
-        t1 = time.perf_counter()
+        draft_ctx = self.partial.count
+        self.draft_pos.fill_(draft_ctx)
         base = n - 1
         if len(self.full) > base:
             self.full.truncate(base)
         self.full.reserve(self.Tmax)
-        self._verify(n)
+        if self.use_graph and self._eager_steps >= 1:
+            if self._graph is None:
+                self._capture()
+            self._graph.replay()
+            L.launch_count += self._graph_launches
+        else:
+            self._draft(n)
+            self._verify(n)
+            self.result_host.copy_(self.result, non_blocking=True)
+            self._eager_steps += 1
+        self.forward_counts["draft"] += 1
         self.forward_counts["verify"] += 1
-        self.result_host.copy_(self.result, non_blocking=True)
+        t1 = time.perf_counter()
         self._ev.record()
         self._ev.synchronize()
         r = self.result_host.tolist()
@@ -334,6 +368,27 @@ class Session:
                               draft_ctx=draft_ctx, verify_ctx=base, verify_rows=rows, path_index=pick)
         self.records.append(rec)
         return rec
+
+    def _capture(self) -> None:
+        """Capture draft + verify + result copy as one CUDA graph (step-invariant
+        launch arguments; see the module docstring). Capture does not run the
+        work: step() replays the graph right after."""
+        m, F = self.model, self.full
+        # size every workspace for the largest context first: no allocation may
+        # move under the captured pointers
+        m.workspace(max(L.load().sd_attention_workspace_bytes(self.Tmax, m.H, m.dh, F.capacity),
+                        L.load().sd_attention_workspace_bytes(1, m.H, m.dh, self.partial.slot_cap)))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        n = len(self.tokens)
+        l0 = L.launch_count
+        with torch.cuda.graph(g):
+            self._draft(n, graph=True)
+            self._verify(n, graph=True)
+            self.result_host.copy_(self.result, non_blocking=True)
+        self._graph_launches = L.launch_count - l0  # our kernels per replay
+        L.launch_count = l0
+        self._graph = g
 
     def metrics(self) -> RunMetrics:
         return collect_metrics(self.records, self.gamma, self.emitted, dict(self.forward_counts),

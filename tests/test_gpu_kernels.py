@@ -75,7 +75,7 @@ def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, T, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, lib.ptr(bits), lib.MASK_WORDS,
-             None, None, None, 0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+             None, None, None, None, 0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
     # oracle on the same (rounded) inputs
     Kr = kt.double().cpu().numpy().transpose(1, 0, 2)
     Vr = vt.double().cpu().numpy().transpose(1, 0, 2)
@@ -119,7 +119,7 @@ def test_verify_attention_tcgen05(lib, ctx, T, H, Hk, layer):
         ws = torch.empty(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
                  F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
-                 F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, tm[0], tm[1],
+                 F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, tm[0], tm[1],
                  layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
         outs.append(out.double().cpu().numpy().reshape(T, H, dh))
     Kr = F.k_rot[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
@@ -131,6 +131,60 @@ def test_verify_attention_tcgen05(lib, ctx, T, H, Hk, layer):
     np.testing.assert_allclose(outs[0], want, rtol=2e-2, atol=2e-2)
     np.testing.assert_allclose(outs[0], outs[1], rtol=2e-2, atol=2e-2)
     assert np.max(np.abs(outs[0] - want)) < 1.5e-2
+
+
+@pytest.mark.parametrize("tc", [True, False])
+@pytest.mark.parametrize("ctx", [70, 3000, 20000])
+def test_attention_ctx_dev_matches_host_ctx(lib, tc, ctx):
+    """Device-resident context (graph replay): ctx read on device with a larger
+    host upper bound, tree rows right after the live rows, stale workspace —
+    same result as the host-ctx call (bitwise on the CUDA-core path)."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200.model import mask_bits_from_bool
+    dev = torch.device("cuda")
+    g = np.random.default_rng(ctx)
+    T, H, Hk, dh, Lr, layer = 41, 32, 8, 128, 2, 1
+    cap = 24000
+    F = FullCache(Lr, Hk, dh, capacity=cap, dtype=torch.bfloat16)
+    F.k_rot.normal_()
+    F.v.normal_()
+    parent = [-1] + [int(g.integers(0, i)) for i in range(1, T)]
+    mask = np.zeros((T, T), dtype=bool)
+    for i in range(T):
+        j = i
+        while j >= 0:
+            mask[i, j] = True
+            j = parent[j]
+    bits = torch.as_tensor(mask_bits_from_bool(mask), device=dev)
+    qt = (torch.randn((T, H, dh), device=dev) * 0.2).to(torch.bfloat16)
+    tm = F.tmaps if tc else (None, None)
+    ctx_dev = torch.tensor([ctx], dtype=torch.int32, device=dev)
+    upper = cap - T
+    ws = torch.full((lib.load().sd_attention_workspace_bytes(T, H, dh, upper),), 255, dtype=torch.uint8, device=dev)
+    outs = []
+    for mode in ("host", "dev"):
+        out = torch.empty((T, H * dh), dtype=torch.bfloat16, device=dev)
+        if mode == "host":
+            lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
+                     F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
+                     F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, tm[0],
+                     tm[1], layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
+        else:
+            lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
+                     F.head_stride, upper, None, None, None, None, None, F.head_stride, lib.ptr(bits), lib.MASK_WORDS,
+                     None, lib.ptr(ctx_dev), tm[0], tm[1], layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(),
+                     lib.stream())
+        outs.append(out.float())
+    assert torch.isfinite(outs[1]).all()
+    if tc:
+        torch.testing.assert_close(outs[1], outs[0], rtol=2e-2, atol=2e-2)
+    Kr = F.k_rot[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
+    Vr = F.v[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
+    vis = np.zeros((T, ctx + T), dtype=bool)
+    vis[:, :ctx] = True
+    vis[:, ctx:] = mask
+    want = attend_oracle(qt.double().cpu().numpy(), Kr, Vr, vis)
+    np.testing.assert_allclose(outs[1].double().cpu().numpy().reshape(T, H, dh), want, rtol=2e-2, atol=2e-2)
 
 
 def test_attention_rows_dev_padding(lib):
@@ -149,7 +203,7 @@ def test_attention_rows_dev_padding(lib):
         ws = torch.empty(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 0, TT, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), 0, cap * dh, ctx, None,
                  None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, lib.ptr(rd),
-                 None, None, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
+                 None, None, None, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
         outs.append(out)
     assert torch.equal(outs[0][:Tl], outs[1])
     assert torch.all(outs[0][Tl:] == 0)
@@ -211,7 +265,7 @@ def test_decode_attention_full_cache(lib, dtype, ctx):
     ws = torch.empty(lib.load().sd_attention_workspace_bytes(1, H, dh, ctx), dtype=torch.uint8, device=dev)
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, 1, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
-             None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, None, None, None, 0,
+             None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, None, None, None, None, 0,
              lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
     Kr = kt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]
     Vr = vt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]

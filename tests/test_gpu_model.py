@@ -240,3 +240,26 @@ def test_session_mechanics():
     assert sum(r.accepted for r in s.records) == len(s.emitted)
     with pytest.raises(SessionExhausted):
         s.step()
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_graph_replay_equals_eager(dtype):
+    """The CUDA-graph step (device-resident base / context, whole slot range in
+    the draft) is the same computation as the eager step: identical tokens,
+    records and partial caches, across refreshes and evictions."""
+    from paper_2502_18890_b200 import Session
+    run = J["engine"][4]
+    mcfg, ecfg = oracle_session_cfg(run)
+    cfg = replace(device_cfg(ecfg), target_length=160)
+    m = dev_model(mcfg, dtype)
+    a = Session(m, run["prompt"], cfg, graph=False)
+    b = Session(m, run["prompt"], cfg, graph=True)
+    while not a.done:
+        ra, rb = a.step(), b.step()
+        assert rec_tuple(ra) == rec_tuple(rb), f"step {ra.step}"
+        assert a.partial.positions == b.partial.positions
+    assert a.emitted == b.emitted
+    assert b._graph is not None and b.device_error() == 0
+    assert torch.equal(a.q_sum, b.q_sum)
+    n = len(a.full)
+    assert torch.equal(a.full.k_rot[:, :, :n], b.full.k_rot[:, :, :n])
