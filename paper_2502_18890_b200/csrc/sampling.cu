@@ -41,6 +41,7 @@ struct RowCtx {
   int n_patch;
   int patch_tok[MAX_PATCH];
   int patch_val[MAX_PATCH];
+  uint32_t bloom[32];  // bit (v & 1023) set for every patched token v
   int64_t pos;
 };
 
@@ -51,8 +52,9 @@ __device__ __forceinline__ bool is_member(const SampleDev& a, const RowCtx& rc, 
     case SD_MEMBER_TREE: {
       if (a.window <= 0) return false;
       bool m = a.win_count[v] > 0;
-      for (int i = 0; i < rc.n_patch; ++i)
-        if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
+      if ((rc.bloom[(v >> 5) & 31] >> (v & 31)) & 1u)  // rare: v may be a patched token
+        for (int i = 0; i < rc.n_patch; ++i)
+          if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
       return m;
     }
     default: return false;
@@ -75,6 +77,7 @@ __device__ __forceinline__ double scaled(double l, bool member, const SampleDev&
 // thread 0: per-row patches (engine.py:155-181) and draw position
 __device__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
   rc.n_patch = 0;
+  for (int i = 0; i < 32; ++i) rc.bloom[i] = 0u;
   if (a.positions) {
     rc.pos = a.positions[row];
   } else {
@@ -118,6 +121,10 @@ __device__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
       rc.patch_tok[found] = tok;
     }
     rc.patch_val[found] = 1;
+  }
+  for (int i = 0; i < rc.n_patch; ++i) {
+    const int v = rc.patch_tok[i];
+    rc.bloom[(v >> 5) & 31] |= 1u << (v & 31);
   }
 }
 
@@ -212,11 +219,19 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   };
   const bool is_probs = IN == SD_IN_PROBS_F64;
   if (FAST) {
+    // one pass: running max and sum of exp per thread, combined in fp64
     float lm = -INFINITY;
-    for (int v = tid; v < V; v += SMP_THREADS) lm = fmaxf(lm, scaled_f(v));
-    mf = block_reduce(lm, (float*)dred, [](float x, float y) { return fmaxf(x, y); });
     double lz = 0.0;
-    for (int v = tid; v < V; v += SMP_THREADS) lz += (double)expf(scaled_f(v) - mf);
+    for (int v = tid; v < V; v += SMP_THREADS) {
+      const float s = scaled_f(v);
+      if (s > lm) {
+        lz = lz * (double)expf(lm - s);  // exp(-inf) = 0 on the first element
+        lm = s;
+      }
+      lz += (double)expf(s - lm);
+    }
+    mf = block_reduce(lm, (float*)dred, [](float x, float y) { return fmaxf(x, y); });
+    lz = lm == -INFINITY ? 0.0 : lz * exp((double)lm - (double)mf);
     Z = block_reduce(lz, dred, sum_op);
     invZ = 1.0 / Z;
   } else if (!is_probs) {
@@ -362,30 +377,49 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
     }
     return p >= thr ? p : 0.0;
   };
+  // ---- kept mass in warp-contiguous chunks (coalesced; chunk w = [w*S, (w+1)*S)) ----
+  const int lane = tid & 31, wid = tid >> 5;
+  constexpr int NWARP = SMP_THREADS / 32;
+  const int S = (V + NWARP * 32 - 1) / (NWARP * 32) * 32;
+  const int c0 = wid * S, c1 = min(V, c0 + S);
   double lk = 0.0;
-  for (int v = tid; v < V; v += SMP_THREADS) lk += kept(v, prob(v));
-  const double K = block_reduce(lk, dred, sum_op);
+  for (int v = c0 + lane; v < c1; v += 32) lk += kept(v, prob(v));
+  lk = warp_sum_d(lk);
+  __shared__ double wtot[NWARP];
+  if (lane == 0) wtot[wid] = lk;
+  __syncthreads();
+  double K = 0.0;
+  for (int w = 0; w < NWARP; ++w) K += wtot[w];
   if (a.trunc_out)
     for (int v = tid; v < V; v += SMP_THREADS) a.trunc_out[base + v] = kept(v, prob(v)) / K;
   if (!a.token_out) return;
   // ---- inverse CDF: first v with cumsum(kept / K) > u ----
+  // the warp whose chunk holds the crossing walks it 32 keys at a time
   const double u = uniform_at(a.seed, (uint64_t)rc.pos);
-  const int seg = (V + SMP_THREADS - 1) / SMP_THREADS;
-  const int b0 = tid * seg, b1 = min(V, b0 + seg);
-  double ssum = 0.0;
-  for (int v = b0; v < b1; ++v) ssum += kept(v, prob(v)) / K;
-  double tot;
-  const double before = block_exclusive_scan(ssum, dred, &tot);
+  double before = 0.0;
+  for (int w = 0; w < wid; ++w) before += wtot[w] / K;
+  const double mine = wtot[wid] / K;
+  const bool last_warp = c1 >= V || wid == NWARP - 1;
   if (tid == 0) s_int[1] = V;
   __syncthreads();
-  if (b0 < b1 && before + ssum > u && before <= u) {
+  // (chunk prefix sums and the walk round differently: neighbouring warps within
+  // 1e-12 of the crossing also walk; the lowest hit wins)
+  if (c0 < c1 && before <= u + 1e-12 && (before + mine > u - 1e-12 || last_warp)) {
     double c = before;
-    for (int v = b0; v < b1; ++v) {
-      c += kept(v, prob(v)) / K;
-      if (c > u) {
-        atomicMin(&s_int[1], v);
+    for (int v0 = c0; v0 < c1; v0 += 32) {
+      const int v = v0 + lane;
+      double x = v < c1 ? kept(v, prob(v)) / K : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, v < c1 && c + x > u);
+      if (hit) {
+        if (lane == 0) atomicMin(&s_int[1], v0 + __ffs(hit) - 1);
         break;
       }
+      c += __shfl_sync(0xffffffffu, x, 31);
     }
   }
   __syncthreads();
