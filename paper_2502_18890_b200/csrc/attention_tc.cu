@@ -33,7 +33,7 @@ namespace tc {
 constexpr int BN = 64;          // keys per tile
 constexpr int DH = 128;
 #ifndef SD_TC_ST
-#define SD_TC_ST 3
+#define SD_TC_ST 4
 #endif
 constexpr int ST = SD_TC_ST;    // K ring depth == V ring depth
 constexpr int THREADS = 384;
@@ -47,8 +47,9 @@ constexpr int P_TILE = 128 * BN * 2;            // 16 KB: [128 rows][64 keys * 2
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
-constexpr int OFF_P = OFF_V + ST * KV_TILE;     // [mt][buf]
-constexpr int OFF_BAR = OFF_P + 4 * P_TILE;
+constexpr int OFF_P = OFF_V + ST * KV_TILE;     // [mt]: one P buffer per M-tile (P(j) is written
+                                                // after PV(j-1) retired, which it has by then)
+constexpr int OFF_BAR = OFF_P + 2 * P_TILE;
 constexpr int N_BAR = 4 * ST + 4 * 4 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
@@ -277,32 +278,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   const int nm = act[1] > 0 ? 2 : 1;
 
-  // ---- stage Q (M-tiles, K-major SW128): all loads in flight, then stores ----
-  {
-    constexpr int PER = (ROWS * (DH / 8) + THREADS - 1) / THREADS;  // 16-byte chunks per thread
-    uint4 v[PER];
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = tid + k * THREADS;
-      const int row = i >> 4, c = i & 15;
-      const int rho = rg + row;
-      v[k] = make_uint4(0, 0, 0, 0);
-      if (i < ROWS * 16 && rho < GT) {
-        const int t = rho / p.G, g = rho - t * p.G;
-        v[k] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8));
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = tid + k * THREADS;
-      if (i < ROWS * 16) {
-        const int row = i >> 4, c = i & 15;
-        const int mt = row >> 7, r = row & 127, half = c >> 3;
-        *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v[k];
-      }
-    }
-  }
-  if (tid == 0) trace(0, 60, 1);
+  // ---- barriers first, so the TMA producers start streaming at once ----
   if (tid == 0) {
     for (int s = 0; s < ST; ++s) {
       mbar_init(&k_full[s], 1);
@@ -322,18 +298,47 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     fence_barrier_init();
   }
-  if (warp == 2) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  fence_async_smem();
-  tc_fence_before();
   __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  if (tid == 0) trace(0, 60, 2);
+  uint32_t tmem = 0;
+  if (warp != 0 && warp != 3) {
+    // ---- stage Q (M-tiles, K-major SW128) while the first K/V tiles are in flight ----
+    constexpr int NT = THREADS - 64;  // warps 1, 2, 4..11
+    const int qt = tid < 96 ? tid - 32 : tid - 64;
+    constexpr int PER = (ROWS * (DH / 8) + NT - 1) / NT;  // 16-byte chunks per thread
+    uint4 v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = qt + k * NT;
+      const int row = i >> 4, c = i & 15;
+      const int rho = rg + row;
+      v[k] = make_uint4(0, 0, 0, 0);
+      if (i < ROWS * 16 && rho < GT) {
+        const int t = rho / p.G, g = rho - t * p.G;
+        v[k] = __ldg(reinterpret_cast<const uint4*>(p.q + ((int64_t)t * p.H + kvh * p.G + g) * DH + c * 8));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = qt + k * NT;
+      if (i < ROWS * 16) {
+        const int row = i >> 4, c = i & 15;
+        const int mt = row >> 7, r = row & 127, half = c >> 3;
+        *reinterpret_cast<uint4*>(smem + OFF_Q + mt * 32768 + half * 16384 + sw128(r, c & 7)) = v[k];
+      }
+    }
+    if (warp == 2) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_async_smem();
+    tc_fence_before();
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");  // Q staged + TMEM allocated (consumers only)
+    tc_fence_after();
+    tmem = *tmem_slot;
+    if (tid == 32) trace(0, 60, 2);
+  }
 
   if (warp == 0 || warp == 3) {
     // ================= TMA producers: K (warp 0) and V (warp 3), decoupled =================
@@ -406,7 +411,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (mt == 0) trace(1, j, 3);
         mbar_wait(&v_full[s], (j / ST) & 1);
         const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
-        const uint32_t p_base = smem_u32(smem + OFF_P + (2 * mt + b) * P_TILE);
+        const uint32_t p_base = smem_u32(smem + OFF_P + mt * P_TILE);
         mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
         if (mt == 0) trace(1, j, 4);
         tc_fence_after();
@@ -464,7 +469,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_before();
         mbar_arrive(&s_free[2 * mt + b]);  // S(j) is in registers: QK(j+2) may reuse the buffer
         if (SD_TC_EXPERIMENT == 1 || SD_TC_EXPERIMENT == 4) {
-          if (j >= 2) mbar_wait(&pv_done[2 * mt + b], ((j - 2) >> 1) & 1);
+          if (j >= 1) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
           mbar_arrive(&p_full[2 * mt + b]);
           l += __uint_as_float(sr[lane]);
           continue;
@@ -524,9 +529,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         if (role < 4) trace(role, j, 2);
+        bool rescale_waited = false;
         if (__any_sync(0xffffffffu, rescale)) {
           // O must be stable: wait for every earlier O += P V of this M-tile (PV(j-1) retires last)
           if (j > 0) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          rescale_waited = true;
           tc_fence_after();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -541,9 +548,10 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_wait_st();
         }
         if (role < 4) trace(role, j, 3);
-        // P(j) -> shared memory buffer b (free once PV(j-2) has retired)
-        if (j >= 2) mbar_wait(&pv_done[2 * mt + b], ((j - 2) >> 1) & 1);
-        uint8_t* prow = smem + OFF_P + (2 * mt + b) * P_TILE;
+        // P(j) -> the M-tile's P buffer, free once PV(j-1) has retired (the
+        // rescale above may already have waited for it)
+        if (j >= 1 && !rescale_waited) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        uint8_t* prow = smem + OFF_P + mt * P_TILE;
 #pragma unroll
         for (int c = 0; c < 8; ++c)
           *reinterpret_cast<uint4*>(prow + sw128(row, c)) =

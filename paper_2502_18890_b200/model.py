@@ -221,9 +221,8 @@ class TinyTransformer:
                 return t
             return torch.as_tensor(reference_tensor(c, idx, shape, scale), dtype=torch.float64).to(dev)
 
-        H, Hk, dh, d = c.num_heads, c.num_kv_heads, c.head_dim, c.hidden_dim
-        q0, q1 = self.rank * self.H * dh, (self.rank + 1) * self.H * dh
-        k0, k1 = self.rank * self.Hk * dh, (self.rank + 1) * self.Hk * dh
+        from .parallel import shard_heads
+        (q0, q1), (k0, k1) = shard_heads(c.num_heads, c.num_kv_heads, c.head_dim, self.rank, self.world)
         self.layers = []
         cur: dict = {}
         for idx, (name, shape, scale) in enumerate(specs):

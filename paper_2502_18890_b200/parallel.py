@@ -42,10 +42,21 @@ def init_from_env(backend: str = "nccl"):
 
 
 def gather_rank_major(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
-    """All-gather x from every rank -> [world, *x.shape] in rank order."""
-    out = torch.empty((world,) + tuple(x.shape), dtype=x.dtype, device=x.device)
-    dist.all_gather_into_tensor(out, x.contiguous(), group=group)
-    return out
+    """All-gather x from every rank -> [world, *x.shape] in rank order (NCCL
+    over NVLink on the product path; gloo in the CPU tests)."""
+    flat = torch.empty((world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    dist.all_gather_into_tensor(flat, x.contiguous(), group=group)
+    return flat.view((world,) + tuple(x.shape))
+
+
+def shard_heads(num_heads: int, num_kv_heads: int, head_dim: int, rank: int, world: int):
+    """Column ranges of this rank's query and kv heads in Wq / Wk / Wv
+    (rank r owns kv heads [r*Hk/P, (r+1)*Hk/P) and their G query heads)."""
+    if num_kv_heads % world:
+        raise ValueError(f"{num_kv_heads} kv heads cannot be sharded over {world} ranks")
+    hk = num_kv_heads // world
+    h = hk * (num_heads // num_kv_heads)
+    return (rank * h * head_dim, (rank + 1) * h * head_dim), (rank * hk * head_dim, (rank + 1) * hk * head_dim)
 
 
 def all_gather_heads(o: torch.Tensor, world: int, group=None) -> torch.Tensor:
