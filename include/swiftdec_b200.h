@@ -56,9 +56,11 @@ const char* sd_last_error(void);
 /* ---- dense-layer plumbing (model.py:234-236, 278, 306-311) ---- */
 /* h[t,:] = embed[tokens[t],:] (as f32) */
 int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, float* h, sd_stream_t stream);
-/* h += delta (if delta); x = h * gain / sqrt(mean(h^2) + eps) -> x (x_dtype) */
+/* h += delta (if delta); x = h * gain / sqrt(mean(h^2) + eps) -> x (x_dtype).
+ * delta may be `delta_splits` split-K slices `delta_split_stride` floats apart
+ * (sd_gemm output), summed in slice order. */
 int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain, float eps,
-                   void* x, int x_dtype, sd_stream_t stream);
+                   void* x, int x_dtype, int delta_splits, int64_t delta_split_stride, sd_stream_t stream);
 /* out = a / (1 + exp(-a)) */
 int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stream);
 /* out = a + b (f32), cast_out = (cast_dtype) out (nullable) */
@@ -70,6 +72,8 @@ int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int 
  * positions[t] from fp64-derived cos/sin tables [max_pos][dh/2] (f32).
  * q_rot = rope(q) * q_scale -> [T][H][dh] (q_dtype); q_pre = q (f32, nullable).
  * k_raw (nullable), k_rot, v written at row (row_offset + t) of each kv head.
+ * qkv may be `qkv_splits` split-K slices (sd_gemm) `qkv_split_stride` floats
+ * apart, summed in slice order.
  * rows_dev (nullable): rows t >= *rows_dev are skipped. row_offset < 0: rows go
  * to positions[0] + t (device-resident offset; k_raw / k_rot / v then point
  * at row 0 of the layer). */
@@ -77,7 +81,7 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
                   const float* rope_cos, const float* rope_sin, float q_scale,
                   void* q_rot, int q_dtype, float* q_pre,
                   void* k_raw, void* k_rot, void* v, int kv_dtype, int64_t head_stride, int64_t row_offset,
-                  const int32_t* rows_dev, sd_stream_t stream);
+                  const int32_t* rows_dev, int qkv_splits, int64_t qkv_split_stride, sd_stream_t stream);
 
 /* ---- split-KV attention: verify tree / draft / AR (model.py:238-247, 290-305) ----
  * Row t (query head j uses kv head j / (H/Hk)) attends to
@@ -117,6 +121,26 @@ int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap
  * disables); force_chunks > 0 overrides the chunk count. Not used by the
  * product path. */
 int sd_debug_tc_trace(void* trace_dev, int force_chunks);
+
+/* ---- weight-streaming dense layers (model.py:283-285, 306-309) ----
+ * Y = X[M][K] . W[K][N] (bf16 in, fp32 accumulate) on tcgen05, M <= 128
+ * (decode rows), K % 64 == 0, N % 128 == 0. The weight is stored N-tiled,
+ * [N/128][K][128] (sd_tile_weight from the row-major [K][N] reference layout),
+ * stored as [N/128][2][K][64]) and described once by sd_make_weight_tmap.
+ * epi SD_GEMM_EPI_F32: y holds S = sd_gemm_splits(M, N, K, epi) fp32 split-K
+ * slices [S][M][ldy] whose in-order sum is Y (sd_add_rmsnorm / sd_rope_stage
+ * take the slices directly). SD_GEMM_EPI_SILU_BF16: y = bf16 silu(Y) [M][ldy]
+ * (the MLP's non-gated SiLU); for M <= 16 it is split-K too, reduced in split
+ * order inside the kernel through `workspace` (sd_gemm_workspace_bytes; zero it
+ * once before first use — the kernel leaves it zeroed). */
+#define SD_GEMM_EPI_F32 0
+#define SD_GEMM_EPI_SILU_BF16 1
+int sd_tile_weight(const void* w, int K, int N, void* w_tiled, sd_stream_t stream);
+int sd_make_weight_tmap(const void* w_tiled, int K, int N, void* tmap_out_host);
+int sd_gemm_splits(int M, int N, int K, int epi);
+size_t sd_gemm_workspace_bytes(int M, int N, int K);
+int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi, void* y, int64_t ldy,
+            void* workspace, size_t workspace_bytes, sd_stream_t stream);
 
 /* ---- Eq. 2 importance (kvcache.py:243-265) ----
  * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),

@@ -19,6 +19,7 @@ TREE_MAX_ROWS, TREE_MAX_PATHS, TREE_MAX_DEPTH, MASK_WORDS = 256, 512, 8, 8
 MEMBER_NONE, MEMBER_MASK, MEMBER_WINDOW, MEMBER_TREE = 0, 1, 2, 3
 TRUNC_NONE, TRUNC_TOP_P, TRUNC_MIN_P, TRUNC_ETA = 0, 1, 2, 3
 IN_LOGITS_F32, IN_LOGITS_F64, IN_PROBS_F64 = 0, 1, 2
+GEMM_EPI_F32, GEMM_EPI_SILU_BF16 = 0, 1
 ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR, ST_BASE = 0, 1, 2, 3, 4, 5
 RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_BASE = 0, 1, 2, 3, 4, 5, 6, 7
 RES_YS, RES_KEEP = 8, 16
@@ -50,14 +51,19 @@ _SIGS = {
     "sd_version": (INT, []),
     "sd_last_error": (C.c_char_p, []),
     "sd_embed": (INT, [P, INT, P, INT, INT, P, P]),
-    "sd_add_rmsnorm": (INT, [P, P, INT, INT, P, F32, P, INT, P]),
+    "sd_add_rmsnorm": (INT, [P, P, INT, INT, P, F32, P, INT, INT, I64, P]),
     "sd_silu": (INT, [P, P, INT, SZ, P]),
     "sd_add_cast": (INT, [P, P, P, P, INT, SZ, P]),
-    "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, P]),
+    "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, INT, I64, P]),
     "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P, P,
                            P, P, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
+    "sd_tile_weight": (INT, [P, INT, INT, P, P]),
+    "sd_make_weight_tmap": (INT, [P, INT, INT, P]),
+    "sd_gemm_splits": (INT, [INT, INT, INT, INT]),
+    "sd_gemm_workspace_bytes": (SZ, [INT, INT, INT]),
+    "sd_gemm": (INT, [P, INT, INT, P, INT, INT, P, I64, P, SZ, P]),
     "sd_debug_tc_trace": (INT, [P, INT]),
     "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
     "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
@@ -117,7 +123,8 @@ def require_cuda():
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
-              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_debug_tc_trace"}
+              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
+              "sd_gemm_splits", "sd_gemm_workspace_bytes"}
 launch_count = 0
 
 

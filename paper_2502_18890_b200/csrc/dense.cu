@@ -52,7 +52,8 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* x, int64_t 
 
 template <typename XT, int PER>
 __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
-                                   const float* __restrict__ gain, float eps, XT* __restrict__ x) {
+                                   const float* __restrict__ gain, float eps, XT* __restrict__ x, int splits,
+                                   int64_t split_stride) {
   __shared__ float red[32];
   const int64_t base = (int64_t)blockIdx.x * d;
   float4 v[PER];
@@ -63,7 +64,11 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
     if (i < d) {
       v[k] = *reinterpret_cast<const float4*>(h + base + i);
       if (delta) {
-        const float4 dd = *reinterpret_cast<const float4*>(delta + base + i);
+        float4 dd = *reinterpret_cast<const float4*>(delta + base + i);
+        for (int s = 1; s < splits; ++s) {  // split-K slices, summed in order
+          const float4 e = *reinterpret_cast<const float4*>(delta + s * split_stride + base + i);
+          dd.x += e.x; dd.y += e.y; dd.z += e.z; dd.w += e.w;
+        }
         v[k].x += dd.x; v[k].y += dd.y; v[k].z += dd.z; v[k].w += dd.w;
         *reinterpret_cast<float4*>(h + base + i) = v[k];
       }
@@ -84,14 +89,17 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
 
 template <typename XT>
 __global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
-                                          const float* __restrict__ gain, float eps, XT* __restrict__ x) {
+                                          const float* __restrict__ gain, float eps, XT* __restrict__ x, int splits,
+                                          int64_t split_stride) {
   __shared__ float red[32];
   const int64_t base = (int64_t)blockIdx.x * d;
   float ss = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     float v = h[base + i];
     if (delta) {
-      v += delta[base + i];
+      float dd = delta[base + i];
+      for (int s = 1; s < splits; ++s) dd += delta[s * split_stride + base + i];
+      v += dd;
       h[base + i] = v;
     }
     ss += v * v;
@@ -138,7 +146,7 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
                                   const float* __restrict__ sinT, float q_scale, QT* __restrict__ q_rot,
                                   float* __restrict__ q_pre, KT* __restrict__ k_raw, KT* __restrict__ k_rot,
                                   KT* __restrict__ v, int64_t head_stride, int64_t row_offset,
-                                  const int32_t* __restrict__ rows_dev) {
+                                  const int32_t* __restrict__ rows_dev, int splits, int64_t split_stride) {
   const int t = blockIdx.x;
   if (rows_dev && t >= *rows_dev) return;
   const int half = dh >> 1;
@@ -150,7 +158,11 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   const int64_t dst_row = (row_offset >= 0 ? row_offset : (int64_t)positions[0]) + t;
   const int quads_rot = (H + Hk) * dh / 4, quads_all = width / 4;
   for (int u = threadIdx.x; u < quads_all; u += blockDim.x) {
-    const float4 x = *reinterpret_cast<const float4*>(row + 4 * u);
+    float4 x = *reinterpret_cast<const float4*>(row + 4 * u);
+    for (int s = 1; s < splits; ++s) {  // split-K slices of the QKV GEMM, summed in order
+      const float4 e = *reinterpret_cast<const float4*>(row + s * split_stride + 4 * u);
+      x.x += e.x; x.y += e.y; x.z += e.z; x.w += e.w;
+    }
     const int col = 4 * u, head = col / dh, e = col - head * dh;
     if (u < quads_rot) {
       const int j = e >> 1;  // pair index of x.x/x.y; x.z/x.w is j + 1
@@ -208,7 +220,8 @@ int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, 
 }
 
 int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain, float eps, void* x, int x_dtype,
-                   sd_stream_t stream) {
+                   int delta_splits, int64_t delta_split_stride, sd_stream_t stream) {
+  if (delta_splits < 1) delta_splits = 1;
   SD_REQUIRE(T > 0 && d > 0, "sd_add_rmsnorm: bad sizes");
   SD_REQUIRE(x_dtype == SD_BF16 || x_dtype == SD_F32, "sd_add_rmsnorm: dtype");
   auto st = as_stream(stream);
@@ -216,7 +229,7 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
     const int quads = d / 4;
     const int threads = quads >= 1024 ? 1024 : ((quads + 31) / 32) * 32;
     const bool two = quads > threads;
-#define SD_NORM(XT, PER) add_rmsnorm_kernel<XT, PER><<<T, threads, 0, st>>>(h, delta, d, gain, eps, (XT*)x)
+#define SD_NORM(XT, PER) add_rmsnorm_kernel<XT, PER><<<T, threads, 0, st>>>(h, delta, d, gain, eps, (XT*)x, delta_splits, delta_split_stride)
     if (x_dtype == SD_BF16) {
       if (two) SD_NORM(__nv_bfloat16, 2); else SD_NORM(__nv_bfloat16, 1);
     } else {
@@ -226,9 +239,9 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
   } else {
     const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
     if (x_dtype == SD_BF16)
-      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x);
+      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x, delta_splits, delta_split_stride);
     else
-      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x);
+      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x, delta_splits, delta_split_stride);
   }
   return check_launch("sd_add_rmsnorm");
 }
@@ -257,12 +270,14 @@ int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int 
 int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t* positions, const float* rope_cos,
                   const float* rope_sin, float q_scale, void* q_rot, int q_dtype, float* q_pre, void* k_raw,
                   void* k_rot, void* v, int kv_dtype, int64_t head_stride, int64_t row_offset,
-                  const int32_t* rows_dev, sd_stream_t stream) {
+                  const int32_t* rows_dev, int qkv_splits, int64_t qkv_split_stride, sd_stream_t stream) {
+  if (qkv_splits < 1) qkv_splits = 1;
   SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 4) == 0, "sd_rope_stage: head_dim must be a multiple of 4");
   auto st = as_stream(stream);
 #define SD_RS(QT, KT)                                                                                          \
   rope_stage_kernel<QT, KT><<<T, 512, 0, st>>>(qkv, H, Hk, dh, positions, rope_cos, rope_sin, q_scale, (QT*)q_rot, \
-                                              q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev)
+                                              q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev, \
+                                              qkv_splits, qkv_split_stride)
   if (q_dtype == SD_F32 && kv_dtype == SD_F32)
     SD_RS(float, float);
   else if (q_dtype == SD_BF16 && kv_dtype == SD_BF16)

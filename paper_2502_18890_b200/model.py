@@ -7,9 +7,11 @@ draft heads (Eq. 1, model.py:104-120). Weights live in HBM in `dtype`
 and every GEMM accumulator are fp32.
 
 Per layer the forward is: fused residual-add + RMSNorm (sd_add_rmsnorm) ->
-QKV GEMM (cuBLAS via torch.mm, fp32 out) -> RoPE + KV staging (sd_rope_stage)
--> split-KV attention (sd_attention: verify tree / draft / AR / prefill block)
--> O GEMM -> add + RMSNorm -> W1 GEMM -> SiLU (sd_silu) -> W2 GEMM.
+QKV GEMM -> RoPE + KV staging (sd_rope_stage) -> split-KV attention
+(sd_attention: verify tree / draft / AR / prefill block) -> O GEMM -> add +
+RMSNorm -> W1 GEMM + SiLU -> W2 GEMM. Decode rows (<= 128) use the
+weight-streaming tcgen05 GEMM (sd_gemm, N-tiled weight copies, split-K slices
+summed by the consuming norm / RoPE kernel); prefill and fp32 builds use cuBLAS.
 
 KV-head sharding (world > 1): rank r owns kv heads [r*Hk/P, (r+1)*Hk/P) and
 their query heads; attention outputs are all-gathered before the replicated
@@ -157,6 +159,14 @@ def _validate(req: ForwardRequest, max_positions: int) -> int:
     return ctx
 
 
+def _splits(y: torch.Tensor) -> tuple[int, int]:
+    """(slices, elements between slices) of a dense() output: [S, T, N] split-K
+    slices from sd_gemm or a plain [T, N] product."""
+    if y.dim() == 3:
+        return y.shape[0], y.shape[1] * y.shape[2]
+    return 1, 0
+
+
 def mask_bits_from_bool(block: np.ndarray) -> np.ndarray:
     """(T, T) bool over request rows -> int32 [T][MASK_WORDS] bit rows
     (only j <= r is honoured, like _row_ancestors, model.py:146-147)."""
@@ -248,7 +258,52 @@ class TinyTransformer:
             del t
         if not hasattr(self, "heads"):
             self.heads = []
+        self._gemm_ws = None
+        if dt == torch.bfloat16 and self.use_gemm:
+            self._make_gemm_maps()
         torch.cuda.empty_cache()
+
+    # Weight-streaming tcgen05 GEMM (sd_gemm) for the decode rows. Off by
+    # default: on the cfg3 shapes it measures 0.7-1.5x cuBLAS (its activation
+    # loads queue behind the weight stream in the SM's TMA unit; see DESIGN.md
+    # §7), so the product path keeps cuBLAS for the dense layers.
+    use_gemm = False
+
+    def _make_gemm_maps(self):
+        """N-tiled copies [N/128][K][128] of the layer weights for sd_gemm (the
+        row-major originals stay for cuBLAS prefill)."""
+        import ctypes
+        need = 0
+        for ly in self.layers:
+            for key in ("wqkv", "wo", "w1", "w2"):
+                K, N = ly[key].shape
+                if K % 64 or N % 128:
+                    continue
+                wt = torch.empty((N // 128, 2, K, 64), dtype=self.dtype, device=self.device)
+                L.call("sd_tile_weight", L.ptr(ly[key]), K, N, L.ptr(wt), L.stream())
+                tm = ctypes.create_string_buffer(128)
+                L.call("sd_make_weight_tmap", L.ptr(wt), K, N, tm)
+                ly["wt_" + key], ly["tm_" + key] = wt, tm
+                need = max(need, L.load().sd_gemm_workspace_bytes(16, N, K))
+        self._gemm_ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
+
+    def dense(self, x: torch.Tensor, ly: dict, key: str, silu: bool = False) -> torch.Tensor:
+        """x @ ly[key] -> fp32 [T, N], or [S, T, N] split-K slices whose in-order
+        sum is the product (consumed by norm() / rope_stage()); silu=True gives
+        bf16 silu(x @ w) (the MLP up-projection)."""
+        tm = ly.get("tm_" + key)
+        T = x.shape[0]
+        if tm is None or T > 128 or not self.use_gemm or not x.is_contiguous():
+            y = self.mm(x, ly[key])
+            return self.silu(y) if silu else y
+        K, N = ly[key].shape
+        epi = L.GEMM_EPI_SILU_BF16 if silu else L.GEMM_EPI_F32
+        S = L.load().sd_gemm_splits(T, N, K, epi)
+        y = torch.empty((T, N) if silu else (S, T, N), dtype=self.dtype if silu else torch.float32,
+                        device=self.device)
+        L.call("sd_gemm", L.ptr(x), T, K, tm, N, epi, L.ptr(y), N, L.ptr(self._gemm_ws), self._gemm_ws.numel(),
+               L.stream())
+        return y
 
     def parameters_host(self) -> dict:
         """Weights back in the reference layout (fp64 numpy; shard-local)."""
@@ -315,15 +370,19 @@ class TinyTransformer:
     def rope_stage(self, qkv, T, positions_dev, q_rot, q_pre, k_raw, k_rot, v, head_stride, row_offset,
                    rows_dev=None):
         kd = L.dcode(self.dtype)
+        S, sstride = _splits(qkv)
         L.call("sd_rope_stage", L.ptr(qkv), T, self.H, self.Hk, self.dh, L.ptr(positions_dev),
                L.ptr(self.rope_cos), L.ptr(self.rope_sin), self.q_scale, L.ptr(q_rot), kd, L.ptr(q_pre),
-               L.ptr(k_raw), L.ptr(k_rot), L.ptr(v), kd, head_stride, row_offset, L.ptr(rows_dev), L.stream())
+               L.ptr(k_raw), L.ptr(k_rot), L.ptr(v), kd, head_stride, row_offset, L.ptr(rows_dev), S, sstride,
+               L.stream())
 
     def norm(self, h, delta, gain, out_dtype=None):
         T, d = h.shape
         dt = out_dtype or self.dtype
         x = torch.empty((T, d), dtype=dt, device=self.device)
-        L.call("sd_add_rmsnorm", L.ptr(h), L.ptr(delta), T, d, L.ptr(gain), 1e-6, L.ptr(x), L.dcode(dt), L.stream())
+        S, sstride = _splits(delta) if delta is not None else (1, 0)
+        L.call("sd_add_rmsnorm", L.ptr(h), L.ptr(delta), T, d, L.ptr(gain), 1e-6, L.ptr(x), L.dcode(dt), S, sstride,
+               L.stream())
         return x
 
     def embed_rows(self, tokens_dev, T):
@@ -345,13 +404,13 @@ class TinyTransformer:
         x = self.norm(h, None, self.layers[0]["ln1"])
         nl = len(self.layers)
         for l, ly in enumerate(self.layers):
-            qkv = self.mm(x, ly["wqkv"])
+            qkv = self.dense(x, ly, "wqkv")
             o = attend(l, qkv, None if q_pre is None else q_pre[l])
             o = self._gather_heads(o)
-            x = self.norm(h, self.mm(o, ly["wo"]), ly["ln2"])
-            a = self.silu(self.mm(x, ly["w1"]))
+            x = self.norm(h, self.dense(o, ly, "wo"), ly["ln2"])
+            a = self.dense(x, ly, "w1", silu=True)
             last = l + 1 == nl
-            x = self.norm(h, self.mm(a, ly["w2"]), self.ln_f if last else self.layers[l + 1]["ln1"],
+            x = self.norm(h, self.dense(a, ly, "w2"), self.ln_f if last else self.layers[l + 1]["ln1"],
                           out_dtype=torch.float32 if last else None)
         return x  # fp32 h0
 

@@ -591,3 +591,87 @@ def test_accept_commit_matches_oracle(lib):
         assert r[Lb.RES_YS:Lb.RES_YS + acc] == ys
         assert r[Lb.RES_KEEP:Lb.RES_KEEP + acc] == keep
         assert r[Lb.RES_PENDING] == ys[-1]
+
+
+@pytest.mark.parametrize("M", [1, 4, 41, 101, 128])
+@pytest.mark.parametrize("K,N", [(4096, 6144), (4096, 4096), (512, 16384), (16384, 4096), (1024, 128)])
+def test_gemm_stream_vs_fp32_reference(lib, M, K, N):
+    """Weight-streaming tcgen05 GEMM (model.py:283-285, 306-309) vs a torch fp32
+    reference on the same bf16 operands: fp32 split-K slices summed in order,
+    and fused SiLU -> bf16; deterministic (two calls bitwise equal)."""
+    import ctypes
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(M * 7 + N)
+    x = torch.randn((M, K), generator=g, device=dev).to(torch.bfloat16)
+    w = (torch.randn((K, N), generator=g, device=dev) * K ** -0.5).to(torch.bfloat16)
+    wt = torch.empty((N // 128, 2, K, 64), dtype=torch.bfloat16, device=dev)
+    lib.call("sd_tile_weight", lib.ptr(w), K, N, lib.ptr(wt), lib.stream())
+    assert torch.equal(wt, w.reshape(K, N // 128, 2, 64).permute(1, 2, 0, 3))
+    ws = torch.zeros(max(256, lib.load().sd_gemm_workspace_bytes(M, N, K)), dtype=torch.uint8, device=dev)
+    tm = ctypes.create_string_buffer(128)
+    lib.call("sd_make_weight_tmap", lib.ptr(wt), K, N, tm)
+    want = x.float() @ w.float()
+    S = lib.load().sd_gemm_splits(M, N, K, lib.GEMM_EPI_F32)
+    assert S >= 1
+    ys = []
+    for _ in range(2):
+        y = torch.full((S, M, N), float("nan"), dtype=torch.float32, device=dev)
+        lib.call("sd_gemm", lib.ptr(x), M, K, tm, N, lib.GEMM_EPI_F32, lib.ptr(y), N, None, 0, lib.stream())
+        acc = y[0].clone()
+        for s in range(1, S):
+            acc += y[s]
+        ys.append(acc)
+    torch.testing.assert_close(ys[0], want, rtol=1e-3, atol=1e-3)
+    assert torch.equal(ys[0], ys[1])
+    assert lib.load().sd_gemm_splits(M, N, K, lib.GEMM_EPI_SILU_BF16) == 1
+    ysil = torch.empty((M, N), dtype=torch.bfloat16, device=dev)
+    for _ in range(2):  # second call: the split-SiLU counters were left zeroed
+        lib.call("sd_gemm", lib.ptr(x), M, K, tm, N, lib.GEMM_EPI_SILU_BF16, lib.ptr(ysil), N, lib.ptr(ws), ws.numel(),
+                 lib.stream())
+        torch.testing.assert_close(ysil.float(), torch.nn.functional.silu(want), rtol=1e-2, atol=1e-2)
+
+
+@pytest.mark.parametrize("S", [1, 3])
+def test_norm_and_rope_sum_split_slices(lib, S):
+    """sd_add_rmsnorm / sd_rope_stage consume split-K slices: same result as
+    the pre-summed input (slices summed in order)."""
+    dev = torch.device("cuda")
+    T, d, H, Hk, dh = 5, 512, 8, 2, 64
+    g = torch.Generator(device=dev)
+    g.manual_seed(S)
+    h0 = torch.randn((T, d), generator=g, device=dev)
+    sl = torch.randn((S, T, d), generator=g, device=dev)
+    gain = torch.rand(d, generator=g, device=dev) + 0.5
+    tot = sl[0].clone()
+    for s in range(1, S):
+        tot += sl[s]
+    outs = []
+    for delta, splits, stride in ((tot, 1, 0), (sl, S, T * d)):
+        h = h0.clone()
+        x = torch.empty((T, d), dtype=torch.bfloat16, device=dev)
+        lib.call("sd_add_rmsnorm", lib.ptr(h), lib.ptr(delta), T, d, lib.ptr(gain), 1e-6, lib.ptr(x), 1, splits,
+                 stride, lib.stream())
+        outs.append((h, x))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+    W = (H + 2 * Hk) * dh
+    q = torch.randn((S, T, W), generator=g, device=dev)
+    qt = q[0].clone()
+    for s in range(1, S):
+        qt += q[s]
+    pos = torch.arange(T, dtype=torch.int32, device=dev) + 7
+    inv = 10000.0 ** (-np.arange(0, dh, 2) / dh)
+    ang = np.arange(64)[:, None] * inv[None]
+    cs = torch.as_tensor(np.cos(ang), dtype=torch.float32, device=dev)
+    sn = torch.as_tensor(np.sin(ang), dtype=torch.float32, device=dev)
+    res = []
+    for src, splits, stride in ((qt, 1, 0), (q, S, T * W)):
+        q_rot = torch.empty((T, H, dh), dtype=torch.bfloat16, device=dev)
+        kr = torch.zeros((Hk, 32, dh), dtype=torch.bfloat16, device=dev)
+        kro, vv = torch.zeros_like(kr), torch.zeros_like(kr)
+        lib.call("sd_rope_stage", lib.ptr(src), T, H, Hk, dh, lib.ptr(pos), lib.ptr(cs), lib.ptr(sn), 0.125,
+                 lib.ptr(q_rot), 1, None, lib.ptr(kr), lib.ptr(kro), lib.ptr(vv), 1, 32 * dh, 3, None, splits, stride,
+                 lib.stream())
+        res.append((q_rot, kr, kro, vv))
+    for a, b in zip(res[0], res[1]):
+        assert torch.equal(a, b)

@@ -50,7 +50,7 @@ t = tr.cpu().numpy()
 base = t[t > 0].min()
 print("cta(0,0,0) milestones [entry, q staged, tmem+sync, softmax loop done, o_final, epilogue done, exit]:",
       [int(x - base) if x else None for x in t[0, 60, :7]])
-names = {0: ["k_empty?", "k_empty ok", "v_empty ok"], 1: ["qk wait", "k_full ok", "qk issued", "v wait", "p0 ok", "p1 ok", "pv issued"],
+names = {0: ["-", "K issued", "V issued"], 1: ["qk wait", "k_full ok", "qk issued", "v wait", "p ok", "-", "pv issued"],
          2: ["s wait", "s ok", "exp done", "rescaled", "p arrive"], 3: ["s wait", "s ok", "exp done", "rescaled", "p arrive"]}
 for j in list(range(0, 6)) + list(range(20, 24)):
     row = []
