@@ -102,6 +102,9 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
  * captured once in a CUDA graph and replayed as the cache grows.
  * CUDA-core split boundaries depend on ctx only (bitwise identical across GPU
  * counts); the tensor-core path splits by SM count. */
+/* The workspace starts with SD_ATTN_WS_HEAD bytes of arrival counters: zero
+ * them once when the workspace is allocated; every call leaves them zero. */
+#define SD_ATTN_WS_HEAD 4096
 size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx);
 int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
                  int src_kind, const void* k_cache, const void* v_cache, int kv_dtype, int64_t head_stride,

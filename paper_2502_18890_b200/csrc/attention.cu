@@ -413,6 +413,77 @@ __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* _
   }
 }
 
+template <typename T> __device__ __forceinline__ void store4(T* p, float a, float b, float c, float d);
+template <> __device__ __forceinline__ void store4<float>(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+template <> __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float a, float b, float c, float d) {
+  const __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 v;
+  v.x = *reinterpret_cast<const uint32_t*>(&lo);
+  v.y = *reinterpret_cast<const uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(p) = v;
+}
+
+// head_dim 128: one warp per (t, head) row, lane = 4 dims. Split weights
+// exp(lse_c - max) are recomputed per lane from a broadcast lse load, so every
+// split's partial is an independent float4 load (all in flight) and the merge is
+// a single L2 round trip; splits are accumulated in ascending order.
+template <typename OT>
+__global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+                                                       int nsplit, int TH, int H, const int32_t* __restrict__ rows_dev,
+                                                       OT* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);  // t * H + head
+  if (row >= TH) return;
+  OT* dst = out + (int64_t)row * 128 + 4 * lane;
+  if (rows_dev && row / H >= *rows_dev) {  // padded row: defined zeros
+    store4<OT>(dst, 0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  // lse of split c lives in lane c % 32, register c / 32 (nsplit <= 96)
+  float lv[3], wv[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int c = lane + 32 * k;
+    lv[k] = c < nsplit ? ws_lse[(int64_t)c * TH + row] : -INFINITY;
+  }
+  const float m = warp_max(fmaxf(lv[0], fmaxf(lv[1], lv[2])));
+  float lsum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    wv[k] = lv[k] == -INFINITY ? 0.f : __expf(lv[k] - m);
+    lsum += wv[k];
+  }
+  lsum = warp_sum(lsum);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* base = ws_o + (int64_t)row * 128 + 4 * lane;
+#pragma unroll 8
+  for (int c = 0; c < nsplit; ++c) {
+    const float w = __shfl_sync(0xffffffffu, c < 32 ? wv[0] : (c < 64 ? wv[1] : wv[2]), c & 31);
+    // unconditional load (all in flight); empty splits (never written: past a
+    // device-resident context) carry weight 0 and are dropped by the select
+    const float4 o = *reinterpret_cast<const float4*>(base + (int64_t)c * TH * 128);
+    if (w != 0.f) {
+      acc.x = fmaf(w, o.x, acc.x);
+      acc.y = fmaf(w, o.y, acc.y);
+      acc.z = fmaf(w, o.z, acc.z);
+      acc.w = fmaf(w, o.w, acc.w);
+    }
+  }
+  const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+  store4<OT>(dst, acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+}
+
+template <typename OT>
+static void launch_merge(const float* ws_o, const float* ws_lse, int nsplit, int TH, int H, const int32_t* rows_dev,
+                         OT* out, int dh, cudaStream_t st) {
+  if (dh == 128 && nsplit <= 96)
+    merge128_kernel<OT><<<(TH + 7) / 8, 256, 0, st>>>(ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
+  else
+    attn_merge_kernel<128, OT><<<TH, 128, 0, st>>>(ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
+}
+
 template <int DH, typename QT, typename KT, typename OT>
 static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaStream_t st, bool tree_only) {
   AttnParams p = p0;
@@ -433,8 +504,11 @@ static int launch_attention(const AttnParams& p0, int src_kind, void* out, cudaS
   }
   int rc = check_launch("sd_attention(partial)");
   if (rc) return rc;
-  attn_merge_kernel<DH, OT><<<p.T * p.H, DH >= 128 ? 128 : (DH < 32 ? 32 : DH), 0, st>>>(
-      p.ws_o, p.ws_lse, p.n_chunks + 1, p.T * p.H, p.H, p.rows_dev, (OT*)out);
+  if (DH == 128)
+    launch_merge<OT>(p.ws_o, p.ws_lse, p.n_chunks + 1, p.T * p.H, p.H, p.rows_dev, (OT*)out, DH, st);
+  else
+    attn_merge_kernel<DH, OT><<<p.T * p.H, DH >= 128 ? 128 : (DH < 32 ? 32 : DH), 0, st>>>(
+        p.ws_o, p.ws_lse, p.n_chunks + 1, p.T * p.H, p.H, p.rows_dev, (OT*)out);
   return check_launch("sd_attention(merge)");
 }
 
@@ -644,8 +718,7 @@ static int launch_decode(AttnParams p, int src_kind, void* out, cudaStream_t st)
   }
   int rc = check_launch("sd_attention(decode)");
   if (rc) return rc;
-  attn_merge_kernel<DH, OT><<<p.H, DH >= 128 ? 128 : DH, 0, st>>>(p.ws_o, p.ws_lse, p.n_chunks + 1, p.H, p.H,
-                                                                   p.rows_dev, (OT*)out);
+  launch_merge<OT>(p.ws_o, p.ws_lse, p.n_chunks + 1, p.H, p.H, p.rows_dev, (OT*)out, DH, st);
   return check_launch("sd_attention(decode merge)");
 }
 
@@ -659,6 +732,182 @@ static int dispatch_decode(const AttnParams& p, int q_dtype, int kv_dtype, int o
     return launch_decode<DH, float, float, float>(p, src_kind, out, st);
   set_error("sd_attention(decode): unsupported dtype combination");
   return SD_EUNSUPPORTED;
+}
+
+// ------------------------------------------------------------------------
+// Draft attention over the partial cache (model.py:301-305, kvcache.py:158-165):
+// one query row, G <= 8 query heads per kv head, K_raw rotated on load at the
+// slot's rank, holes (rank < 0) skipped, the pending token's own row (k_tree /
+// v_tree) attended by the last chunk. Grid (chunks of DR_CHUNK slots, kv head),
+// 8 warps x 16 keys per CTA so every SM holds ~2 CTAs with all key loads of a
+// warp in flight. Chunk partials are merged by the LAST CTA of each kv head to
+// finish (arrival counter in the zeroed workspace head, reset after use), in
+// fixed chunk order — one launch, deterministic, no separate merge kernel.
+constexpr int DR_WARPS = 8, DR_CHUNK = DR_WARPS * 16, DR_MAX_CHUNKS = 96;
+
+template <typename KT, int GM>
+__global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* __restrict__ counters,
+                                                            __nv_bfloat16* __restrict__ out) {
+  using V4 = typename Vec4<KT>::T;
+  constexpr int DH = 128, NB = 8;
+  __shared__ float Sm[DR_WARPS][GM], Sl[DR_WARPS][GM], So[DR_WARPS][GM][DH];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kvh = blockIdx.y, G = p.G, nc = gridDim.x, cx = blockIdx.x;
+  const KT* K = (const KT*)p.k_cache + kvh * p.head_stride;
+  const KT* V = (const KT*)p.v_cache + kvh * p.head_stride;
+  const int w0 = cx * DR_CHUNK + warp * 16, w1 = min(p.ctx, w0 + 16);
+  int my_rank = -1;
+  if (lane < 16 && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
+  float q[GM][4];
+#pragma unroll
+  for (int g = 0; g < GM; ++g) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) q[g][e] = 0.f;
+    if (g < G) {
+      const KT* qp = (const KT*)p.q + (int64_t)(kvh * G + g) * DH + lane * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) q[g][e] = to_f(qp[e]);
+    }
+  }
+  float m[GM], l[GM], acc[GM][4];
+#pragma unroll
+  for (int g = 0; g < GM; ++g) {
+    m[g] = -INFINITY;
+    l[g] = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[g][e] = 0.f;
+  }
+  auto update = [&](const float* kf, const float* vf) {
+    float sg[GM];
+#pragma unroll
+    for (int g = 0; g < GM; ++g) sg[g] = fmaf(q[g][0], kf[0], fmaf(q[g][1], kf[1], fmaf(q[g][2], kf[2], q[g][3] * kf[3])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int g = 0; g < GM; ++g) sg[g] += __shfl_xor_sync(0xffffffffu, sg[g], o);
+#pragma unroll
+    for (int g = 0; g < GM; ++g) {
+      if (g < G) {
+        const float mn = fmaxf(m[g], sg[g]);
+        const float corr = __expf(m[g] - mn), pw = __expf(sg[g] - mn);
+        l[g] = l[g] * corr + pw;
+        m[g] = mn;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[g][e] = fmaf(acc[g][e], corr, pw * vf[e]);
+      }
+    }
+  };
+  // two batches of 8 keys: every load of a batch issued before any math
+#pragma unroll
+  for (int b0 = 0; b0 < 16; b0 += NB) {
+    V4 kv[NB], vv[NB];
+    float2 cs[NB][2];
+    bool ok[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = w0 + b0 + b;
+      const int rk = __shfl_sync(0xffffffffu, my_rank, b0 + b);
+      ok[b] = k < w1 && rk >= 0;
+      const int kk = ok[b] ? k : 0;  // in-bounds address for masked keys
+      kv[b] = *reinterpret_cast<const V4*>(K + (int64_t)kk * DH + lane * 4);
+      vv[b] = *reinterpret_cast<const V4*>(V + (int64_t)kk * DH + lane * 4);
+      const int64_t r = rk > 0 ? rk : 0;
+      cs[b][0] = *reinterpret_cast<const float2*>(p.cosT + r * (DH / 2) + lane * 2);
+      cs[b][1] = *reinterpret_cast<const float2*>(p.sinT + r * (DH / 2) + lane * 2);
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      if (!ok[b]) continue;  // warp-uniform
+      float kf[4], vf[4];
+      Vec4<KT>::unpack(kv[b], kf);
+      Vec4<KT>::unpack(vv[b], vf);
+      const float a0 = kf[0], c0 = kf[1], a1 = kf[2], c1 = kf[3];  // pairs (0,1), (2,3) of this lane
+      kf[0] = a0 * cs[b][0].x - c0 * cs[b][1].x;
+      kf[1] = a0 * cs[b][1].x + c0 * cs[b][0].x;
+      kf[2] = a1 * cs[b][0].y - c1 * cs[b][1].y;
+      kf[3] = a1 * cs[b][1].y + c1 * cs[b][0].y;
+      update(kf, vf);
+    }
+  }
+  if (cx == nc - 1 && warp == DR_WARPS - 1) {  // the pending token's own row (always visible)
+    const KT* Kt = (const KT*)p.k_tree + kvh * p.tree_head_stride;
+    const KT* Vt = (const KT*)p.v_tree + kvh * p.tree_head_stride;
+    float kf[4], vf[4];
+    Vec4<KT>::unpack(*reinterpret_cast<const V4*>(Kt + lane * 4), kf);
+    Vec4<KT>::unpack(*reinterpret_cast<const V4*>(Vt + lane * 4), vf);
+    update(kf, vf);
+  }
+  // ---- CTA combine of the 8 warps' states -> chunk partial ----
+#pragma unroll
+  for (int g = 0; g < GM; ++g) {
+    if (g < G) {
+      if (lane == 0) {
+        Sm[warp][g] = m[g];
+        Sl[warp][g] = l[g];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) So[warp][g][lane * 4 + e] = acc[g][e];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * DH; i += 256) {
+    const int g = i / DH, d = i - g * DH;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < DR_WARPS; ++w) M = fmaxf(M, Sm[w][g]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < DR_WARPS; ++w) {
+        const float sc = __expf(Sm[w][g] - M);
+        L += Sl[w][g] * sc;
+        O += So[w][g][d] * sc;
+      }
+    }
+    const int64_t oi = (int64_t)cx * p.H + kvh * G + g;
+    p.ws_o[oi * DH + d] = L > 0.f ? O / L : 0.f;
+    if (d == 0) p.ws_lse[oi] = L > 0.f ? M + __logf(L) : -INFINITY;
+  }
+  // ---- the last CTA of this kv head merges the chunks in order ----
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&counters[kvh], 1) == nc - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (warp < G) {
+    const int row = kvh * G + warp;  // T == 1: row = head
+    float lv[3], wv[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const int c = lane + 32 * k;
+      lv[k] = c < nc ? __ldcg(p.ws_lse + (int64_t)c * p.H + row) : -INFINITY;
+    }
+    const float M = warp_max(fmaxf(lv[0], fmaxf(lv[1], lv[2])));
+    float L = 0.f;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      wv[k] = lv[k] == -INFINITY ? 0.f : __expf(lv[k] - M);
+      L += wv[k];
+    }
+    L = warp_sum(L);
+    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+    for (int c = 0; c < nc; ++c) {
+      const float w = __shfl_sync(0xffffffffu, c < 32 ? wv[0] : (c < 64 ? wv[1] : wv[2]), c & 31);
+      const float4 o = __ldcg(reinterpret_cast<const float4*>(p.ws_o + ((int64_t)c * p.H + row) * DH) + lane);
+      if (w != 0.f) {
+        o4.x = fmaf(w, o.x, o4.x);
+        o4.y = fmaf(w, o.y, o4.y);
+        o4.z = fmaf(w, o.z, o4.z);
+        o4.w = fmaf(w, o.w, o4.w);
+      }
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    store4<__nv_bfloat16>(out + (int64_t)row * DH + lane * 4, o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
+  }
+  if (tid == 0) counters[kvh] = 0;  // ready for the next launch / graph replay
 }
 
 int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
@@ -692,7 +941,7 @@ size_t sd_attention_workspace_bytes(int T, int H, int dh, int ctx) {
     const int dc = (ctx + dec_chunk_for(ctx) - 1) / dec_chunk_for(ctx);
     if (dc > nc) nc = dc;
   }
-  return ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
+  return SD_ATTN_WS_HEAD + ((size_t)nc + 1) * (size_t)T * H * (dh + 1) * sizeof(float);
 }
 
 int sd_debug_tc_trace(void* trace_dev, int force_chunks) { return tc_set_trace(trace_dev, force_chunks); }
@@ -737,7 +986,8 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   p.mask_words = mask_words;
   p.chunk = chunk_len_for(ctx);
   p.n_chunks = n_chunks_for(ctx);
-  p.ws_o = (float*)workspace;
+  int* counters = (int*)workspace;  // SD_ATTN_WS_HEAD bytes, zero between calls
+  p.ws_o = (float*)((char*)workspace + SD_ATTN_WS_HEAD);
   p.ws_lse = p.ws_o + (size_t)(p.n_chunks + 1) * T * H * dh;
   p.rows_dev = rows_dev;
   p.ctx_dev = ctx_dev;
@@ -756,9 +1006,21 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, ctx_dev, mask_bits,
                               mask_words, p.ws_o, ws_lse, nc, chunk, st);
     if (rc) return rc;
-    attn_merge_kernel<128, __nv_bfloat16><<<T * H, 128, 0, st>>>(p.ws_o, ws_lse, nc, T * H, H, rows_dev,
-                                                                  (__nv_bfloat16*)out);
+    launch_merge<__nv_bfloat16>(p.ws_o, ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out, 128, st);
     return check_launch("sd_attention(tc merge)");
+  }
+  if (T == 1 && src_kind == 1 && dh == 128 && p.G <= 8 && !rows_dev && q_dtype == kv_dtype &&
+      out_dtype == SD_BF16 && kv_dtype == SD_BF16 && (ctx + DR_CHUNK - 1) / DR_CHUNK <= DR_MAX_CHUNKS &&
+      Hk * sizeof(int) <= SD_ATTN_WS_HEAD) {
+    // draft attention: rank-rotated partial cache, merge fused (last CTA per kv head)
+    const int nc = ctx > 0 ? (ctx + DR_CHUNK - 1) / DR_CHUNK : 1;
+    p.ws_lse = p.ws_o + (size_t)nc * H * dh;
+    dim3 grid(nc, Hk);
+    if (p.G <= 4)
+      draft_attn_kernel<__nv_bfloat16, 4><<<grid, 256, 0, st>>>(p, counters, (__nv_bfloat16*)out);
+    else
+      draft_attn_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(p, counters, (__nv_bfloat16*)out);
+    return check_launch("sd_attention(draft)");
   }
   if (T == 1 && p.G <= 8 && dh == 128 && !rows_dev && !ctx_dev) {
     // single-row decode (draft / AR): latency-tolerant streaming kernel

@@ -430,25 +430,38 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (role < 4) trace(role, j, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
+      // Every MMA of the CTA has retired once both M-tiles' o_final fired, so the
+      // K/V rings are free: each warp stages its 32 rows x 512 B there (16-byte
+      // chunks XOR-swizzled by row: conflict-free both ways) and writes them out
+      // one contiguous row per instruction instead of 32 rows x 16 B.
       if (row == 0 && mt == 0) trace(0, 60, 3);
-      mbar_wait(&o_final[mt], 0);
+      for (int m2 = 0; m2 < nm; ++m2) mbar_wait(&o_final[m2], 0);
       if (row == 0 && mt == 0) trace(0, 60, 4);
       tc_fence_after();
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
       const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint8_t* stage = smem + OFF_K + (warp - 4) * (32 * DH * 4);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         uint32_t o[32];
         tmem_ld32(tmem + lane_base + COL_O + 128 * mt + 32 * q4, o);
         tmem_wait_ld();
-        if (valid) {
-          float4* dst = reinterpret_cast<float4*>(p.ws_o + oi * DH + 32 * q4);
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            dst[c] = make_float4(__uint_as_float(o[4 * c]) * inv, __uint_as_float(o[4 * c + 1]) * inv,
-                                 __uint_as_float(o[4 * c + 2]) * inv, __uint_as_float(o[4 * c + 3]) * inv);
+        for (int c = 0; c < 8; ++c) {
+          const int chunk = 8 * q4 + c;  // 16-byte chunk of this row
+          *reinterpret_cast<float4*>(stage + lane * 512 + ((chunk ^ lane) << 4)) =
+              make_float4(__uint_as_float(o[4 * c]) * inv, __uint_as_float(o[4 * c + 1]) * inv,
+                          __uint_as_float(o[4 * c + 2]) * inv, __uint_as_float(o[4 * c + 3]) * inv);
         }
+      }
+      __syncwarp();
+      for (int rr = 0; rr < 32; ++rr) {
+        const int64_t oi_r = __shfl_sync(0xffffffffu, oi, rr);
+        const bool v_r = __shfl_sync(0xffffffffu, valid, rr);
+        if (v_r)
+          reinterpret_cast<float4*>(p.ws_o + oi_r * DH)[lane] =
+              *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
       }
       if (valid) p.ws_lse[oi] = l > 0.f ? (m_used + __log2f(l)) / LOG2E : -INFINITY;
       if (row == 0 && mt == 0) trace(0, 60, 5);

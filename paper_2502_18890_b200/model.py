@@ -341,8 +341,8 @@ class TinyTransformer:
         return torch.mm(a, b)
 
     def workspace(self, nbytes: int) -> torch.Tensor:
-        if self._ws.numel() < nbytes:
-            self._ws = torch.empty(int(nbytes * 1.25) + 1024, dtype=torch.uint8, device=self.device)
+        if self._ws.numel() < nbytes:  # zeroed: sd_attention keeps arrival counters in its head
+            self._ws = torch.zeros(int(nbytes * 1.25) + 1024, dtype=torch.uint8, device=self.device)
         return self._ws
 
     def _gather_heads(self, o: torch.Tensor) -> torch.Tensor:

@@ -71,7 +71,7 @@ def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
     vt = torch.as_tensor(Vv, dtype=dtype, device=dev).contiguous()
     qt = torch.as_tensor(q, dtype=dtype, device=dev).contiguous()
     out = torch.empty((T, H * dh), dtype=dtype, device=dev)
-    ws = torch.empty(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, T, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, lib.ptr(bits), lib.MASK_WORDS,
@@ -116,7 +116,7 @@ def test_verify_attention_tcgen05(lib, ctx, T, H, Hk, layer):
     outs = []
     for tm in (F.tmaps, (None, None)):
         out = torch.empty((T, H * dh), dtype=torch.bfloat16, device=dev)
-        ws = torch.empty(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
                  F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
                  F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, tm[0], tm[1],
@@ -161,6 +161,7 @@ def test_attention_ctx_dev_matches_host_ctx(lib, tc, ctx):
     ctx_dev = torch.tensor([ctx], dtype=torch.int32, device=dev)
     upper = cap - T
     ws = torch.full((lib.load().sd_attention_workspace_bytes(T, H, dh, upper),), 255, dtype=torch.uint8, device=dev)
+    ws[:4096] = 0  # SD_ATTN_WS_HEAD: the counter head is zero between calls; the rest is stale
     outs = []
     for mode in ("host", "dev"):
         out = torch.empty((T, H * dh), dtype=torch.bfloat16, device=dev)
@@ -200,7 +201,7 @@ def test_attention_rows_dev_padding(lib):
     for rd in (rows, None):
         TT = T if rd is not None else Tl
         out = torch.full((TT, H * dh), 7.0, dtype=torch.float32, device=dev)
-        ws = torch.empty(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
+        ws = torch.zeros(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 0, TT, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), 0, cap * dh, ctx, None,
                  None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, lib.ptr(rd),
                  None, None, None, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
@@ -262,7 +263,7 @@ def test_decode_attention_full_cache(lib, dtype, ctx):
     vt = torch.as_tensor(g.normal(size=(Hk, cap, dh)), dtype=dtype, device=dev)
     qt = torch.as_tensor(g.normal(size=(1, H, dh)) * 2 / np.sqrt(dh), dtype=dtype, device=dev)
     out = torch.empty((1, H * dh), dtype=dtype, device=dev)
-    ws = torch.empty(lib.load().sd_attention_workspace_bytes(1, H, dh, ctx), dtype=torch.uint8, device=dev)
+    ws = torch.zeros(lib.load().sd_attention_workspace_bytes(1, H, dh, ctx), dtype=torch.uint8, device=dev)
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, 1, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, None, None, None, None, 0,

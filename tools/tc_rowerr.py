@@ -16,7 +16,7 @@ q = torch.as_tensor(g.normal(size=(T, H, dh)) * 2 / np.sqrt(dh), dtype=torch.bfl
 mask = np.tril(np.ones((T, T), dtype=bool))
 bits = torch.as_tensor(mask_bits_from_bool(mask), device="cuda")
 out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
-ws = torch.empty(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
 L.call("sd_debug_tc_trace", None, force)
 L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
        None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),

@@ -22,7 +22,7 @@ F.v.normal_()
 q = (torch.randn((T, H, dh), device="cuda") * 0.1).to(torch.bfloat16)
 bits = torch.as_tensor(mask_bits_from_bool(np.tril(np.ones((T, T), dtype=bool))), device="cuda")
 out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
-ws = torch.empty(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
 tr = torch.zeros((4, 64, 8), dtype=torch.int64, device="cuda")
 
 

@@ -9,7 +9,7 @@ for (ctx, T, Hk) in [(54096, 41, 8), (54096, 20, 8), (54096, 101, 8), (4096, 41,
     q = (torch.randn((T, H, dh), device="cuda") * 0.1).to(torch.bfloat16)
     bits = torch.as_tensor(mask_bits_from_bool(np.tril(np.ones((T, T), dtype=bool))), device="cuda")
     out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
-    ws = torch.empty(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
     def run():
         L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
                None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
