@@ -7,21 +7,22 @@
 //
 // One CTA = (key chunk, kv head, 256-row group), 12 warps; the last chunk
 // also covers the T staged tree rows (keys ctx..ctx+T-1) under the tree mask.
-//   warp 0      TMA producer: K and V tiles of 64 keys x 128 dh (two 128-byte
-//               swizzled boxes each) into separate 3-deep rings (mbarrier
-//               tx-count);
-//   warp 1      MMA issuer (one thread): S[mt][j%2] = Q K(j)^T (M=128, N=64,
-//               SS) and O[mt] += P(j) V(j) (M=128, N=128, A = P from shared
-//               memory, B = V MN-major straight from the TMA layout);
-//   warp 2      TMEM allocator (512 columns: O 2x128, S 2x2x64);
-//   warps 4-11  two softmax warpgroups, one per 128-row M-tile: thread = row =
-//               TMEM lane; online softmax in base 2 with lazy rescale (O is
-//               rescaled in TMEM only when the row max grows by > 2^8).
-// P goes to shared memory (SW128 K-major, the layout the MMA reads), not back
-// into TMEM over S: the S buffer is released (s_free) as soon as the softmax
-// has loaded it, so QK(j+2) is issued while the softmax of tile j is still
-// computing, and the issuer never waits for an MMA to retire. The tensor pipe
-// therefore runs QK(j+1) / QK(j+2) / PV(j) back to back under the softmax.
+//   warps 0, 3  TMA producers for K and V: separate 5-deep rings of 64-key x
+//               128-dh tiles (two 128-byte swizzled boxes each), started before
+//               Q is staged;
+//   warps 1, 2  one MMA-issuer thread per 128-row M-tile: S[mt][j%2] = Q K(j)^T
+//               (M=128, N=64, SS) and O[mt] += P(j) V(j) (M=128, N=128, A = P
+//               from TMEM, B = V MN-major straight from the TMA layout);
+//   warps 4-11  two softmax warpgroups, one per M-tile: thread = row = TMEM lane;
+//               online softmax in base 2 with lazy rescale (O is rescaled in TMEM
+//               only when the row max grows by > 2^8); P (bf16x2) is written back
+//               over the first 32 columns of the S buffer it came from.
+// S(j+2) reuses buffer j%2, whose P(j) is still an operand of O += P(j) V(j).
+// Both MMAs come from the same issuer thread with the PV first, and tcgen05.mma
+// instructions of one thread execute in issue order (the pipelined-pair rule of
+// the tcgen05 memory model), so the write-after-read on TMEM needs no barrier:
+// the issuer never waits for an MMA to retire, and a tile costs it three
+// barrier waits (K landed, V landed, P written) and four commits.
 #include "tc_common.cuh"
 
 namespace sd {
@@ -30,7 +31,7 @@ namespace tc {
 constexpr int BN = 64;          // keys per tile
 constexpr int DH = 128;
 #ifndef SD_TC_ST
-#define SD_TC_ST 4
+#define SD_TC_ST 5
 #endif
 constexpr int ST = SD_TC_ST;    // K ring depth == V ring depth
 constexpr int THREADS = 384;
@@ -40,19 +41,17 @@ constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 
 constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
 constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [dh half][64 rows][128 B]
-constexpr int P_TILE = 128 * BN * 2;            // 16 KB: [128 rows][64 keys * 2 B] SW128 K-major
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + Q_BYTES;
 constexpr int OFF_V = OFF_K + ST * KV_TILE;
-constexpr int OFF_P = OFF_V + ST * KV_TILE;     // [mt]: one P buffer per M-tile (P(j) is written
-                                                // after PV(j-1) retired, which it has by then)
-constexpr int OFF_BAR = OFF_P + 2 * P_TILE;
-constexpr int N_BAR = 4 * ST + 4 * 4 + 2;
+constexpr int OFF_BAR = OFF_V + ST * KV_TILE;
+constexpr int N_BAR = 4 * ST + 3 * 4 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
 // TMEM columns (512): O[mt] fp32 128 each; S[mt][buf] fp32 64 each (double
-// buffered).
+// buffered); P[mt][buf] (bf16x2, the TMEM A operand of O += P V) overwrites the
+// first 32 columns of the S buffer it was computed from.
 constexpr uint32_t COL_O = 0;
 constexpr uint32_t COL_S = 256;
 constexpr uint32_t TMEM_COLS = 512;
@@ -103,9 +102,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* k_empty = bars + 2 * ST;
   uint64_t* v_empty = bars + 3 * ST;
   uint64_t* s_full = bars + 4 * ST;      // [mt][buf]: QK retired -> softmax
-  uint64_t* s_free = s_full + 4;         // [mt][buf]: softmax has loaded S -> QK(j+2) may overwrite it
-  uint64_t* p_full = s_free + 4;         // [mt][buf]: P(j) in shared memory -> PV(j)
-  uint64_t* pv_done = p_full + 4;        // [mt][buf]: PV(j) retired -> P buffer free, O stable
+  uint64_t* p_full = s_full + 4;         // [mt][buf]: P(j) in TMEM -> PV(j), then QK(j+2)
+  uint64_t* pv_done = p_full + 4;        // [mt][buf]: PV(j) retired -> O stable (lazy rescale)
   uint64_t* o_final = pv_done + 4;       // [mt]: single phase, after the last PV
   uint32_t* tmem_slot = (uint32_t*)(o_final + 2);
 
@@ -158,7 +156,6 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t arrivals = 32 * (act[mt] > 0 ? act[mt] : 1);
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full[2 * mt + b], 1);
-        mbar_init(&s_free[2 * mt + b], arrivals);
         mbar_init(&p_full[2 * mt + b], arrivals);
         mbar_init(&pv_done[2 * mt + b], 1);
       }
@@ -269,32 +266,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST, b = j & 1;
-        // S(j+2) into buffer b as soon as the softmax has read S(j) out of it
-        if (j + 2 < n_tiles) {
-          wait_k(j + 2);
-          mbar_wait(&s_free[2 * mt + b], (j >> 1) & 1);
-          tc_fence_after();
-          issue_qk(j + 2);
-        }
         if (mt == 0) trace(1, j, 3);
         mbar_wait(&v_full[s], (j / ST) & 1);
         const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
-        const uint32_t p_base = smem_u32(smem + OFF_P + mt * P_TILE);
         mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
         if (mt == 0) trace(1, j, 4);
         tc_fence_after();
+        const uint32_t p_tmem = tmem + COL_S + 128 * mt + 64 * b;  // P(j) over S(j)'s first 32 columns
 #pragma unroll
         for (int ks = 0; ks < BN / 16; ++ks) {
           // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
           const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-          const uint64_t ad = umma_desc(p_base + ks * 32, 16, 1024);
           if (SD_TC_EXPERIMENT != 2 && SD_TC_EXPERIMENT != 4)
-            umma_bf16(o_col, ad, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
+            umma_bf16_ts(o_col, p_tmem + 8 * ks, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[2 * mt + b]);
         if (j == n_tiles - 1) umma_commit(&o_final[mt]);
         umma_commit(&v_empty[s]);
         if (mt == 0) trace(1, j, 6);
+        // S(j+2) into buffer b: issued after PV(j) by this thread, so it is
+        // ordered after PV(j)'s reads of P(j) (same-thread tcgen05.mma order)
+        if (j + 2 < n_tiles) {
+          wait_k(j + 2);
+          issue_qk(j + 2);
+        }
       }
     }
   } else if (warp >= 4) {
@@ -334,10 +329,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld32(s_addr, sr);
         tmem_ld32(s_addr + 32, sr + 32);
         tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(&s_free[2 * mt + b]);  // S(j) is in registers: QK(j+2) may reuse the buffer
         if (SD_TC_EXPERIMENT == 1 || SD_TC_EXPERIMENT == 4) {
-          if (j >= 1) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          tc_fence_before();
           mbar_arrive(&p_full[2 * mt + b]);
           l += __uint_as_float(sr[lane]);
           continue;
@@ -397,11 +390,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
         if (role < 4) trace(role, j, 2);
-        bool rescale_waited = false;
         if (__any_sync(0xffffffffu, rescale)) {
           // O must be stable: wait for every earlier O += P V of this M-tile (PV(j-1) retires last)
           if (j > 0) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-          rescale_waited = true;
           tc_fence_after();
 #pragma unroll
           for (int q4 = 0; q4 < 4; ++q4) {
@@ -416,15 +407,8 @@ __global__ void __launch_bounds__(THREADS, 1)
           tmem_wait_st();
         }
         if (role < 4) trace(role, j, 3);
-        // P(j) -> the M-tile's P buffer, free once PV(j-1) has retired (the
-        // rescale above may already have waited for it)
-        if (j >= 1 && !rescale_waited) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-        uint8_t* prow = smem + OFF_P + mt * P_TILE;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(prow + sw128(row, c)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        fence_async_smem();  // generic-proxy stores -> visible to the tensor pipe
+        tmem_st32(s_addr, pk);  // P(j) (bf16x2) over the consumed S columns
+        tmem_wait_st();
         tc_fence_before();
         mbar_arrive(&p_full[2 * mt + b]);
         if (role < 4) trace(role, j, 4);
