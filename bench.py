@@ -77,7 +77,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
@@ -117,6 +117,15 @@ def measured_peaks():
         d = json.load(open(p))
         return float(d["hbm_gbs"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), "measured"
     return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic():
+    """dram__bytes_read + dram__bytes_write per launch of the verification kernel
+    from the committed ncu --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_verify_traffic.json")
+    if not os.path.exists(p):
+        return None
+    return json.load(open(p)).get("traffic_bytes_per_launch")
 
 
 def cpu_baseline_line(c, ctx, accepted, tree_rows):
@@ -242,7 +251,7 @@ def main():
         "roofline": {"bound": bound, "achieved": achieved if bound == "hbm" else alg_flops / attn["avg_s"] / 1e12,
                      "peak": hbm if bound == "hbm" else tflops, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
                      "frac": (achieved / hbm) if bound == "hbm" else (alg_flops / attn["avg_s"] / 1e12) / tflops,
-                     "traffic": None, "kernel": "sd_attention verify (split-KV + merge), one layer",
+                     "traffic": ncu_traffic(), "kernel": "sd_attention verify (tcgen05 split-KV + merge), one layer",
                      "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes, "alg_flops_per_launch": alg_flops,
                      "avg_launch_us": attn["avg_s"] * 1e6, "rows": rows,
                      "share_of_step": attn["avg_s"] * model.config.num_layers / (dev_s / args.steps)},
