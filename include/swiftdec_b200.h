@@ -145,6 +145,17 @@ size_t sd_gemm_workspace_bytes(int M, int N, int K);
 int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi, void* y, int64_t ldy,
             void* workspace, size_t workspace_bytes, sd_stream_t stream);
 
+/* ---- single-row weight streaming (the draft forward's projections and draft
+ * heads, model.py:104-120, 283-285, 306-309) ----
+ * y[N] = x[K] . W[K][N]; x, W bf16 (W row-major, the reference layout), fp32
+ * accumulate; epi SD_GEMM_EPI_F32 -> fp32 y, SD_GEMM_EPI_SILU_BF16 -> bf16 silu.
+ * N % 8 == 0. K is split across CTAs and reduced in slice order by the last
+ * CTA of each column block through `workspace` (sd_gemv_workspace_bytes; zero
+ * it once, calls leave it zeroed). */
+size_t sd_gemv_workspace_bytes(int K, int N);
+int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
+            sd_stream_t stream);
+
 /* ---- Eq. 2 importance (kvcache.py:243-265) ----
  * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),
  * heads summed in ascending order. per_head (nullable): [L][Hk][end-start]. */

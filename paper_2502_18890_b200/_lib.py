@@ -59,6 +59,8 @@ _SIGS = {
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P, P,
                            P, P, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
+    "sd_gemv_workspace_bytes": (SZ, [INT, INT]),
+    "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_tile_weight": (INT, [P, INT, INT, P, P]),
     "sd_make_weight_tmap": (INT, [P, INT, INT, P]),
     "sd_gemm_splits": (INT, [INT, INT, INT, INT]),
@@ -124,7 +126,7 @@ def require_cuda():
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
               "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
-              "sd_gemm_splits", "sd_gemm_workspace_bytes"}
+              "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes"}
 launch_count = 0
 
 

@@ -757,6 +757,8 @@ __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* _
   const KT* K = (const KT*)p.k_cache + kvh * p.head_stride;
   const KT* V = (const KT*)p.v_cache + kvh * p.head_stride;
   const int w0 = cx * DR_CHUNK + warp * 16, w1 = min(p.ctx, w0 + 16);
+  pdl_trigger();
+  pdl_wait();  // q and the pending row come from the kernel before
   int my_rank = -1;
   if (lane < 16 && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
   float q[GM][4];
@@ -1017,9 +1019,9 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     p.ws_lse = p.ws_o + (size_t)nc * H * dh;
     dim3 grid(nc, Hk);
     if (p.G <= 4)
-      draft_attn_kernel<__nv_bfloat16, 4><<<grid, 256, 0, st>>>(p, counters, (__nv_bfloat16*)out);
+      launch_pdl(draft_attn_kernel<__nv_bfloat16, 4>, grid, dim3(256), 0, st, p, counters, (__nv_bfloat16*)out);
     else
-      draft_attn_kernel<__nv_bfloat16, 8><<<grid, 256, 0, st>>>(p, counters, (__nv_bfloat16*)out);
+      launch_pdl(draft_attn_kernel<__nv_bfloat16, 8>, grid, dim3(256), 0, st, p, counters, (__nv_bfloat16*)out);
     return check_launch("sd_attention(draft)");
   }
   if (T == 1 && p.G <= 8 && dh == 128 && !rows_dev && !ctx_dev) {

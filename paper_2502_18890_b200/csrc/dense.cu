@@ -55,6 +55,8 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
                                    const float* __restrict__ gain, float eps, XT* __restrict__ x, int splits,
                                    int64_t split_stride) {
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const int64_t base = (int64_t)blockIdx.x * d;
   float4 v[PER];
   float ss = 0.f;
@@ -92,6 +94,8 @@ __global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __
                                           const float* __restrict__ gain, float eps, XT* __restrict__ x, int splits,
                                           int64_t split_stride) {
   __shared__ float red[32];
+  pdl_trigger();
+  pdl_wait();
   const int64_t base = (int64_t)blockIdx.x * d;
   float ss = 0.f;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -148,6 +152,8 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
                                   KT* __restrict__ v, int64_t head_stride, int64_t row_offset,
                                   const int32_t* __restrict__ rows_dev, int splits, int64_t split_stride) {
   const int t = blockIdx.x;
+  pdl_trigger();
+  pdl_wait();
   if (rows_dev && t >= *rows_dev) return;
   const int half = dh >> 1;
   const int width = (H + 2 * Hk) * dh;
@@ -229,7 +235,9 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
     const int quads = d / 4;
     const int threads = quads >= 1024 ? 1024 : ((quads + 31) / 32) * 32;
     const bool two = quads > threads;
-#define SD_NORM(XT, PER) add_rmsnorm_kernel<XT, PER><<<T, threads, 0, st>>>(h, delta, d, gain, eps, (XT*)x, delta_splits, delta_split_stride)
+#define SD_NORM(XT, PER) \
+  launch_pdl(add_rmsnorm_kernel<XT, PER>, dim3(T), dim3(threads), 0, st, h, delta, d, gain, eps, (XT*)x, delta_splits, \
+             delta_split_stride)
     if (x_dtype == SD_BF16) {
       if (two) SD_NORM(__nv_bfloat16, 2); else SD_NORM(__nv_bfloat16, 1);
     } else {
@@ -239,9 +247,11 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
   } else {
     const int threads = d >= 1024 ? 1024 : (d >= 256 ? 256 : 128);
     if (x_dtype == SD_BF16)
-      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (__nv_bfloat16*)x, delta_splits, delta_split_stride);
+      launch_pdl(add_rmsnorm_scalar_kernel<__nv_bfloat16>, dim3(T), dim3(threads), 0, st, h, delta, d, gain, eps,
+                 (__nv_bfloat16*)x, delta_splits, delta_split_stride);
     else
-      add_rmsnorm_scalar_kernel<<<T, threads, 0, st>>>(h, delta, d, gain, eps, (float*)x, delta_splits, delta_split_stride);
+      launch_pdl(add_rmsnorm_scalar_kernel<float>, dim3(T), dim3(threads), 0, st, h, delta, d, gain, eps, (float*)x,
+                 delta_splits, delta_split_stride);
   }
   return check_launch("sd_add_rmsnorm");
 }
@@ -275,9 +285,9 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
   SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 4) == 0, "sd_rope_stage: head_dim must be a multiple of 4");
   auto st = as_stream(stream);
 #define SD_RS(QT, KT)                                                                                          \
-  rope_stage_kernel<QT, KT><<<T, 512, 0, st>>>(qkv, H, Hk, dh, positions, rope_cos, rope_sin, q_scale, (QT*)q_rot, \
-                                              q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev, \
-                                              qkv_splits, qkv_split_stride)
+  launch_pdl(rope_stage_kernel<QT, KT>, dim3(T), dim3(512), 0, st, qkv, H, Hk, dh, positions, rope_cos, rope_sin,  \
+             q_scale, (QT*)q_rot, q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev,       \
+             qkv_splits, qkv_split_stride)
   if (q_dtype == SD_F32 && kv_dtype == SD_F32)
     SD_RS(float, float);
   else if (q_dtype == SD_BF16 && kv_dtype == SD_BF16)

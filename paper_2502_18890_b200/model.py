@@ -261,6 +261,15 @@ class TinyTransformer:
         self._gemm_ws = None
         if dt == torch.bfloat16 and self.use_gemm:
             self._make_gemm_maps()
+        self._gemv_ws = None
+        if dt == torch.bfloat16:
+            need = 256
+            for ly in self.layers:
+                for key in ("wqkv", "wo", "w1", "w2"):
+                    need = max(need, L.load().sd_gemv_workspace_bytes(*ly[key].shape))
+            for f in self.heads:
+                need = max(need, L.load().sd_gemv_workspace_bytes(*f.shape))
+            self._gemv_ws = torch.zeros(need, dtype=torch.uint8, device=dev)
         torch.cuda.empty_cache()
 
     # Weight-streaming tcgen05 GEMM (sd_gemm) for the decode rows. Off by
@@ -287,10 +296,27 @@ class TinyTransformer:
                 need = max(need, L.load().sd_gemm_workspace_bytes(16, N, K))
         self._gemm_ws = torch.zeros(max(need, 256), dtype=torch.uint8, device=self.device)
 
+    # single-row (draft) projections stream their weights with sd_gemv
+    use_gemv = True
+
+    def gemv(self, x: torch.Tensor, w: torch.Tensor, silu: bool = False) -> torch.Tensor:
+        """[1, K] bf16 @ w [K, N] -> [1, N] fp32 (bf16 silu(.) with silu=True)."""
+        K, N = w.shape
+        y = torch.empty((1, N), dtype=self.dtype if silu else torch.float32, device=self.device)
+        L.call("sd_gemv", L.ptr(x), K, L.ptr(w), N, L.GEMM_EPI_SILU_BF16 if silu else L.GEMM_EPI_F32, L.ptr(y),
+               L.ptr(self._gemv_ws), self._gemv_ws.numel(), L.stream())
+        return y
+
+    def _gemv_ok(self, x: torch.Tensor, w: torch.Tensor) -> bool:
+        return (self.use_gemv and self._gemv_ws is not None and x.shape[0] == 1 and x.dtype == torch.bfloat16
+                and x.is_contiguous() and w.shape[1] % 8 == 0)
+
     def dense(self, x: torch.Tensor, ly: dict, key: str, silu: bool = False) -> torch.Tensor:
         """x @ ly[key] -> fp32 [T, N], or [S, T, N] split-K slices whose in-order
         sum is the product (consumed by norm() / rope_stage()); silu=True gives
         bf16 silu(x @ w) (the MLP up-projection)."""
+        if self._gemv_ok(x, ly[key]):
+            return self.gemv(x, ly[key], silu)
         tm = ly.get("tm_" + key)
         T = x.shape[0]
         if tm is None or T > 128 or not self.use_gemm or not x.is_contiguous():
@@ -418,7 +444,8 @@ class TinyTransformer:
         """Chained draft heads on the LAST row of h0 ([1, d] fp32) -> [heads, V] fp32."""
         hs = [h0]
         for i in range(heads - 1):
-            d = self.mm(hs[-1].to(self.dtype), self.heads[i])
+            xb = hs[-1].to(self.dtype)
+            d = self.gemv(xb, self.heads[i]) if self._gemv_ok(xb, self.heads[i]) else self.mm(xb, self.heads[i])
             hs.append(hs[-1] + d)
         stack = torch.cat(hs, dim=0).to(self.dtype)
         return self.mm(stack, self.embed.t())

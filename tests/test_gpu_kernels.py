@@ -676,3 +676,29 @@ def test_norm_and_rope_sum_split_slices(lib, S):
         res.append((q_rot, kr, kro, vv))
     for a, b in zip(res[0], res[1]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("K,N", [(4096, 6144), (4096, 4096), (4096, 16384), (16384, 4096), (256, 512), (64, 40)])
+def test_gemv_vs_fp32_reference(lib, K, N):
+    """Single-row weight streaming (draft forward projections, model.py:283-309):
+    fp32 out and fused SiLU -> bf16; deterministic split-K reduction; the
+    counter head is left zeroed so back-to-back calls (graph replays) work."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(K + N)
+    x = torch.randn((1, K), generator=g, device=dev).to(torch.bfloat16)
+    w = (torch.randn((K, N), generator=g, device=dev) * K ** -0.5).to(torch.bfloat16)
+    ws = torch.zeros(max(256, lib.load().sd_gemv_workspace_bytes(K, N)), dtype=torch.uint8, device=dev)
+    want = x.float() @ w.float()
+    ys = []
+    for _ in range(2):
+        y = torch.full((1, N), float("nan"), device=dev)
+        lib.call("sd_gemv", lib.ptr(x), K, lib.ptr(w), N, lib.GEMM_EPI_F32, lib.ptr(y), lib.ptr(ws), ws.numel(),
+                 lib.stream())
+        ys.append(y)
+    torch.testing.assert_close(ys[0], want, rtol=1e-4, atol=1e-4)
+    assert torch.equal(ys[0], ys[1])
+    ysil = torch.empty((1, N), dtype=torch.bfloat16, device=dev)
+    lib.call("sd_gemv", lib.ptr(x), K, lib.ptr(w), N, lib.GEMM_EPI_SILU_BF16, lib.ptr(ysil), lib.ptr(ws), ws.numel(),
+             lib.stream())
+    torch.testing.assert_close(ysil.float(), torch.nn.functional.silu(want), rtol=1e-2, atol=1e-2)

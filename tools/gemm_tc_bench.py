@@ -49,3 +49,32 @@ for M in (1, 101):
             us = best
             out.append(f"{impl} {us:6.1f} us {K * N * 2 / us / 1e3:5.0f} GB/s")
         print(f"M={M:3d} {name:4s}: " + " | ".join(out), flush=True)
+
+# single-row weight streaming (sd_gemv) vs cuBLAS
+for name, (K, N) in list(shapes.items()) + [("head", (4096, 4096))]:
+    copies = max(2, int(600e6 // (K * N * 2)))
+    Ws = [(torch.randn(K, N, device=dev) * 0.02).to(torch.bfloat16) for _ in range(copies)]
+    ws = torch.zeros(max(256, L.load().sd_gemv_workspace_bytes(K, N)), dtype=torch.uint8, device=dev)
+    x = torch.randn(1, K, device=dev).to(torch.bfloat16)
+    y = torch.empty(1, N, device=dev)
+    out = []
+    for impl in ("cublas", "sd_gemv"):
+        def run(i):
+            if impl == "cublas":
+                torch.mm(x, Ws[i % copies], out_dtype=torch.float32)
+            else:
+                L.call("sd_gemv", L.ptr(x), K, L.ptr(Ws[i % copies]), N, 0, L.ptr(y), L.ptr(ws), ws.numel(), L.stream())
+        for i in range(5):
+            run(i)
+        torch.cuda.synchronize()
+        best = 1e9
+        for rep in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for i in range(20):
+                run(i)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1) / 20 * 1e3)
+        out.append(f"{impl} {best:6.1f} us {K * N * 2 / best / 1e3:5.0f} GB/s")
+    print(f"M=  1 {name:4s} (gemv): " + " | ".join(out), flush=True)
