@@ -9,7 +9,11 @@
 // the window's count array plus at most 2*depth patched tokens (tokens slid
 // out of the window by the branch, tokens of the branch itself), so the
 // [T, V] boolean mask of the reference is never materialised.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sd {
 
@@ -430,6 +434,134 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   }
 }
 
+// Engine path (fp32 logits, no truncation or min-p, token draw only): a
+// cluster of SC_CTAS CTAs per row, each owning a contiguous 1/SC_CTAS of the
+// vocabulary, so a row is spread over 8 SMs instead of one. Cross-CTA
+// reductions go through distributed shared memory and are combined in CTA
+// order on every CTA (identical results everywhere, deterministic):
+//   1. online max / sum-exp of the penalised scaled logits (sampling.py:142-162);
+//   2. kept mass per CTA (min-p keeps p >= p_base * p_max, sampling.py:207-210);
+//   3. the CTA whose prefix holds u = uniform_at(seed, pos) walks its slice in
+//      32-key warp chunks for the first cumsum > u (sampling.py:219-224).
+constexpr int SC_CTAS = 8, SC_THREADS = 512;
+
+__global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
+    sample_rows_cluster_kernel(const float* __restrict__ logits, SampleDev a) {
+  __shared__ RowCtx rc;
+  __shared__ float s_m;
+  __shared__ double s_z, s_k;
+  __shared__ double dred[32];
+  __shared__ float fred[32];
+  __shared__ double wtot[SC_THREADS / 32];
+  __shared__ int s_hit;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int row = blockIdx.x / SC_CTAS, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool live = row < a.rows && !(a.member_kind == SD_MEMBER_TREE && row >= a.tree[tree_off::T]);
+  const int V = a.V;
+  const int v0 = (int)((int64_t)V * rank / SC_CTAS), v1 = (int)((int64_t)V * (rank + 1) / SC_CTAS);
+  const float* lg = logits + (int64_t)row * V;
+  if (live && tid == 0) row_setup(a, row, rc);
+  __syncthreads();
+  const float inv_t = (float)(1.0 / a.temperature), inv_tt = (float)(1.0 / (a.temperature * a.theta));
+  const float th = (float)a.theta;
+  auto scaled_f = [&](int v) -> float {
+    const float l = lg[v];
+    if (!is_member(a, rc, row, v)) return l * inv_t;
+    if (a.ctrl_style) return (l < 0.f ? l * th : l / th) * inv_t;
+    return l * inv_tt;
+  };
+  // ---- 1. online max / sum-exp over this CTA's slice ----
+  float lm = -INFINITY;
+  double lz = 0.0;
+  if (live) {
+    for (int v = v0 + tid; v < v1; v += SC_THREADS) {
+      const float sv = scaled_f(v);
+      if (sv > lm) {
+        lz = lz * (double)expf(lm - sv);
+        lm = sv;
+      }
+      lz += (double)expf(sv - lm);
+    }
+  }
+  const float cm = block_reduce(lm, fred, [](float x, float y) { return fmaxf(x, y); });
+  lz = lm == -INFINITY ? 0.0 : lz * exp((double)lm - (double)cm);
+  const double cz = block_reduce(lz, dred, [](double x, double y) { return x + y; });
+  if (tid == 0) {
+    s_m = cm;
+    s_z = cz;
+  }
+  cluster.sync();
+  float mf = -INFINITY;
+  for (int r = 0; r < SC_CTAS; ++r) mf = fmaxf(mf, *cluster.map_shared_rank(&s_m, r));
+  double Z = 0.0;
+  for (int r = 0; r < SC_CTAS; ++r) {
+    const float mr = *cluster.map_shared_rank(&s_m, r);
+    const double zr = *cluster.map_shared_rank(&s_z, r);
+    Z += mr == -INFINITY ? 0.0 : zr * exp((double)mr - (double)mf);
+  }
+  const double invZ = 1.0 / Z;
+  // min-p: p_max = exp(0) / Z, so keep p >= p_base / Z
+  const double thr = a.trunc_kind == SD_TRUNC_MIN_P ? a.trunc_value * invZ : -1.0;
+  auto kept = [&](int v) -> double {
+    const double p = (double)expf(scaled_f(v) - mf) * invZ;
+    return p >= thr ? p : 0.0;
+  };
+  // ---- 2. kept mass in warp-contiguous chunks of this CTA's slice ----
+  constexpr int NW = SC_THREADS / 32;
+  const int S = ((v1 - v0) + NW * 32 - 1) / (NW * 32) * 32;
+  const int c0 = v0 + wid * S, c1 = min(v1, c0 + S);
+  double lk = 0.0;
+  if (live)
+    for (int v = c0 + lane; v < c1; v += 32) lk += kept(v);
+  lk = warp_sum_d(lk);
+  if (lane == 0) wtot[wid] = lk;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += wtot[w];
+    s_k = t;
+    s_hit = 0x7fffffff;
+  }
+  cluster.sync();
+  double K = 0.0, prefix = 0.0;
+  for (int r = 0; r < SC_CTAS; ++r) {
+    const double kr = *cluster.map_shared_rank(&s_k, r);
+    if (r < rank) prefix += kr;
+    K += kr;
+  }
+  // ---- 3. inverse CDF: first v with cumsum(kept / K) > u ----
+  const double u = live ? uniform_at(a.seed, (uint64_t)rc.pos) : 2.0;
+  double before = prefix / K;
+  for (int w = 0; w < wid; ++w) before += wtot[w] / K;
+  const double mine = wtot[wid] / K;
+  const bool last_chunk = c1 >= V;
+  if (live && c0 < c1 && before <= u + 1e-12 && (before + mine > u - 1e-12 || last_chunk)) {
+    double c = before;
+    for (int vb = c0; vb < c1; vb += 32) {
+      const int v = vb + lane;
+      double x = v < c1 ? kept(v) / K : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      const unsigned hit = __ballot_sync(0xffffffffu, v < c1 && c + x > u);
+      if (hit) {
+        if (lane == 0) atomicMin(cluster.map_shared_rank(&s_hit, 0), vb + __ffs(hit) - 1);
+        break;
+      }
+      c += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  cluster.sync();
+  if (live && rank == 0 && tid == 0) {
+    int idx = s_hit;
+    if (idx > V - 1) idx = V - 1;
+    a.token_out[row] = idx;
+  }
+}
+
 // draft per-head top-w (engine.py:207-215): one CTA per head, one pass over
 // the vocabulary. Candidates are ranked by the penalised scaled logit s
 // (exp(s - m) / Z is monotone in s), ties to the lower id. Each thread keeps a
@@ -536,6 +668,12 @@ int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t 
   SD_REQUIRE(h.positions || h.tree, "sd_sample_rows: need positions or tree");
   SampleDev d = to_dev(h);
   auto st = as_stream(stream);
+  if (h.in_kind == SD_IN_LOGITS_F32 && !h.probs_out && !h.trunc_out && h.token_out &&
+      (h.trunc_kind == SD_TRUNC_NONE || h.trunc_kind == SD_TRUNC_MIN_P)) {
+    // engine path: one CTA cluster per row
+    sample_rows_cluster_kernel<<<h.rows * SC_CTAS, SC_THREADS, 0, st>>>((const float*)in, d);
+    return check_launch("sd_sample_rows(cluster)");
+  }
   switch (h.in_kind) {
     case SD_IN_LOGITS_F32: sample_rows_kernel<SD_IN_LOGITS_F32><<<h.rows, SMP_THREADS, 0, st>>>(in, d); break;
     case SD_IN_LOGITS_F64: sample_rows_kernel<SD_IN_LOGITS_F64><<<h.rows, SMP_THREADS, 0, st>>>(in, d); break;

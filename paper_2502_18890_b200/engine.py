@@ -151,7 +151,9 @@ class Session:
         self.state[L.ST_PENDING] = self.tokens[-1]
         self.state[L.ST_BASE] = len(self.tokens) - 1
         self._ev = torch.cuda.Event()
-        self.use_graph = graph
+        # CUDA-graph replay on one GPU; sharded sessions (NCCL all-gathers inside
+        # the forward) run eagerly
+        self.use_graph = graph and model.world == 1
         self._graph: torch.cuda.CUDAGraph | None = None
         self._eager_steps = 0
         if prefill:
