@@ -101,7 +101,11 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
  * ignored). With ctx_dev every argument is step-invariant, so the call can be
  * captured once in a CUDA graph and replayed as the cache grows.
  * CUDA-core split boundaries depend on ctx only (bitwise identical across GPU
- * counts); the tensor-core path splits by SM count. */
+ * counts); the tensor-core path splits by SM count. The tensor-core and draft
+ * kernels are programmatic dependent launches: rows_dev, ctx_dev, ranks and
+ * the committed cache rows are read before the dependency wait, so they must
+ * not be written by the kernel launched immediately before (q, the tree rows
+ * and the pending row may be). */
 /* The workspace starts with SD_ATTN_WS_HEAD bytes of arrival counters: zero
  * them once when the workspace is allocated; every call leaves them zero. */
 #define SD_ATTN_WS_HEAD 4096

@@ -435,6 +435,8 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
                                                        OT* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);  // t * H + head
+  pdl_trigger();
+  pdl_wait();  // the split partials are the predecessor's output
   if (row >= TH) return;
   OT* dst = out + (int64_t)row * 128 + 4 * lane;
   if (rows_dev && row / H >= *rows_dev) {  // padded row: defined zeros
@@ -479,7 +481,7 @@ template <typename OT>
 static void launch_merge(const float* ws_o, const float* ws_lse, int nsplit, int TH, int H, const int32_t* rows_dev,
                          OT* out, int dh, cudaStream_t st) {
   if (dh == 128 && nsplit <= 96)
-    merge128_kernel<OT><<<(TH + 7) / 8, 256, 0, st>>>(ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
+    launch_pdl(merge128_kernel<OT>, dim3((TH + 7) / 8), dim3(256), 0, st, ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
   else
     attn_merge_kernel<128, OT><<<TH, 128, 0, st>>>(ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
 }

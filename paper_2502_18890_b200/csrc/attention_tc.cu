@@ -109,6 +109,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kvh = blockIdx.y;
+  // Programmatic dependent launch: this kernel may start while its predecessor
+  // (the RoPE/KV staging of this layer) still runs. rows_dev / ctx_dev (the
+  // tree record) and the committed cache rows come from earlier kernels and are
+  // read at once; q and the staged tree rows only after pdl_wait.
+  pdl_trigger();
   const int T = p.rows_dev ? min(*p.rows_dev, p.T) : p.T;
   const int GT = p.G * T;
   const int rg = blockIdx.z * ROWS;
@@ -171,6 +176,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int qt = tid < 96 ? tid - 32 : tid - 64;
     constexpr int PER = (ROWS * (DH / 8) + NT - 1) / NT;  // 16-byte chunks per thread
     uint4 v[PER];
+    pdl_wait();  // q is the predecessor's output
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
       const int i = qt + k * NT;
@@ -216,9 +222,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint64_t* empty = is_k ? k_empty : v_empty;
       uint8_t* ring = smem + (is_k ? OFF_K : OFF_V);
       tma_prefetch(map);
+      bool waited = false;
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
         const int key0 = key_begin + j * BN;
+        if (!waited && key0 + BN > ctx) {  // tile reaches the tree rows staged by the predecessor
+          pdl_wait();
+          waited = true;
+        }
         if (j >= ST) mbar_wait(&empty[s], ((j / ST) + 1) & 1);
         trace(0, j, is_k ? 1 : 2);
         uint8_t* d = ring + s * KV_TILE;
@@ -551,7 +562,7 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   CUtensorMap mk, mv;
   memcpy(&mk, tmap_k, sizeof(CUtensorMap));
   memcpy(&mv, tmap_v, sizeof(CUtensorMap));
-  tc::verify_attn_tc_kernel<<<grid, tc::THREADS, tc::SMEM_ALLOC, st>>>(mk, mv, p);
+  launch_pdl(tc::verify_attn_tc_kernel, grid, dim3(tc::THREADS), tc::SMEM_ALLOC, st, mk, mv, p);
   return check_launch("sd_attention(tcgen05)");
 }
 
