@@ -74,10 +74,19 @@ struct Params {
 // production kernels carry no instrumentation on the MMA critical path.
 __device__ int64_t* g_tc_trace = nullptr;
 // Debug-only pipeline experiments (-DSD_TC_EXPERIMENT=n, tools/gpu_tc_exp.sh):
-// 1 = softmax skips its math, 2 = no PV MMAs, 3 = no QK MMAs, 4 = 1+2+3 (TMA stream only).
+// 1 = softmax skips its math, 2 = no PV MMAs, 3 = no QK MMAs, 4 = 1+2+3 (TMA stream only),
+// 5 = 4 without the softmax's TMEM loads, 6 = 5 with plain mbarrier arrives instead of commits.
 #ifndef SD_TC_EXPERIMENT
 #define SD_TC_EXPERIMENT 0
 #endif
+#define SD_TC_NOMMA (SD_TC_EXPERIMENT >= 4)
+__device__ __forceinline__ void tc_signal(uint64_t* bar) {
+#if SD_TC_EXPERIMENT == 6
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+#else
+  umma_commit(bar);
+#endif
+}
 constexpr int TR_TILES = 64, TR_EV = 8;
 __device__ __forceinline__ void trace(int role, int j, int ev) {
 #ifdef SD_TC_TRACE
@@ -259,11 +268,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t half = ks >> 2, in = (ks & 3) * 32;
           const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
           const uint64_t a = umma_desc(q_base + half * 16384 + in, 16, 1024);
-          if (SD_TC_EXPERIMENT != 3 && SD_TC_EXPERIMENT != 4)
+          if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA)
             umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
         }
-        umma_commit(&s_full[2 * mt + b]);
-        umma_commit(&k_empty[s]);
+        tc_signal(&s_full[2 * mt + b]);
+        tc_signal(&k_empty[s]);
       };
       auto wait_k = [&](int j) {
         if (mt == 0) trace(1, j, 0);
@@ -288,12 +297,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ks = 0; ks < BN / 16; ++ks) {
           // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
           const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-          if (SD_TC_EXPERIMENT != 2 && SD_TC_EXPERIMENT != 4)
+          if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA)
             umma_bf16_ts(o_col, p_tmem + 8 * ks, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
         }
-        umma_commit(&pv_done[2 * mt + b]);
-        if (j == n_tiles - 1) umma_commit(&o_final[mt]);
-        umma_commit(&v_empty[s]);
+        tc_signal(&pv_done[2 * mt + b]);
+        if (j == n_tiles - 1) tc_signal(&o_final[mt]);
+        tc_signal(&v_empty[s]);
         if (mt == 0) trace(1, j, 6);
         // S(j+2) into buffer b: issued after PV(j) by this thread, so it is
         // ordered after PV(j)'s reads of P(j) (same-thread tcgen05.mma order)
@@ -337,10 +346,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t s_addr = tmem + lane_base + COL_S + 128 * mt + 64 * b;
         uint32_t sr[64];
+#if SD_TC_EXPERIMENT < 5
         tmem_ld32(s_addr, sr);
         tmem_ld32(s_addr + 32, sr + 32);
         tmem_wait_ld();
-        if (SD_TC_EXPERIMENT == 1 || SD_TC_EXPERIMENT == 4) {
+#else
+        for (int c = 0; c < 64; ++c) sr[c] = 0u;
+#endif
+        if (SD_TC_EXPERIMENT == 1 || SD_TC_NOMMA) {
           tc_fence_before();
           mbar_arrive(&p_full[2 * mt + b]);
           l += __uint_as_float(sr[lane]);

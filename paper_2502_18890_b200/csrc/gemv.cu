@@ -23,7 +23,13 @@ namespace gv {
 
 constexpr int COLS = 256;    // columns per CTA (32 lanes x 8)
 constexpr int WARPS = 8;
-constexpr int UNROLL = 8;    // weight rows in flight per warp
+#ifndef SD_GEMV_UNROLL
+#define SD_GEMV_UNROLL 8
+#endif
+#ifndef SD_GEMV_CTAS_PER_SM
+#define SD_GEMV_CTAS_PER_SM 4
+#endif
+constexpr int UNROLL = SD_GEMV_UNROLL;  // weight rows in flight per warp
 
 __device__ __forceinline__ void fma8(float* acc, float xv, const uint4& w) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
@@ -120,7 +126,7 @@ static int splits_for(int K, int N) {
   const int blocks = (N + COLS - 1) / COLS;
   // ~4 CTAs per SM in flight, each with >= 256 weight rows; wide outputs (many
   // column blocks) keep longer K slices
-  int s = (148 * (blocks >= 64 ? 2 : 4) + blocks - 1) / blocks;
+  int s = (148 * (blocks >= 64 ? SD_GEMV_CTAS_PER_SM / 2 : SD_GEMV_CTAS_PER_SM) + blocks - 1) / blocks;
   const int max_s = K / 256 > 0 ? K / 256 : 1;
   if (s > max_s) s = max_s;
   return s < 1 ? 1 : s;

@@ -44,6 +44,8 @@ def init_from_env(backend: str = "nccl"):
 def gather_rank_major(x: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """All-gather x from every rank -> [world, *x.shape] in rank order (NCCL
     over NVLink on the product path; gloo in the CPU tests)."""
+    if x.is_cuda and dist.get_backend(group) == "gloo":  # CPU-side collectives (single-GPU multi-rank checks)
+        return gather_rank_major(x.cpu(), world, group).to(x.device)
     flat = torch.empty((world * x.shape[0],) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
     dist.all_gather_into_tensor(flat, x.contiguous(), group=group)
     return flat.view((world,) + tuple(x.shape))
