@@ -30,6 +30,14 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+SHAPE_NAME = {"cfg1": "tiny LLaMA-style", "cfg2": "Qwen2.5-1.5B shape", "cfg3": "LLaMA3.1-8B shape",
+              "cfg4": "YaRN-LLaMA2-7B (MHA) shape", "cfg5": "Qwen2.5-14B shape"}
+
+
+def metric_name(cfg_name):
+    return f"generated tokens/s (TokenSwift decode, {SHAPE_NAME[cfg_name]})"
+
+
 CONFIGS = {
     # name: model dims, engine, sampler (Table 9 / SURVEY.md §8d)
     "cfg1": dict(V=32000, d=256, L=2, H=8, Hk=2, prefix=512, gen=2000, B=512, S=32, trunc=("min_p", 1.0), theta=1.2),
@@ -150,7 +158,7 @@ def run_reference(args, c, ctx):
         line = cpu_baseline_line(c, ctx, accepted=4.0, tree_rows=41)
         vals.append(line["value"])
     v = statistics.median(vals)
-    out = {"metric": "generated tokens/s (TokenSwift decode, LLaMA3.1-8B shape)", "value": v, "unit": "tokens/s",
+    out = {"metric": metric_name(args.config), "value": v, "unit": "tokens/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
            "ms_per_step": 4000.0 / v if v else None, "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -238,7 +246,7 @@ def main():
         return
     clocks = clk.summary()
     out = {
-        "metric": "generated tokens/s (TokenSwift decode, LLaMA3.1-8B shape)",
+        "metric": metric_name(args.config),
         "value": tokens / dev_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",

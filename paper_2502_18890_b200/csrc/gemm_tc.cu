@@ -350,7 +350,7 @@ size_t sd_gemm_workspace_bytes(int M, int N, int K) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   const int s = gm::splits_for(M, N, K, SD_GEMM_EPI_SILU_BF16);
   if (s <= 1) return 0;
-  return (((size_t)(N / gm::BN) * sizeof(int) + 255) & ~(size_t)255) + (size_t)s * M * N * sizeof(float);
+  return (size_t)4096 + (size_t)s * M * N * sizeof(float);  // fixed counter head: shapes may share a workspace
 }
 
 int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi, void* y, int64_t ldy,
@@ -386,7 +386,8 @@ int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi
   p.y = y;
   p.ldy = ldy;
   p.counters = (int*)workspace;
-  p.ws = need ? (float*)((char*)workspace + (((size_t)(N / gm::BN) * sizeof(int) + 255) & ~(size_t)255)) : nullptr;
+  SD_REQUIRE((N / gm::BN) * sizeof(int) <= 4096, "sd_gemm: N too wide for the counter head");
+  p.ws = need ? (float*)((char*)workspace + 4096) : nullptr;
   const int items = (N / gm::BN) * p.splits;
   dim3 grid(items < 148 ? items : 148);
   gm::gemm_stream_kernel<<<grid, gm::THREADS, gm::SMEM_ALLOC, as_stream(stream)>>>(mx, mw, p);

@@ -122,6 +122,11 @@ __global__ void __launch_bounds__(WARPS * 32) gemv_kernel(const __nv_bfloat16* _
   if (tid == 0) counters[cb] = 0;  // ready for the next launch / graph replay
 }
 
+// The workspace starts with a fixed 4 KB counter head (one int per column block)
+// so that calls of different shapes sharing one workspace never see each other's
+// partials in their counters.
+constexpr size_t WS_HEAD = 4096;
+
 static int splits_for(int K, int N) {
   const int blocks = (N + COLS - 1) / COLS;
   // ~4 CTAs per SM in flight, each with >= 256 weight rows; wide outputs (many
@@ -142,8 +147,7 @@ extern "C" {
 size_t sd_gemv_workspace_bytes(int K, int N) {
   if (K <= 0 || N <= 0) return 0;
   const int s = gv::splits_for(K, N);
-  const size_t blocks = (N + gv::COLS - 1) / gv::COLS;
-  return ((blocks * sizeof(int) + 255) & ~(size_t)255) + (s > 1 ? (size_t)s * N * sizeof(float) : 0);
+  return gv::WS_HEAD + (s > 1 ? (size_t)s * N * sizeof(float) : 0);
 }
 
 int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
@@ -154,7 +158,8 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
   const int s = gv::splits_for(K, N);
   SD_REQUIRE(s == 1 || (workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N)), "sd_gemv: workspace");
   const int blocks = (N + gv::COLS - 1) / gv::COLS;
-  const size_t head = ((size_t)blocks * sizeof(int) + 255) & ~(size_t)255;
+  SD_REQUIRE((size_t)blocks * sizeof(int) <= gv::WS_HEAD, "sd_gemv: N=%d too wide for the counter head", N);
+  const size_t head = gv::WS_HEAD;
   const int kslice = (K + s - 1) / s + 1;
   const size_t smem = (size_t)kslice * sizeof(float);
   SD_REQUIRE(smem <= 200 * 1024, "sd_gemv: K slice too long");

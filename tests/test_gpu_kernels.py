@@ -702,3 +702,20 @@ def test_gemv_vs_fp32_reference(lib, K, N):
     lib.call("sd_gemv", lib.ptr(x), K, lib.ptr(w), N, lib.GEMM_EPI_SILU_BF16, lib.ptr(ysil), lib.ptr(ws), ws.numel(),
              lib.stream())
     torch.testing.assert_close(ysil.float(), torch.nn.functional.silu(want), rtol=1e-2, atol=1e-2)
+
+
+def test_gemv_shared_workspace_across_shapes(lib):
+    """One zeroed workspace serves every shape (the model shares it across
+    layers): a narrow split call's partials must not land in a wider call's
+    arrival counters (cfg5: w2 [20480, 5120] then w1 [5120, 20480])."""
+    dev = torch.device("cuda")
+    shapes = [(20480, 5120), (5120, 20480), (4096, 6144), (5120, 20480)]
+    need = max(lib.load().sd_gemv_workspace_bytes(K, N) for K, N in shapes)
+    ws = torch.zeros(need, dtype=torch.uint8, device=dev)
+    for K, N in shapes:
+        x = torch.randn((1, K), device=dev).to(torch.bfloat16)
+        w = (torch.randn((K, N), device=dev) * K ** -0.5).to(torch.bfloat16)
+        y = torch.empty((1, N), device=dev)
+        lib.call("sd_gemv", lib.ptr(x), K, lib.ptr(w), N, lib.GEMM_EPI_F32, lib.ptr(y), lib.ptr(ws), ws.numel(),
+                 lib.stream())
+        torch.testing.assert_close(y, x.float() @ w.float(), rtol=1e-4, atol=1e-4)
