@@ -434,19 +434,24 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
   }
 }
 
-// Engine path (fp32 logits, no truncation or min-p, token draw only): a
+// Engine path (fp32 logits; no truncation, min-p or top-p; token draw only): a
 // cluster of SC_CTAS CTAs per row, each owning a contiguous 1/SC_CTAS of the
 // vocabulary, so a row is spread over 8 SMs instead of one. Cross-CTA
 // reductions go through distributed shared memory and are combined in CTA
 // order on every CTA (identical results everywhere, deterministic):
 //   1. online max / sum-exp of the penalised scaled logits (sampling.py:142-162);
-//   2. kept mass per CTA (min-p keeps p >= p_base * p_max, sampling.py:207-210);
+//   2. truncation: min-p keeps p >= p_base * p_max (sampling.py:207-210); top-p
+//      bisects the nucleus threshold over the bit patterns of e = exp(s - max)
+//      (fp32, positive: bit order == value order == order of p = e / Z, and equal
+//      bits <=> equal p) with cluster-summed masses, ties at the threshold kept
+//      lowest index first (sampling.py:198-205); then kept mass per CTA;
 //   3. the CTA whose prefix holds u = uniform_at(seed, pos) walks its slice in
 //      32-key warp chunks for the first cumsum > u (sampling.py:219-224).
 constexpr int SC_CTAS = 8, SC_THREADS = 512;
 
 __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
     sample_rows_cluster_kernel(const float* __restrict__ logits, SampleDev a) {
+  extern __shared__ float ecache[];  // e = exp(s - max) of this CTA's slice
   __shared__ RowCtx rc;
   __shared__ float s_m;
   __shared__ double s_z, s_k;
@@ -454,6 +459,8 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
   __shared__ float fred[32];
   __shared__ double wtot[SC_THREADS / 32];
   __shared__ int s_hit;
+  __shared__ double s_tot;
+  __shared__ int s_cnt, s_vcut;
   cg::cluster_group cluster = cg::this_cluster();
   const int rank = (int)cluster.block_rank();
   const int row = blockIdx.x / SC_CTAS, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -501,16 +508,163 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
     Z += mr == -INFINITY ? 0.0 : zr * exp((double)mr - (double)mf);
   }
   const double invZ = 1.0 / Z;
-  // min-p: p_max = exp(0) / Z, so keep p >= p_base / Z
-  const double thr = a.trunc_kind == SD_TRUNC_MIN_P ? a.trunc_value * invZ : -1.0;
-  auto kept = [&](int v) -> double {
-    const double p = (double)expf(scaled_f(v) - mf) * invZ;
-    return p >= thr ? p : 0.0;
-  };
-  // ---- 2. kept mass in warp-contiguous chunks of this CTA's slice ----
+  // warp-contiguous chunks of this CTA's slice (coalesced; chunk w = [c0, c1))
   constexpr int NW = SC_THREADS / 32;
   const int S = ((v1 - v0) + NW * 32 - 1) / (NW * 32) * 32;
   const int c0 = v0 + wid * S, c1 = min(v1, c0 + S);
+  if (live)
+    for (int v = v0 + tid; v < v1; v += SC_THREADS) ecache[v - v0] = expf(scaled_f(v) - mf);
+  __syncthreads();
+  auto ebits = [&](int v) -> int { return __float_as_int(ecache[v - v0]); };
+  auto prob = [&](int v) -> double { return (double)ecache[v - v0] * invZ; };
+  // min-p: p_max = exp(0) / Z, so keep p >= p_base / Z
+  const double thr = a.trunc_kind == SD_TRUNC_MIN_P ? a.trunc_value * invZ : -1.0;
+  int pbits = -1;  // top-p threshold: keep bits > pbits, and bits == pbits up to index vcut
+  int vcut = V;
+  if (a.trunc_kind == SD_TRUNC_TOP_P) {
+    // cluster-wide masses of {e >= t_i} for NQ thresholds at once (fp64, CTA order):
+    // an NQ+1-ary search over the bit range needs ~ceil(31 / log2(NQ+1)) passes
+    constexpr int NQ = 1;  // binary search measured fastest (fp64 partial sums per threshold cost more than passes)
+    __shared__ double s_q[SC_THREADS / 32][NQ];
+    __shared__ double s_qc[NQ];
+    auto mass_ge_n = [&](const int* t, double* out) {
+      double ml[NQ];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) ml[i] = 0.0;
+      double all = 0.0;  // elements at or above the top threshold count for every t_i
+      if (live)
+        for (int v = v0 + tid; v < v1; v += SC_THREADS) {
+          const int b = ebits(v);
+          if (b < t[0]) continue;  // the common case once the range has narrowed
+          const double e = (double)ecache[v - v0];
+          if (b >= t[NQ - 1]) {
+            all += e;
+          } else {
+#pragma unroll
+            for (int i = 0; i < NQ - 1; ++i) ml[i] += b >= t[i] ? e : 0.0;
+          }
+        }
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const double w = warp_sum_d(ml[i] + all);
+        if (lane == 0) s_q[wid][i] = w;
+      }
+      __syncthreads();
+      if (tid < NQ) {
+        double c = 0.0;
+        for (int w = 0; w < SC_THREADS / 32; ++w) c += s_q[w][tid];
+        s_qc[tid] = c;
+      }
+      cluster.sync();
+      if (tid < NQ) {
+        double t2 = 0.0;
+        for (int r = 0; r < SC_CTAS; ++r) t2 += cluster.map_shared_rank(s_qc, r)[tid];
+        s_q[0][tid] = t2 * invZ;  // own smem scratch: peers only read s_qc
+      }
+      cluster.sync();  // s_qc is rewritten by the next query
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) out[i] = s_q[0][i];
+      __syncthreads();
+    };
+    int t0[NQ];
+    double m0[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) t0[i] = i == 0 ? 0 : 0x7f800001;
+    mass_ge_n(t0, m0);
+    const double total = m0[0];
+    if (a.trunc_value < total) {
+      // largest b with mass(e >= b) >= top_p: an element's value; above = mass(e > b)
+      int lo = 0, hi = 0x7f800001;
+      double above = 0.0;
+      while (hi - lo > 1) {
+        int t[NQ];
+        double mm[NQ];
+        const int64_t span = (int64_t)hi - lo;
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) {
+          int64_t ti = lo + span * (i + 1) / (NQ + 1);
+          if (ti <= lo) ti = lo + 1;
+          if (ti >= hi) ti = hi - 1;
+          t[i] = (int)ti;
+        }
+        mass_ge_n(t, mm);
+        // thresholds ascend, masses descend: lo = the largest t_i with mass >= top_p
+        int nlo = lo, nhi = hi;
+        double nabove = above;
+#pragma unroll
+        for (int i = NQ - 1; i >= 0; --i) {
+          if (mm[i] >= a.trunc_value) {
+            if (t[i] > nlo) nlo = t[i];
+          } else if (t[i] < nhi) {
+            nhi = t[i];
+            nabove = mm[i];
+          }
+        }
+        lo = nlo;
+        hi = nhi;
+        above = nabove;
+      }
+      pbits = lo;
+      const double pstar = (double)__int_as_float(lo) * invZ;
+      // elements equal to pstar: keep the lowest-index `need` of them
+      int ce = 0;
+      if (live)
+        for (int v = v0 + tid; v < v1; v += SC_THREADS) ce += ebits(v) == lo;
+      ce = (int)block_reduce((double)ce, dred, [](double x, double y) { return x + y; });
+      if (tid == 0) {
+        s_cnt = ce;
+        s_vcut = V;
+      }
+      cluster.sync();
+      int ceq = 0, before_eq = 0;
+      for (int r = 0; r < SC_CTAS; ++r) {
+        const int cr = *cluster.map_shared_rank(&s_cnt, r);
+        if (r < rank) before_eq += cr;
+        ceq += cr;
+      }
+      int need = (int)ceil((a.trunc_value - above) / pstar);
+      if (need < 1) need = 1;
+      if (need > ceq) need = ceq;
+      if (need < ceq && before_eq < need && need <= before_eq + ce && live) {
+        // the need-th equal element (index order) is in this CTA's slice: warp-chunk scan
+        const int want = need - before_eq;
+        int cw = 0;
+        for (int v = c0 + lane; v < c1; v += 32) cw += ebits(v) == lo;
+        cw = (int)warp_sum_d((double)cw);
+        if (lane == 0) wtot[wid] = (double)cw;
+        __syncthreads();
+        int bw = 0;
+        for (int w = 0; w < wid; ++w) bw += (int)wtot[w];
+        if (bw < want && want <= bw + cw) {
+          int cnt = bw;
+          for (int vb = c0; vb < c1; vb += 32) {
+            const int v = vb + lane;
+            const unsigned eq = __ballot_sync(0xffffffffu, v < c1 && ebits(v) == lo);
+            const int n_eq = __popc(eq);
+            if (cnt + n_eq >= want) {
+              unsigned m2 = eq;
+              for (int k = cnt; k < want - 1; ++k) m2 &= m2 - 1;  // drop the lowest (want-1-cnt) bits
+              if (lane == 0) *cluster.map_shared_rank(&s_vcut, 0) = vb + __ffs(m2) - 1;
+              break;
+            }
+            cnt += n_eq;
+          }
+        }
+        __syncthreads();
+      }
+      cluster.sync();
+      vcut = need >= ceq ? V : *cluster.map_shared_rank(&s_vcut, 0);
+    }
+  }
+  auto kept = [&](int v) -> double {
+    const double p = prob(v);
+    if (pbits >= 0) {
+      const int b = ebits(v);
+      return (b > pbits || (b == pbits && v <= vcut)) ? p : 0.0;
+    }
+    return p >= thr ? p : 0.0;
+  };
+  // ---- 2. kept mass in warp-contiguous chunks of this CTA's slice ----
   double lk = 0.0;
   if (live)
     for (int v = c0 + lane; v < c1; v += 32) lk += kept(v);
@@ -669,9 +823,16 @@ int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t 
   SampleDev d = to_dev(h);
   auto st = as_stream(stream);
   if (h.in_kind == SD_IN_LOGITS_F32 && !h.probs_out && !h.trunc_out && h.token_out &&
-      (h.trunc_kind == SD_TRUNC_NONE || h.trunc_kind == SD_TRUNC_MIN_P)) {
+      (h.trunc_kind == SD_TRUNC_NONE || h.trunc_kind == SD_TRUNC_MIN_P || h.trunc_kind == SD_TRUNC_TOP_P)) {
     // engine path: one CTA cluster per row
-    sample_rows_cluster_kernel<<<h.rows * SC_CTAS, SC_THREADS, 0, st>>>((const float*)in, d);
+    const size_t smem = (size_t)((h.V + SC_CTAS - 1) / SC_CTAS) * sizeof(float);
+    SD_REQUIRE(smem <= 200 * 1024, "sd_sample_rows: vocabulary too large for the cluster path");
+    static size_t attr_smem = 0;
+    if (smem > 48 * 1024 && smem > attr_smem) {
+      cudaFuncSetAttribute(sample_rows_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_smem = smem;
+    }
+    sample_rows_cluster_kernel<<<h.rows * SC_CTAS, SC_THREADS, smem, st>>>((const float*)in, d);
     return check_launch("sd_sample_rows(cluster)");
   }
   switch (h.in_kind) {

@@ -719,3 +719,45 @@ def test_gemv_shared_workspace_across_shapes(lib):
         lib.call("sd_gemv", lib.ptr(x), K, lib.ptr(w), N, lib.GEMM_EPI_F32, lib.ptr(y), lib.ptr(ws), ws.numel(),
                  lib.stream())
         torch.testing.assert_close(y, x.float() @ w.float(), rtol=1e-4, atol=1e-4)
+
+
+@pytest.mark.parametrize("V", [64, 5000, 151936])
+@pytest.mark.parametrize("trunc", ["none", "min_p", "top_p"])
+def test_cluster_sampler_equals_row_sampler(lib, V, trunc):
+    """Engine-path sampler (8-CTA cluster per row, DSMEM reductions, top-p radix
+    descent across the cluster) draws the same tokens as the single-CTA row
+    sampler (selected by requesting probs_out) on fp32 logits with per-row
+    window splices (engine.py:155-181, sampling.py:142-224)."""
+    from paper_2502_18890_b200 import _lib as Lb
+    from paper_2502_18890_b200.sampling import PenaltyWindow
+    g = np.random.default_rng(V)
+    W, depth = 64, 4
+    st = torch.zeros(16, dtype=torch.int64, device="cuda")
+    dw = PenaltyWindow(W, V, state=st)
+    dw.push_many(g.integers(0, V, size=40).tolist())
+    per_head = [[int(x) for x in g.choice(V, w, replace=False)] for w in (1, 3, 3, 3)]
+    rec = torch.zeros(Lb.tree_layout()["TOTAL"], dtype=torch.int32, device="cuda")
+    flat = torch.tensor([t for c in per_head for t in c], dtype=torch.int32, device="cuda")
+    Lb.call("sd_tree_build", Lb.ptr(flat), Lb.host_i32([1, 3, 3, 3]), 4, None, None, 0, None, 99, Lb.ptr(rec),
+            Lb.stream())
+    T = 41
+    code, val = {"none": (Lb.TRUNC_NONE, 0.0), "min_p": (Lb.TRUNC_MIN_P, 0.1), "top_p": (Lb.TRUNC_TOP_P, 0.9)}[trunc]
+    outs = []
+    for trial in range(2):
+        logits = torch.as_tensor(g.normal(scale=3.0, size=(T, V)), dtype=torch.float32, device="cuda")
+        for use_row in (False, True):
+            y = torch.full((T,), -1, dtype=torch.int32, device="cuda")
+            probs = torch.empty((T, V), dtype=torch.float64, device="cuda") if use_row else None
+            a = Lb.SampleArgs()
+            a.rows, a.V, a.in_kind = T, V, Lb.IN_LOGITS_F32
+            a.temperature, a.theta, a.ctrl_style = 0.9, 1.2, 0
+            a.member_kind = Lb.MEMBER_TREE
+            a.win_count, a.win_ring, a.state, a.window = Lb.ptr(dw.count), Lb.ptr(dw.ring), Lb.ptr(st), W
+            a.tree, a.depth = Lb.ptr(rec), depth
+            a.trunc_kind, a.trunc_value, a.eta_alpha = code, val, -1.0
+            a.seed, a.n = trial, 100
+            a.probs_out, a.token_out = Lb.ptr(probs), Lb.ptr(y)
+            Lb.call("sd_sample_rows", Lb.ptr(logits), a, Lb.stream())
+            outs.append(y.cpu().tolist())
+        assert outs[-2] == outs[-1], (trunc, V, trial)
+        assert all(0 <= t < V for t in outs[-1])
