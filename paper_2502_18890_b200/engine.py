@@ -151,9 +151,10 @@ class Session:
         self.state[L.ST_PENDING] = self.tokens[-1]
         self.state[L.ST_BASE] = len(self.tokens) - 1
         self._ev = torch.cuda.Event()
-        # CUDA-graph replay on one GPU; sharded sessions (NCCL all-gathers inside
-        # the forward) run eagerly
-        self.use_graph = graph and model.world == 1
+        # CUDA-graph replay; a sharded session captures its NCCL all-gathers with
+        # the step (NCCL supports stream capture) and falls back to eager steps
+        # if the capture is refused. gloo process groups cannot be captured.
+        self.use_graph = graph and (model.world == 1 or _nccl_group(model.group))
         self._graph: torch.cuda.CUDAGraph | None = None
         self._eager_steps = 0
         if prefill:
@@ -336,9 +337,15 @@ class Session:
         if len(self.full) > base:
             self.full.truncate(base)
         self.full.reserve(self.Tmax)
-        if self.use_graph and self._eager_steps >= 1:
-            if self._graph is None:
+        if self.use_graph and self._eager_steps >= 1 and self._graph is None:
+            try:
                 self._capture()
+            except Exception as e:  # noqa: BLE001 - e.g. a collective that refuses stream capture
+                import warnings
+                warnings.warn(f"CUDA-graph capture failed ({type(e).__name__}: {e}); running eager steps")
+                torch.cuda.synchronize()
+                self.use_graph = False
+        if self.use_graph and self._graph is not None:
             self._graph.replay()
             L.launch_count += self._graph_launches
         else:
@@ -398,6 +405,11 @@ class Session:
 
     def device_error(self) -> int:
         return int(self.state[L.ST_ERROR].item())
+
+
+def _nccl_group(group) -> bool:
+    import torch.distributed as dist
+    return dist.is_initialized() and dist.get_backend(group) == "nccl"
 
 
 def prefill(model: TinyTransformer, prompt: list[int], config: EngineConfig) -> Session:
