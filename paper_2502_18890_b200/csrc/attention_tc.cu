@@ -75,13 +75,15 @@ struct Params {
 __device__ int64_t* g_tc_trace = nullptr;
 // Debug-only pipeline experiments (-DSD_TC_EXPERIMENT=n, tools/gpu_tc_exp.sh):
 // 1 = softmax skips its math, 2 = no PV MMAs, 3 = no QK MMAs, 4 = 1+2+3 (TMA stream only),
-// 5 = 4 without the softmax's TMEM loads, 6 = 5 with plain mbarrier arrives instead of commits.
+// 5 = 4 without the softmax's TMEM loads, 6 = 5 with plain mbarrier arrives instead of commits,
+// 8 = bare TMA stream inside this kernel (producers recycle their own slots; no issuer / softmax),
+// 9 = 6 without the softmax warps (the issuer does not wait for P).
 #ifndef SD_TC_EXPERIMENT
 #define SD_TC_EXPERIMENT 0
 #endif
 #define SD_TC_NOMMA (SD_TC_EXPERIMENT >= 4)
 __device__ __forceinline__ void tc_signal(uint64_t* bar) {
-#if SD_TC_EXPERIMENT == 6
+#if SD_TC_EXPERIMENT == 6 || SD_TC_EXPERIMENT == 9
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
 #else
   umma_commit(bar);
@@ -167,7 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&v_empty[s], nm);
     }
     for (int mt = 0; mt < 2; ++mt) {
-      const uint32_t arrivals = 32 * (act[mt] > 0 ? act[mt] : 1);
+      const uint32_t arrivals = act[mt] > 0 ? act[mt] : 1;  // one arrive per active softmax warp
       for (int b = 0; b < 2; ++b) {
         mbar_init(&s_full[2 * mt + b], 1);
         mbar_init(&p_full[2 * mt + b], arrivals);
@@ -239,7 +241,11 @@ __global__ void __launch_bounds__(THREADS, 1)
           pdl_wait();
           waited = true;
         }
+#if SD_TC_EXPERIMENT == 8
+        if (j >= ST) mbar_wait(&full[s], ((j / ST) + 1) & 1);
+#else
         if (j >= ST) mbar_wait(&empty[s], ((j / ST) + 1) & 1);
+#endif
         trace(0, j, is_k ? 1 : 2);
         uint8_t* d = ring + s * KV_TILE;
         mbar_expect_tx(&full[s], KV_TILE);
@@ -253,8 +259,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     // columns; the two issuers share the K/V rings (a slot is free once both
     // have committed it) and their MMAs interleave in the tensor pipe, so one
     // tile's barrier waits never stall the other's MMAs.
+    // The whole warp runs the issuer loop (lane 0 issues the MMAs and commits) so
+    // that "P(j) written" can arrive as a hardware named barrier from the softmax
+    // warpgroup instead of an mbarrier round trip.
     const int mt = warp - 1;
-    if (lane == 0 && mt < nm) {
+#if SD_TC_EXPERIMENT == 8
+    if (lane == 0 && mt < nm) mbar_arrive(&o_final[mt]);
+    if (false) {
+#else
+    if (mt < nm) {
+#endif
+      const uint32_t p_bar_count = 32u * (uint32_t)(act[mt] + 1);
       const uint32_t id_qk = idesc_bf16(BN, false);
       const uint32_t id_pv = idesc_bf16(DH, true);
       const uint32_t q_base = smem_u32(smem + OFF_Q + mt * 32768);
@@ -268,11 +283,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t half = ks >> 2, in = (ks & 3) * 32;
           const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
           const uint64_t a = umma_desc(q_base + half * 16384 + in, 16, 1024);
-          if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA)
+          if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA && lane == 0)
             umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
         }
-        tc_signal(&s_full[2 * mt + b]);
-        tc_signal(&k_empty[s]);
+        if (lane == 0) {
+          tc_signal(&s_full[2 * mt + b]);
+          tc_signal(&k_empty[s]);
+        }
+        __syncwarp();
       };
       auto wait_k = [&](int j) {
         if (mt == 0) trace(1, j, 0);
@@ -289,7 +307,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (mt == 0) trace(1, j, 3);
         mbar_wait(&v_full[s], (j / ST) & 1);
         const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
-        mbar_wait(&p_full[2 * mt + b], (j >> 1) & 1);
+#if SD_TC_EXPERIMENT != 9
+        asm volatile("bar.sync %0, %1;" ::"r"(2 + 2 * mt + b), "r"(p_bar_count) : "memory");  // P(j) written
+#endif
         if (mt == 0) trace(1, j, 4);
         tc_fence_after();
         const uint32_t p_tmem = tmem + COL_S + 128 * mt + 64 * b;  // P(j) over S(j)'s first 32 columns
@@ -297,12 +317,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int ks = 0; ks < BN / 16; ++ks) {
           // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
           const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
-          if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA)
+          if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA && lane == 0)
             umma_bf16_ts(o_col, p_tmem + 8 * ks, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
         }
-        tc_signal(&pv_done[2 * mt + b]);
-        if (j == n_tiles - 1) tc_signal(&o_final[mt]);
-        tc_signal(&v_empty[s]);
+        if (lane == 0) {
+          tc_signal(&pv_done[2 * mt + b]);
+          if (j == n_tiles - 1) tc_signal(&o_final[mt]);
+          tc_signal(&v_empty[s]);
+        }
+        __syncwarp();
         if (mt == 0) trace(1, j, 6);
         // S(j+2) into buffer b: issued after PV(j) by this thread, so it is
         // ordered after PV(j)'s reads of P(j) (same-thread tcgen05.mma order)
@@ -337,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmask[w] = bits;
       }
       float m_used = -INFINITY, l = 0.f;
-      for (int j = 0; j < n_tiles; ++j) {
+      for (int j = 0; j < (SD_TC_EXPERIMENT == 8 || SD_TC_EXPERIMENT == 9 ? 0 : n_tiles); ++j) {
         const int b = j & 1;
         const int role = (lane == 0 && wl == 0) ? 2 + mt : 99;
         if (role < 4) trace(role, j, 0);
@@ -355,7 +378,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
         if (SD_TC_EXPERIMENT == 1 || SD_TC_NOMMA) {
           tc_fence_before();
-          mbar_arrive(&p_full[2 * mt + b]);
+          asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 * mt + b), "r"(32u * (uint32_t)(act[mt] + 1)) : "memory");
           l += __uint_as_float(sr[lane]);
           continue;
         }
@@ -433,8 +456,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (role < 4) trace(role, j, 3);
         tmem_st32(s_addr, pk);  // P(j) (bf16x2) over the consumed S columns
         tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[2 * mt + b]);
+        tc_fence_before();  // P(j) in TMEM -> the issuer warp's bar.sync releases it to the MMA
+        asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 * mt + b), "r"(32u * (uint32_t)(act[mt] + 1)) : "memory");
         if (role < 4) trace(role, j, 4);
       }
       // ---- epilogue: O / l, lse (natural log) ----
