@@ -30,22 +30,25 @@ namespace tc {
 
 constexpr int BN = 64;          // keys per tile
 constexpr int DH = 128;
-#ifndef SD_TC_ST
-#define SD_TC_ST 5
-#endif
-constexpr int ST = SD_TC_ST;    // K ring depth == V ring depth
+// K and V stream in 128-key slots (one TMA pair = 2 x 16 KB per slot; one
+// full/empty barrier pair per slot) while S / P / softmax work on 64-key
+// sub-tiles: half the ring synchronisation per key of 64-key slots.
+constexpr int SLOT_KEYS = 128;
+constexpr int KST = 2;          // K ring depth (32 KB slots)
+constexpr int VST = 3;          // V ring depth (V is held until the PV of its sub-tiles)
 constexpr int THREADS = 384;
 constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 
 constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
-constexpr int KV_TILE = BN * DH * 2;            // 16 KB: [dh half][64 rows][128 B]
+constexpr int KV_SLOT = SLOT_KEYS * DH * 2;     // 32 KB: [dh half][128 rows][128 B]
+constexpr int HALF = KV_SLOT / 2;               // 16 KB: one dh half of a slot
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + Q_BYTES;
-constexpr int OFF_V = OFF_K + ST * KV_TILE;
-constexpr int OFF_BAR = OFF_V + ST * KV_TILE;
-constexpr int N_BAR = 4 * ST + 3 * 4 + 2;
+constexpr int OFF_V = OFF_K + KST * KV_SLOT;
+constexpr int OFF_BAR = OFF_V + VST * KV_SLOT;
+constexpr int N_BAR = 2 * KST + 2 * VST + 3 * 4 + 2;
 constexpr int SMEM_BYTES = OFF_BAR + N_BAR * 8 + 16;
 constexpr int SMEM_ALLOC = SMEM_BYTES + 1024;   // slack for 1024-byte alignment
 
@@ -109,10 +112,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* bars = (uint64_t*)(smem + OFF_BAR);
   uint64_t* k_full = bars;
-  uint64_t* v_full = bars + ST;
-  uint64_t* k_empty = bars + 2 * ST;
-  uint64_t* v_empty = bars + 3 * ST;
-  uint64_t* s_full = bars + 4 * ST;      // [mt][buf]: QK retired -> softmax
+  uint64_t* k_empty = k_full + KST;
+  uint64_t* v_full = k_empty + KST;
+  uint64_t* v_empty = v_full + VST;
+  uint64_t* s_full = v_empty + VST;      // [mt][buf]: QK retired -> softmax
   uint64_t* p_full = s_full + 4;         // [mt][buf]: P(j) in TMEM -> PV(j), then QK(j+2)
   uint64_t* pv_done = p_full + 4;        // [mt][buf]: PV(j) retired -> O stable (lazy rescale)
   uint64_t* o_final = pv_done + 4;       // [mt]: single phase, after the last PV
@@ -162,10 +165,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   // ---- barriers first, so the TMA producers start streaming at once ----
   if (tid == 0) {
-    for (int s = 0; s < ST; ++s) {
+    for (int s = 0; s < KST; ++s) {
       mbar_init(&k_full[s], 1);
-      mbar_init(&v_full[s], 1);
       mbar_init(&k_empty[s], nm);  // one commit per M-tile issuer
+    }
+    for (int s = 0; s < VST; ++s) {
+      mbar_init(&v_full[s], 1);
       mbar_init(&v_empty[s], nm);
     }
     for (int mt = 0; mt < 2; ++mt) {
@@ -232,25 +237,27 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint64_t* full = is_k ? k_full : v_full;
       uint64_t* empty = is_k ? k_empty : v_empty;
       uint8_t* ring = smem + (is_k ? OFF_K : OFF_V);
+      const int depth = is_k ? KST : VST;
       tma_prefetch(map);
       bool waited = false;
-      for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % ST;
-        const int key0 = key_begin + j * BN;
-        if (!waited && key0 + BN > ctx) {  // tile reaches the tree rows staged by the predecessor
+      const int n_slots = (n_tiles + 1) / 2;
+      for (int q = 0; q < n_slots; ++q) {
+        const int s = q % depth;
+        const int key0 = key_begin + q * SLOT_KEYS;
+        if (!waited && key0 + SLOT_KEYS > ctx) {  // slot reaches the tree rows staged by the predecessor
           pdl_wait();
           waited = true;
         }
 #if SD_TC_EXPERIMENT == 8
-        if (j >= ST) mbar_wait(&full[s], ((j / ST) + 1) & 1);
+        if (q >= depth) mbar_wait(&full[s], ((q / depth) + 1) & 1);
 #else
-        if (j >= ST) mbar_wait(&empty[s], ((j / ST) + 1) & 1);
+        if (q >= depth) mbar_wait(&empty[s], ((q / depth) + 1) & 1);
 #endif
-        trace(0, j, is_k ? 1 : 2);
-        uint8_t* d = ring + s * KV_TILE;
-        mbar_expect_tx(&full[s], KV_TILE);
+        trace(0, q, is_k ? 1 : 2);
+        uint8_t* d = ring + s * KV_SLOT;
+        mbar_expect_tx(&full[s], KV_SLOT);
         tma_load_4d(d, map, &full[s], 0, key0, kvh, p.layer);
-        tma_load_4d(d + KV_TILE / 2, map, &full[s], 64, key0, kvh, p.layer);
+        tma_load_4d(d + HALF, map, &full[s], 64, key0, kvh, p.layer);
       }
     }
   } else if (warp == 1 || warp == 2) {
@@ -275,26 +282,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       const uint32_t q_base = smem_u32(smem + OFF_Q + mt * 32768);
       const uint32_t o_col = tmem + COL_O + 128 * mt;
       // S[mt][j%2] = Q[mt] K(j)^T (8 K=16 steps)
+      // sub-tile j: slot j/2 of the ring, rows 64*(j%2).. of each dh half
       auto issue_qk = [&](int j) {
-        const int s = j % ST, b = j & 1;
-        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_TILE);
+        const int s = (j >> 1) % KST, b = j & 1;
+        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_SLOT) + (j & 1) * (BN * 128);
 #pragma unroll
         for (int ks = 0; ks < DH / 16; ++ks) {
           const uint32_t half = ks >> 2, in = (ks & 3) * 32;
-          const uint64_t bd = umma_desc(k_base + half * (KV_TILE / 2) + in, 16, 1024);
+          const uint64_t bd = umma_desc(k_base + half * HALF + in, 16, 1024);
           const uint64_t a = umma_desc(q_base + half * 16384 + in, 16, 1024);
           if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA && lane == 0)
             umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
         }
         if (lane == 0) {
           tc_signal(&s_full[2 * mt + b]);
-          tc_signal(&k_empty[s]);
+          if ((j & 1) || j == n_tiles - 1) tc_signal(&k_empty[s]);  // slot's last sub-tile
         }
         __syncwarp();
       };
       auto wait_k = [&](int j) {
+        if (j & 1) return;  // the odd sub-tile shares its slot with the even one
         if (mt == 0) trace(1, j, 0);
-        mbar_wait(&k_full[j % ST], (j / ST) & 1);
+        const int q = j >> 1;
+        mbar_wait(&k_full[q % KST], (q / KST) & 1);
         if (mt == 0) trace(1, j, 1);
         tc_fence_after();
       };
@@ -303,10 +313,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         issue_qk(j0);
       }
       for (int j = 0; j < n_tiles; ++j) {
-        const int s = j % ST, b = j & 1;
+        const int q = j >> 1, s = q % VST, b = j & 1;
         if (mt == 0) trace(1, j, 3);
-        mbar_wait(&v_full[s], (j / ST) & 1);
-        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_TILE);
+        if (!(j & 1)) mbar_wait(&v_full[s], (q / VST) & 1);
+        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_SLOT) + (j & 1) * (BN * 128);
 #if SD_TC_EXPERIMENT != 9
         asm volatile("bar.sync %0, %1;" ::"r"(2 + 2 * mt + b), "r"(p_bar_count) : "memory");  // P(j) written
 #endif
@@ -316,14 +326,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int ks = 0; ks < BN / 16; ++ks) {
           // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
-          const uint64_t bd = umma_desc(v_base + ks * 16 * 128, KV_TILE / 2, 1024);
+          const uint64_t bd = umma_desc(v_base + ks * 16 * 128, HALF, 1024);
           if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA && lane == 0)
             umma_bf16_ts(o_col, p_tmem + 8 * ks, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
         }
         if (lane == 0) {
           tc_signal(&pv_done[2 * mt + b]);
           if (j == n_tiles - 1) tc_signal(&o_final[mt]);
-          tc_signal(&v_empty[s]);
+          if ((j & 1) || j == n_tiles - 1) tc_signal(&v_empty[s]);
         }
         __syncwarp();
         if (mt == 0) trace(1, j, 6);
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (SD_TC_EXPERIMENT == 1 || SD_TC_NOMMA) {
           tc_fence_before();
           asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 * mt + b), "r"(32u * (uint32_t)(act[mt] + 1)) : "memory");
-          l += __uint_as_float(sr[lane]);
+          l += __uint_as_float(sr[0]) + __uint_as_float(sr[63]);  // static indices: sr stays in registers
           continue;
         }
         const int key0 = key_begin + j * BN;
@@ -531,7 +541,7 @@ int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out)
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
   cuuint64_t dims[4] = {(cuuint64_t)dh, (cuuint64_t)cap, (cuuint64_t)Hk, (cuuint64_t)L};
   cuuint64_t strides[3] = {(cuuint64_t)dh * 2, (cuuint64_t)cap * dh * 2, (cuuint64_t)Hk * cap * dh * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)tc::BN, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)tc::SLOT_KEYS, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
