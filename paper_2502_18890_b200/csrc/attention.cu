@@ -460,17 +460,38 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
   lsum = warp_sum(lsum);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const float* base = ws_o + (int64_t)row * 128 + 4 * lane;
-#pragma unroll 8
-  for (int c = 0; c < nsplit; ++c) {
-    const float w = __shfl_sync(0xffffffffu, c < 32 ? wv[0] : (c < 64 ? wv[1] : wv[2]), c & 31);
-    // unconditional load (all in flight); empty splits (never written: past a
-    // device-resident context) carry weight 0 and are dropped by the select
-    const float4 o = *reinterpret_cast<const float4*>(base + (int64_t)c * TH * 128);
-    if (w != 0.f) {
-      acc.x = fmaf(w, o.x, acc.x);
-      acc.y = fmaf(w, o.y, acc.y);
-      acc.z = fmaf(w, o.z, acc.z);
-      acc.w = fmaf(w, o.w, acc.w);
+  // only splits that hold data (empty ones — past a device-resident context —
+  // were never written), in ascending order, four partial loads in flight
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    unsigned live = __ballot_sync(0xffffffffu, lv[k] != -INFINITY);
+    while (live) {
+      int cs[4];
+      float ws4[4];
+      int n = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        cs[u] = live ? __ffs(live) - 1 : 0;
+        ws4[u] = __shfl_sync(0xffffffffu, wv[k], cs[u]);
+        if (live) {
+          live &= live - 1;
+          ++n;
+        } else {
+          ws4[u] = 0.f;
+        }
+      }
+      float4 o[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) o[u] = *reinterpret_cast<const float4*>(base + (int64_t)(32 * k + cs[u]) * TH * 128);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (u < n) {
+          acc.x = fmaf(ws4[u], o[u].x, acc.x);
+          acc.y = fmaf(ws4[u], o[u].y, acc.y);
+          acc.z = fmaf(ws4[u], o[u].z, acc.z);
+          acc.w = fmaf(ws4[u], o[u].w, acc.w);
+        }
+      }
     }
   }
   const float inv = lsum > 0.f ? 1.f / lsum : 0.f;

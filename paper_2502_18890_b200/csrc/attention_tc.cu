@@ -29,6 +29,7 @@ namespace sd {
 namespace tc {
 
 constexpr int BN = 64;          // keys per tile
+constexpr int MIN_CHUNK = 256;  // keys per split at least
 constexpr int DH = 128;
 // K and V stream in 128-key slots (one TMA pair = 2 x 16 KB per slot; one
 // full/empty barrier pair per slot) while S / P / softmax work on 64-key
@@ -137,7 +138,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (p.ctx_dev) {  // device-resident context: chunk the live length over the fixed grid
     ctx = *p.ctx_dev;
     chunk = (ctx + p.n_chunks - 1) / p.n_chunks;
-    chunk = chunk < BN ? BN : (chunk + BN - 1) / BN * BN;
+    chunk = chunk < MIN_CHUNK ? MIN_CHUNK : (chunk + BN - 1) / BN * BN;
     n_live = ctx > 0 ? (ctx + chunk - 1) / chunk : 1;
     if ((int)blockIdx.x >= n_live) {  // empty split: weight 0 in the merge
       for (int r = tid; r < ROWS; r += THREADS) {
@@ -567,9 +568,10 @@ int tc_set_trace(void* dev_ptr, int force_chunks) {
 
 int tc_n_chunks(int ctx, int Hk) {
   if (g_force_chunks > 0) return g_force_chunks;
-  // one wave of one CTA per SM over (chunks x kv heads); >= one tile per chunk
+  // one wave of one CTA per SM over (chunks x kv heads); >= MIN_CHUNK keys per
+  // chunk (short chunks cost more in the split merge than they save)
   int want = 148 / Hk;
-  const int max_by_tiles = (ctx + tc::BN - 1) / tc::BN;
+  const int max_by_tiles = (ctx + tc::MIN_CHUNK - 1) / tc::MIN_CHUNK;
   if (want > max_by_tiles) want = max_by_tiles;
   if (want > 148) want = 148;
   return want < 1 ? 1 : want;

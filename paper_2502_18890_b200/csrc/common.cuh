@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "swiftdec_b200.h"
 
@@ -75,6 +76,16 @@ __device__ __forceinline__ T block_reduce(T v, T* scratch, Op op) {
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// SD_NO_PDL=1 (profiling only): plain stream-ordered launches, so per-kernel
+// durations are not inflated by early-launched kernels waiting on their inputs.
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SD_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                        Args... args) {
@@ -87,7 +98,7 @@ inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
