@@ -766,7 +766,11 @@ static int dispatch_decode(const AttnParams& p, int q_dtype, int kv_dtype, int o
 // warp in flight. Chunk partials are merged by the LAST CTA of each kv head to
 // finish (arrival counter in the zeroed workspace head, reset after use), in
 // fixed chunk order — one launch, deterministic, no separate merge kernel.
-constexpr int DR_WARPS = 8, DR_CHUNK = DR_WARPS * 16, DR_MAX_CHUNKS = 96;
+#ifndef SD_DR_KPW
+#define SD_DR_KPW 16
+#endif
+constexpr int DR_KPW = SD_DR_KPW;  // keys per warp: one batch of loads in flight per warp
+constexpr int DR_WARPS = 8, DR_CHUNK = DR_WARPS * DR_KPW, DR_MAX_CHUNKS = 96;
 
 template <typename KT, int GM>
 __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* __restrict__ counters,
@@ -779,11 +783,11 @@ __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* _
   const int kvh = blockIdx.y, G = p.G, nc = gridDim.x, cx = blockIdx.x;
   const KT* K = (const KT*)p.k_cache + kvh * p.head_stride;
   const KT* V = (const KT*)p.v_cache + kvh * p.head_stride;
-  const int w0 = cx * DR_CHUNK + warp * 16, w1 = min(p.ctx, w0 + 16);
+  const int w0 = cx * DR_CHUNK + warp * DR_KPW, w1 = min(p.ctx, w0 + DR_KPW);
   pdl_trigger();
   pdl_wait();  // q and the pending row come from the kernel before
   int my_rank = -1;
-  if (lane < 16 && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
+  if (lane < DR_KPW && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
   float q[GM][4];
 #pragma unroll
   for (int g = 0; g < GM; ++g) {
@@ -825,7 +829,7 @@ __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* _
   };
   // two batches of 8 keys: every load of a batch issued before any math
 #pragma unroll
-  for (int b0 = 0; b0 < 16; b0 += NB) {
+  for (int b0 = 0; b0 < DR_KPW; b0 += NB) {
     V4 kv[NB], vv[NB];
     float2 cs[NB][2];
     bool ok[NB];
