@@ -429,6 +429,11 @@ template <> __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16*
 // exp(lse_c - max) are recomputed per lane from a broadcast lse load, so every
 // split's partial is an independent float4 load (all in flight) and the merge is
 // a single L2 round trip; splits are accumulated in ascending order.
+#ifndef SD_MERGE_U
+#define SD_MERGE_U 8
+#endif
+constexpr int MU = SD_MERGE_U;  // split partials in flight per warp
+
 template <typename OT>
 __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
                                                        int nsplit, int TH, int H, const int32_t* __restrict__ rows_dev,
@@ -461,16 +466,16 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   const float* base = ws_o + (int64_t)row * 128 + 4 * lane;
   // only splits that hold data (empty ones — past a device-resident context —
-  // were never written), in ascending order, four partial loads in flight
+  // were never written), in ascending order, MU partial loads in flight
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
     unsigned live = __ballot_sync(0xffffffffu, lv[k] != -INFINITY);
     while (live) {
-      int cs[4];
-      float ws4[4];
+      int cs[MU];
+      float ws4[MU];
       int n = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < MU; ++u) {
         cs[u] = live ? __ffs(live) - 1 : 0;
         ws4[u] = __shfl_sync(0xffffffffu, wv[k], cs[u]);
         if (live) {
@@ -480,11 +485,11 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
           ws4[u] = 0.f;
         }
       }
-      float4 o[4];
+      float4 o[MU];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) o[u] = *reinterpret_cast<const float4*>(base + (int64_t)(32 * k + cs[u]) * TH * 128);
+      for (int u = 0; u < MU; ++u) o[u] = *reinterpret_cast<const float4*>(base + (int64_t)(32 * k + cs[u]) * TH * 128);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < MU; ++u) {
         if (u < n) {
           acc.x = fmaf(ws4[u], o[u].x, acc.x);
           acc.y = fmaf(ws4[u], o[u].y, acc.y);

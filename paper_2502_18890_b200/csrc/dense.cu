@@ -113,6 +113,25 @@ __global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[base + i] = from_f<XT>(h[base + i] * (gain[i] * inv));
 }
 
+// 4 elements per thread: one 16-byte load, one 8-byte (bf16) / 16-byte (fp32) store
+template <typename OT>
+__global__ void silu4_kernel(const float4* __restrict__ a, OT* __restrict__ out, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldcs(a + i);
+    const float r0 = v.x / (1.f + __expf(-v.x)), r1 = v.y / (1.f + __expf(-v.y));
+    const float r2 = v.z / (1.f + __expf(-v.z)), r3 = v.w / (1.f + __expf(-v.w));
+    if constexpr (sizeof(OT) == 2) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(r0, r1), hi = __floats2bfloat162_rn(r2, r3);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(out)[i] = pk;
+    } else {
+      reinterpret_cast<float4*>(out)[i] = make_float4(r0, r1, r2, r3);
+    }
+  }
+}
+
 template <typename OT>
 __global__ void silu_kernel(const float* __restrict__ a, OT* __restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -258,7 +277,12 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
 
 int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stream) {
   auto st = as_stream(stream);
-  if (out_dtype == SD_BF16)
+  const bool vec = n % 4 == 0 && ((uintptr_t)a % 16) == 0 && ((uintptr_t)out % 16) == 0;
+  if (vec && out_dtype == SD_BF16)
+    silu4_kernel<<<grid_for(n / 4), 256, 0, st>>>((const float4*)a, (__nv_bfloat16*)out, n / 4);
+  else if (vec && out_dtype == SD_F32)
+    silu4_kernel<<<grid_for(n / 4), 256, 0, st>>>((const float4*)a, (float*)out, n / 4);
+  else if (out_dtype == SD_BF16)
     silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (__nv_bfloat16*)out, n);
   else if (out_dtype == SD_F32)
     silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (float*)out, n);

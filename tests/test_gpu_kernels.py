@@ -678,8 +678,16 @@ def test_norm_and_rope_sum_split_slices(lib, S):
         assert torch.equal(a, b)
 
 
-@pytest.mark.parametrize("K,N", [(4096, 6144), (4096, 4096), (4096, 16384), (16384, 4096), (256, 512), (64, 40)])
-def test_gemv_vs_fp32_reference(lib, K, N):
+@pytest.fixture(params=["ld", "tma"])
+def gemv_impl(request, monkeypatch):
+    """Both weight-streaming implementations: per-lane 16-byte loads, TMA ring."""
+    monkeypatch.setenv("SD_GEMV_IMPL", request.param)
+    return request.param
+
+
+@pytest.mark.parametrize("K,N", [(4096, 6144), (4096, 4096), (4096, 16384), (16384, 4096), (256, 512), (64, 40),
+                                 (100, 8), (4096, 128256 // 16)])
+def test_gemv_vs_fp32_reference(lib, K, N, gemv_impl):
     """Single-row weight streaming (draft forward projections, model.py:283-309):
     fp32 out and fused SiLU -> bf16; deterministic split-K reduction; the
     counter head is left zeroed so back-to-back calls (graph replays) work."""
@@ -704,7 +712,7 @@ def test_gemv_vs_fp32_reference(lib, K, N):
     torch.testing.assert_close(ysil.float(), torch.nn.functional.silu(want), rtol=1e-2, atol=1e-2)
 
 
-def test_gemv_shared_workspace_across_shapes(lib):
+def test_gemv_shared_workspace_across_shapes(lib, gemv_impl):
     """One zeroed workspace serves every shape (the model shares it across
     layers): a narrow split call's partials must not land in a wider call's
     arrival counters (cfg5: w2 [20480, 5120] then w1 [5120, 20480])."""

@@ -1,6 +1,7 @@
 """sd_gemm (tcgen05 weight-streaming) vs cuBLAS on the decode shapes; weights
 rotate over copies larger than L2."""
 import ctypes
+import os
 import sys
 
 import torch
@@ -10,7 +11,7 @@ from paper_2502_18890_b200 import _lib as L  # noqa: E402
 
 shapes = {"qkv": (4096, 6144), "wo": (4096, 4096), "w1": (4096, 16384), "w2": (16384, 4096)}
 dev = "cuda"
-for M in (1, 101):
+for M in [int(m) for m in os.environ.get("GEMM_MS", "1,101").split(",")]:
     for name, (K, N) in shapes.items():
         copies = max(2, int(600e6 // (K * N * 2)))
         Ws = [(torch.randn(K, N, device=dev) * 0.02).to(torch.bfloat16) for _ in range(copies)]
@@ -51,6 +52,8 @@ for M in (1, 101):
         print(f"M={M:3d} {name:4s}: " + " | ".join(out), flush=True)
 
 # single-row weight streaming (sd_gemv) vs cuBLAS
+if os.environ.get("GEMM_NO_GEMV"):
+    sys.exit(0)
 for name, (K, N) in list(shapes.items()) + [("head", (4096, 4096))]:
     copies = max(2, int(600e6 // (K * N * 2)))
     Ws = [(torch.randn(K, N, device=dev) * 0.02).to(torch.bfloat16) for _ in range(copies)]
