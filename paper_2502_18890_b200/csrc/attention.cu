@@ -778,7 +778,7 @@ constexpr int DR_KPW = SD_DR_KPW;  // keys per warp: one batch of loads in fligh
 constexpr int DR_WARPS = 8, DR_CHUNK = DR_WARPS * DR_KPW, DR_MAX_CHUNKS = 96;
 
 template <typename KT, int GM>
-__global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* __restrict__ counters,
+__global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnParams p, int* __restrict__ counters,
                                                             __nv_bfloat16* __restrict__ out) {
   using V4 = typename Vec4<KT>::T;
   constexpr int DH = 128, NB = 8;
@@ -790,9 +790,31 @@ __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* _
   const KT* V = (const KT*)p.v_cache + kvh * p.head_stride;
   const int w0 = cx * DR_CHUNK + warp * DR_KPW, w1 = min(p.ctx, w0 + DR_KPW);
   pdl_trigger();
-  pdl_wait();  // q and the pending row come from the kernel before
+  // the partial cache (slots, ranks) is written only by launches that do not
+  // trigger dependents early (admit / evict / gather), so the first batch of key
+  // loads is issued before waiting on the kernel before (which writes q and the
+  // pending row)
   int my_rank = -1;
   if (lane < DR_KPW && w0 + lane < w1) my_rank = p.ranks[w0 + lane];
+  V4 kv[NB], vv[NB];
+  float2 cs[NB][2];
+  bool ok[NB];
+  auto load_batch = [&](int b0) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int k = w0 + b0 + b;
+      const int rk = __shfl_sync(0xffffffffu, my_rank, b0 + b);
+      ok[b] = k < w1 && rk >= 0;
+      const int kk = ok[b] ? k : 0;  // in-bounds address for masked keys
+      kv[b] = *reinterpret_cast<const V4*>(K + (int64_t)kk * DH + lane * 4);
+      vv[b] = *reinterpret_cast<const V4*>(V + (int64_t)kk * DH + lane * 4);
+      const int64_t r = rk > 0 ? rk : 0;
+      cs[b][0] = *reinterpret_cast<const float2*>(p.cosT + r * (DH / 2) + lane * 2);
+      cs[b][1] = *reinterpret_cast<const float2*>(p.sinT + r * (DH / 2) + lane * 2);
+    }
+  };
+  load_batch(0);
+  pdl_wait();  // q and the pending row come from the kernel before
   float q[GM][4];
 #pragma unroll
   for (int g = 0; g < GM; ++g) {
@@ -832,36 +854,78 @@ __global__ void __launch_bounds__(256, 2) draft_attn_kernel(AttnParams p, int* _
       }
     }
   };
-  // two batches of 8 keys: every load of a batch issued before any math
+  // batches of 8 keys: every load of a batch issued before any math. The
+  // KG x GM partial dots of a key group (32 values per lane) are summed across
+  // the warp by a butterfly reduce-scatter (31 shuffles; lane j ends with the
+  // full dot of key j / GM, head j % GM), then one online-softmax update per
+  // head covers the whole group: one exp per lane instead of one per key & head.
+  constexpr int KG = 32 / GM;  // keys per reduction group
+  const int my_g = lane % GM, my_b = lane / GM;
 #pragma unroll
   for (int b0 = 0; b0 < DR_KPW; b0 += NB) {
-    V4 kv[NB], vv[NB];
-    float2 cs[NB][2];
-    bool ok[NB];
+    if (b0 > 0) load_batch(b0);
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int k = w0 + b0 + b;
-      const int rk = __shfl_sync(0xffffffffu, my_rank, b0 + b);
-      ok[b] = k < w1 && rk >= 0;
-      const int kk = ok[b] ? k : 0;  // in-bounds address for masked keys
-      kv[b] = *reinterpret_cast<const V4*>(K + (int64_t)kk * DH + lane * 4);
-      vv[b] = *reinterpret_cast<const V4*>(V + (int64_t)kk * DH + lane * 4);
-      const int64_t r = rk > 0 ? rk : 0;
-      cs[b][0] = *reinterpret_cast<const float2*>(p.cosT + r * (DH / 2) + lane * 2);
-      cs[b][1] = *reinterpret_cast<const float2*>(p.sinT + r * (DH / 2) + lane * 2);
-    }
+    for (int g0 = 0; g0 < NB; g0 += KG) {
+      float d[32];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      if (!ok[b]) continue;  // warp-uniform
-      float kf[4], vf[4];
-      Vec4<KT>::unpack(kv[b], kf);
-      Vec4<KT>::unpack(vv[b], vf);
-      const float a0 = kf[0], c0 = kf[1], a1 = kf[2], c1 = kf[3];  // pairs (0,1), (2,3) of this lane
-      kf[0] = a0 * cs[b][0].x - c0 * cs[b][1].x;
-      kf[1] = a0 * cs[b][1].x + c0 * cs[b][0].x;
-      kf[2] = a1 * cs[b][0].y - c1 * cs[b][1].y;
-      kf[3] = a1 * cs[b][1].y + c1 * cs[b][0].y;
-      update(kf, vf);
+      for (int b = 0; b < KG; ++b) {
+        float kf[4];
+        Vec4<KT>::unpack(kv[g0 + b], kf);
+        const float a0 = kf[0], c0 = kf[1], a1 = kf[2], c1 = kf[3];  // pairs (0,1), (2,3) of this lane
+        const float2 cc = cs[g0 + b][0], sn = cs[g0 + b][1];
+        const float r0 = a0 * cc.x - c0 * sn.x, r1 = a0 * sn.x + c0 * cc.x;
+        const float r2 = a1 * cc.y - c1 * sn.y, r3 = a1 * sn.y + c1 * cc.y;
+#pragma unroll
+        for (int g = 0; g < GM; ++g) d[b * GM + g] = fmaf(q[g][0], r0, fmaf(q[g][1], r1, fmaf(q[g][2], r2, q[g][3] * r3)));
+      }
+#pragma unroll
+      for (int c = 16; c >= 1; c >>= 1) {  // reduce-scatter: keep the half named by lane bit c
+        const bool up = lane & c;
+#pragma unroll
+        for (int i = 0; i < c; ++i) {
+          const float send = up ? d[i] : d[i + c];
+          const float keep = up ? d[i + c] : d[i];
+          d[i] = keep + __shfl_xor_sync(0xffffffffu, send, c);
+        }
+      }
+      bool okb = false;
+#pragma unroll
+      for (int b = 0; b < KG; ++b) okb = my_b == b ? ok[g0 + b] : okb;
+      const float sc = okb && my_g < G ? d[0] : -INFINITY;
+      float bm = sc;  // group max per head: lanes of equal lane % GM
+#pragma unroll
+      for (int o = GM; o < 32; o <<= 1) bm = fmaxf(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+      float mo = m[0];
+#pragma unroll
+      for (int g = 1; g < GM; ++g) mo = my_g == g ? m[g] : mo;
+      const float mn = fmaxf(mo, bm);
+      const float pw = sc == -INFINITY ? 0.f : __expf(sc - mn);
+      float ps = pw;
+#pragma unroll
+      for (int o = GM; o < 32; o <<= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+      float corr[GM];
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+        const float mg = __shfl_sync(0xffffffffu, mn, g);
+        const float sg = __shfl_sync(0xffffffffu, ps, g);
+        corr[g] = m[g] == -INFINITY ? 0.f : __expf(m[g] - mg);
+        l[g] = l[g] * corr[g] + sg;
+        m[g] = mg;
+      }
+      float vf[KG][4];
+#pragma unroll
+      for (int b = 0; b < KG; ++b) Vec4<KT>::unpack(vv[g0 + b], vf[b]);
+#pragma unroll
+      for (int g = 0; g < GM; ++g) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[g][e] *= corr[g];
+#pragma unroll
+        for (int b = 0; b < KG; ++b) {
+          const float pb = __shfl_sync(0xffffffffu, pw, b * GM + g);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[g][e] = fmaf(pb, vf[b][e], acc[g][e]);
+        }
+      }
     }
   }
   if (cx == nc - 1 && warp == DR_WARPS - 1) {  // the pending token's own row (always visible)

@@ -212,7 +212,8 @@ def test_attention_rows_dev_padding(lib):
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("H,Hk,dh,cap,hi", [(8, 2, 32, 300, 260), (32, 8, 128, 4200, 4100), (40, 8, 128, 700, 650),
-                                            (16, 16, 64, 300, 290)])
+                                            (16, 16, 64, 300, 290), (12, 2, 128, 2100, 2050), (16, 8, 128, 300, 290),
+                                            (24, 8, 128, 130, 5)])
 def test_draft_attention_rank_rope_with_holes(lib, dtype, H, Hk, dh, cap, hi):
     dev = torch.device("cuda")
     g = np.random.default_rng(11)
