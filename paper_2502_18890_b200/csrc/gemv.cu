@@ -368,13 +368,19 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
   SD_REQUIRE((size_t)blocks * sizeof(int) <= gv::WS_HEAD, "sd_gemv: N=%d too wide for the counter head", N);
   const int s_tma = gv::tma_splits(K, N);
   const size_t smem_tma = (size_t)gv::NS * gv::STAGE_BYTES + ((K + s_tma - 1) / s_tma + 1) * sizeof(float);
-  if (gv::use_tma() && smem_tma <= 220 * 1024) {  // else: the register-streaming kernel below
+  if (gv::use_tma() && smem_tma <= 212 * 1024) {  // else: the register-streaming kernel below
     const int s = s_tma;
     const size_t smem = smem_tma;
     SD_REQUIRE(s == 1 || (workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N)), "sd_gemv: workspace");
     CUtensorMap m;
     if (gv::weight_map(w, K, N, &m)) return SD_ECUDA;
-    cudaFuncSetAttribute(gv::gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    // the attribute only grows: graph nodes captured with a larger size must still
+    // launch after a smaller shape was captured (kernel replay re-checks it)
+    static size_t attr = 0;
+    if (smem > attr) {
+      cudaFuncSetAttribute(gv::gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
     launch_pdl(gv::gemv_tma_kernel, dim3(blocks, s), dim3((gv::WARPS + 1) * 32), smem, as_stream(stream), m,
                (const __nv_bfloat16*)x, K, N, s, epi, y, s > 1 ? (float*)((char*)workspace + gv::WS_HEAD) : nullptr,
                (int*)workspace);
@@ -386,7 +392,11 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
   const int kslice = (K + s - 1) / s + 1;
   const size_t smem = (size_t)kslice * sizeof(float);
   SD_REQUIRE(smem <= 200 * 1024, "sd_gemv: K slice too long");
-  if (smem > 48 * 1024) cudaFuncSetAttribute(gv::gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t attr = 48 * 1024;  // only grows (see above)
+  if (smem > attr) {
+    cudaFuncSetAttribute(gv::gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
   launch_pdl(gv::gemv_kernel, dim3(blocks, s), dim3(gv::WARPS * 32), smem, as_stream(stream),
              (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, K, N, s, epi, y,
              s > 1 ? (float*)((char*)workspace + head) : nullptr, (int*)workspace);

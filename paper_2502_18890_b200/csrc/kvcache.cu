@@ -363,7 +363,11 @@ int sd_select_topk(const float* scores, int L, int n_cand, int sink, int take, i
   int N = 1;
   while (N < take) N <<= 1;
   const size_t smem = (size_t)N * 8;
-  cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t attr = 0;  // only grows: earlier captured launches keep fitting
+  if (smem > attr) {
+    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
   select_kernel<<<L, SEL_THREADS, smem, as_stream(stream)>>>(scores, n_cand, sink, take, ppos, prank, pscore,
                                                              slot_cap, (int32_t*)workspace);
   return check_launch("sd_select_topk");

@@ -11,6 +11,6 @@ python tools/launch_summary.py gpurun_out/launches.csv 2 30 > gpurun_out/launch_
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:verify_attn_tc -s 3 -c 1 \
   -o gpurun_out/prof_verify_tc -f python tools/time_tc.py > gpurun_out/prof_verify_tc.log 2>&1; echo "prof tc rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k regex:"draft_attn|gemv_kernel|sample_rows_cluster|merge128" -s 200 -c 6 \
+  -k regex:"draft_attn|gemv_tma|sample_rows_cluster|merge128" -s 200 -c 6 \
   -o gpurun_out/prof_chain -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --attn-reps 1 \
   > gpurun_out/prof_chain.log 2>&1; echo "prof chain rc=$?"
