@@ -106,11 +106,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the weights never depend on the kernel before,
+  // so the W stream starts at once; X loads and every global store wait for it
+  pdl_trigger();
 
   if (warp == 0 || warp == 6) {
     if (lane == 0) {  // ---- TMA producers: W (warp 0, deep ring) and X (warp 6), continuous across items ----
       const bool is_w = warp == 0;
       tma_prefetch(is_w ? &tmap_w : &tmap_x);
+      if (!is_w) pdl_wait();
       const int depth = is_w ? p.wst : p.xst;
       uint8_t* x_ring = smem;
       uint8_t* w_ring = smem + p.xst * p.x_slot;
@@ -165,6 +169,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
   } else if (warp >= 2 && warp <= 5) {
+    pdl_wait();  // y / partials / counters may still be in use by the kernel before
     // ---- epilogue: TMEM -> registers -> split slice (fp32) | silu (bf16) ----
     const int quarter = warp & 3;
     const int row = 32 * quarter + lane;
@@ -390,7 +395,7 @@ int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi
   p.ws = need ? (float*)((char*)workspace + 4096) : nullptr;
   const int items = (N / gm::BN) * p.splits;
   dim3 grid(items < 148 ? items : 148);
-  gm::gemm_stream_kernel<<<grid, gm::THREADS, gm::SMEM_ALLOC, as_stream(stream)>>>(mx, mw, p);
+  launch_pdl(gm::gemm_stream_kernel, grid, dim3(gm::THREADS), gm::SMEM_ALLOC, as_stream(stream), mx, mw, p);
   return check_launch("sd_gemm");
 }
 

@@ -21,9 +21,11 @@ O projection (parallel.py).
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
+
 import torch
 
 from . import _lib as L
@@ -259,6 +261,10 @@ class TinyTransformer:
         if not hasattr(self, "heads"):
             self.heads = []
         self._gemm_ws = None
+        keys = os.environ.get("SD_GEMM_KEYS")  # tuning switch: comma list of projections for sd_gemm
+        if keys is not None:
+            self.use_gemm = bool(keys)
+            self.gemm_keys = tuple(k for k in keys.split(",") if k)
         if dt == torch.bfloat16 and self.use_gemm:
             self._make_gemm_maps()
         self._gemv_ws = None
@@ -273,10 +279,12 @@ class TinyTransformer:
         torch.cuda.empty_cache()
 
     # Weight-streaming tcgen05 GEMM (sd_gemm) for the decode rows. Off by
-    # default: on the cfg3 shapes it measures 0.7-1.5x cuBLAS (its activation
-    # loads queue behind the weight stream in the SM's TMA unit; see DESIGN.md
-    # §7), so the product path keeps cuBLAS for the dense layers.
+    # default: routed per projection (SD_GEMM_KEYS=wqkv,wo,...) the cfg3 step
+    # is slower than with cuBLAS for every subset (8.78 ms with none, 8.95 with
+    # wqkv, 9.24 with wqkv+wo, 9.88 with all; profiles/r01_gemm_keys_sweep.log),
+    # so the product path keeps cuBLAS for the verify forward's dense layers.
     use_gemm = False
+    gemm_keys = ("wqkv", "wo", "w1", "w2")
 
     def _make_gemm_maps(self):
         """N-tiled copies [N/128][K][128] of the layer weights for sd_gemm (the
@@ -284,7 +292,7 @@ class TinyTransformer:
         import ctypes
         need = 0
         for ly in self.layers:
-            for key in ("wqkv", "wo", "w1", "w2"):
+            for key in self.gemm_keys:
                 K, N = ly[key].shape
                 if K % 64 or N % 128:
                     continue

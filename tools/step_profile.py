@@ -26,7 +26,7 @@ ctx = args.ctx or c["prefix"] + c["gen"] // 2
 mcfg = sd.ModelConfig(vocab_size=c["V"], num_layers=c["L"], hidden_dim=c["d"], num_heads=c["H"], num_kv_heads=c["Hk"],
                       gamma=3, max_positions=c["prefix"] + c["gen"] + 256, init_seed=0)
 model = sd.TinyTransformer(mcfg, dtype=torch.bfloat16, init="device")
-model.use_gemm = os.environ.get("SD_NO_GEMM") is None
+
 ecfg = sd.EngineConfig(target_length=c["gen"], sink_size=c["S"], budget=c["B"], tree=sd.TreeConfig((1, 3, 3, 3)), k=20,
                        sampler=sd.SamplerConfig(theta=c["theta"], window=1024, truncation=sd.Truncation(*c["trunc"])))
 sess = sd.Session(model, sd.rng.random_prompt(c["prefix"], c["V"]), ecfg, capacity=c["prefix"] + c["gen"] + 512,
