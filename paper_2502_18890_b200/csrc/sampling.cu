@@ -65,6 +65,32 @@ __device__ __forceinline__ bool is_member(const SampleDev& a, const RowCtx& rc, 
   }
 }
 
+// is_member split in two: the per-element word (loaded in batches, so a thread
+// keeps several global loads in flight) and the decision from it
+__device__ __forceinline__ int member_word(const SampleDev& a, int row, int v) {
+  switch (a.member_kind) {
+    case SD_MEMBER_MASK: return a.member_mask[(int64_t)row * a.V + v];
+    case SD_MEMBER_WINDOW:
+    case SD_MEMBER_TREE: return a.window > 0 ? a.win_count[v] : 0;
+    default: return 0;
+  }
+}
+__device__ __forceinline__ bool member_from(const SampleDev& a, const RowCtx& rc, int v, int word) {
+  switch (a.member_kind) {
+    case SD_MEMBER_MASK: return word != 0;
+    case SD_MEMBER_WINDOW: return a.window > 0 && word > 0;
+    case SD_MEMBER_TREE: {
+      if (a.window <= 0) return false;
+      bool m = word > 0;
+      if ((rc.bloom[(v >> 5) & 31] >> (v & 31)) & 1u)
+        for (int i = 0; i < rc.n_patch; ++i)
+          if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
+      return m;
+    }
+    default: return false;
+  }
+}
+
 template <int IN>
 __device__ __forceinline__ double load_in(const void* in, int64_t idx) {
   if (IN == SD_IN_LOGITS_F32) return (double)((const float*)in)[idx];
@@ -465,6 +491,9 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
   const int rank = (int)cluster.block_rank();
   const int row = blockIdx.x / SC_CTAS, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool live = row < a.rows && !(a.member_kind == SD_MEMBER_TREE && row >= a.tree[tree_off::T]);
+  // a padded row's whole cluster leaves before any cluster barrier or DSMEM access
+  // (every CTA of the cluster sees the same row and the same tree size)
+  if (!live) return;
   const int V = a.V;
   const int v0 = (int)((int64_t)V * rank / SC_CTAS), v1 = (int)((int64_t)V * (rank + 1) / SC_CTAS);
   const float* lg = logits + (int64_t)row * V;
@@ -472,23 +501,37 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
   __syncthreads();
   const float inv_t = (float)(1.0 / a.temperature), inv_tt = (float)(1.0 / (a.temperature * a.theta));
   const float th = (float)a.theta;
-  auto scaled_f = [&](int v) -> float {
-    const float l = lg[v];
-    if (!is_member(a, rc, row, v)) return l * inv_t;
+  // ---- 1. online max / sum-exp over this CTA's slice; the scaled logits are kept
+  // in ecache (shared memory) so pass 2 never touches global memory ----
+  auto scaled_w = [&](float l, int v, int word) -> float {
+    if (!member_from(a, rc, v, word)) return l * inv_t;
     if (a.ctrl_style) return (l < 0.f ? l * th : l / th) * inv_t;
     return l * inv_tt;
   };
-  // ---- 1. online max / sum-exp over this CTA's slice ----
   float lm = -INFINITY;
   double lz = 0.0;
-  if (live) {
-    for (int v = v0 + tid; v < v1; v += SC_THREADS) {
-      const float sv = scaled_f(v);
-      if (sv > lm) {
-        lz = lz * (double)expf(lm - sv);
-        lm = sv;
+  constexpr int UB = 4;  // elements per thread per batch: all their loads issued first
+  for (int vb = v0 + tid; vb < v1; vb += SC_THREADS * UB) {
+    float lv[UB];
+    int wv[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int v = vb + u * SC_THREADS;
+      lv[u] = v < v1 ? lg[v] : 0.f;
+      wv[u] = v < v1 ? member_word(a, row, v) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int v = vb + u * SC_THREADS;
+      if (v < v1) {
+        const float sv = scaled_w(lv[u], v, wv[u]);
+        ecache[v - v0] = sv;
+        if (sv > lm) {
+          lz = lz * (double)expf(lm - sv);
+          lm = sv;
+        }
+        lz += (double)expf(sv - lm);
       }
-      lz += (double)expf(sv - lm);
     }
   }
   const float cm = block_reduce(lm, fred, [](float x, float y) { return fmaxf(x, y); });
@@ -512,8 +555,7 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
   constexpr int NW = SC_THREADS / 32;
   const int S = ((v1 - v0) + NW * 32 - 1) / (NW * 32) * 32;
   const int c0 = v0 + wid * S, c1 = min(v1, c0 + S);
-  if (live)
-    for (int v = v0 + tid; v < v1; v += SC_THREADS) ecache[v - v0] = expf(scaled_f(v) - mf);
+  for (int i = tid; i < v1 - v0; i += SC_THREADS) ecache[i] = expf(ecache[i] - mf);  // same thread wrote i
   __syncthreads();
   auto ebits = [&](int v) -> int { return __float_as_int(ecache[v - v0]); };
   auto prob = [&](int v) -> double { return (double)ecache[v - v0] * invZ; };
@@ -716,23 +758,32 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
   }
 }
 
-// draft per-head top-w (engine.py:207-215): one CTA per head, one pass over
-// the vocabulary. Candidates are ranked by the penalised scaled logit s
-// (exp(s - m) / Z is monotone in s), ties to the lower id. Each thread keeps a
-// sorted top-W list; W rounds of block argmax then pick the head's top-w.
+// draft per-head top-w (engine.py:207-215): a cluster of TW_CTAS CTAs per head,
+// each CTA owning a contiguous 1/TW_CTAS of the vocabulary. Candidates are ranked
+// by the penalised scaled logit s (exp(s - m) / Z is monotone in s), ties to the
+// lower id. Each thread keeps a sorted top-W list; W rounds of block argmax give
+// the CTA's top-W; cluster rank 0 reads every CTA's list through distributed
+// shared memory and picks the head's top-w with the same order (slices ascend,
+// so "lower id" stays exact across CTAs).
+constexpr int TW_CTAS = 8, TW_THREADS = 512;
+
 template <int W>
-__global__ void __launch_bounds__(SMP_THREADS) draft_topw_kernel(const float* __restrict__ logits, int V,
-                                                                 const int32_t* __restrict__ cnt, double t,
-                                                                 double theta, int ctrl, int w0, int w1, int w2,
-                                                                 int w3, int w4, int w5, int w6, int w7,
-                                                                 int32_t* __restrict__ out) {
+__global__ void __cluster_dims__(TW_CTAS, 1, 1) __launch_bounds__(TW_THREADS)
+    draft_topw_kernel(const float* __restrict__ logits, int V, const int32_t* __restrict__ cnt, double t,
+                      double theta, int ctrl, int w0, int w1, int w2, int w3, int w4, int w5, int w6, int w7,
+                      int32_t* __restrict__ out) {
   __shared__ DI ared[32];
-  const int head = blockIdx.x, tid = threadIdx.x;
+  __shared__ DI cand[W];  // this CTA's top-W, best first
+  __shared__ DI all[TW_CTAS * W];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int head = blockIdx.x / TW_CTAS, tid = threadIdx.x;
   const int ws[8] = {w0, w1, w2, w3, w4, w5, w6, w7};
   int off = 0;
   for (int k = 0; k < head; ++k) off += ws[k];
   const int w = ws[head];
   const float* row = logits + (int64_t)head * V;
+  const int v0 = (int)((int64_t)V * rank / TW_CTAS), v1 = (int)((int64_t)V * (rank + 1) / TW_CTAS);
   const double inv_t = 1.0 / t, inv_tt = 1.0 / (t * theta);
   double bv[W];
   int bi[W];
@@ -741,7 +792,7 @@ __global__ void __launch_bounds__(SMP_THREADS) draft_topw_kernel(const float* __
     bv[k] = -INFINITY;
     bi[k] = 0x7fffffff;
   }
-  for (int v = tid; v < V; v += SMP_THREADS) {
+  for (int v = v0 + tid; v < v1; v += TW_THREADS) {
     const double l = (double)row[v];
     const bool mem = cnt != nullptr && cnt[v] > 0;
     double sv;
@@ -773,8 +824,45 @@ __global__ void __launch_bounds__(SMP_THREADS) draft_topw_kernel(const float* __
       if (k == head_pos) mine = DI{bv[k], bi[k]};
     const DI best = block_argmax(mine, ared);
     if (best.i == mine.i && best.v == mine.v) ++head_pos;
-    if (tid == 0) out[off + j] = best.i;
+    if (tid == 0) cand[j] = best;
   }
+  cluster.sync();
+  if (rank == 0 && tid < 32) {
+    // gather the cluster's lists, then w rounds of warp argmax over them
+    for (int e = tid; e < TW_CTAS * W; e += 32) {
+      const int r = e / W, j = e - r * W;
+      all[e] = j < w ? cluster.map_shared_rank(cand, r)[j] : DI{-INFINITY, 0x7fffffff};
+    }
+    __syncwarp();
+    for (int j = 0; j < w; ++j) {
+      DI b{-INFINITY, 0x7fffffff};
+      int be = -1;
+      for (int e = tid; e < TW_CTAS * W; e += 32) {
+        const DI c = all[e];
+        if (c.i != 0x7fffffff || c.v != -INFINITY) {
+          const DI nb = better(b, c);
+          if (nb.i != b.i || nb.v != b.v) be = e;
+          b = nb;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        DI y;
+        y.v = __shfl_xor_sync(0xffffffffu, b.v, o);
+        y.i = __shfl_xor_sync(0xffffffffu, b.i, o);
+        const int ye = __shfl_xor_sync(0xffffffffu, be, o);
+        const DI nb = better(b, y);
+        if (nb.i != b.i || nb.v != b.v) be = ye;
+        b = nb;
+      }
+      if (tid == 0) {
+        out[off + j] = b.i;
+        if (be >= 0) all[be] = DI{-INFINITY, 0x7fffffff};  // taken
+      }
+      __syncwarp();
+    }
+  }
+  cluster.sync();  // peers' lists stay alive until rank 0 has read them
 }
 
 static SampleDev to_dev(const sd_sample_args& h) {
@@ -855,7 +943,7 @@ int sd_draft_topw(const float* logits, int heads, int V, const int32_t* win_coun
     wmax = w[k] > wmax ? w[k] : wmax;
   }
   auto st = as_stream(stream);
-#define SD_TOPW(W) draft_topw_kernel<W><<<heads, SMP_THREADS, 0, st>>>(logits, V, win_count, temperature, theta, \
+#define SD_TOPW(W) draft_topw_kernel<W><<<heads * TW_CTAS, TW_THREADS, 0, st>>>(logits, V, win_count, temperature, theta, \
                                                                        ctrl_style, w[0], w[1], w[2], w[3], w[4], \
                                                                        w[5], w[6], w[7], out)
   if (wmax <= 4) SD_TOPW(4); else if (wmax <= 8) SD_TOPW(8); else SD_TOPW(16);
