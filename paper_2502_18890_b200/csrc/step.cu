@@ -179,10 +179,13 @@ struct Widths {
   int w[SD_TREE_MAX_DEPTH];
 };
 
+// Single-thread build into `tr` (a zeroed shared-memory copy of the record; the
+// trie links live in shared memory too). The ancestor masks are left to
+// tree_masks_dev, which the whole block runs afterwards.
 __device__ void tree_build_dev(const int32_t* per_head, const Widths& W, int K, const int32_t* grams, int n_grams,
-                               int pending, int64_t base_pos, int32_t* tr, int64_t* state) {
+                               int pending, int64_t base_pos, int32_t* tr, int64_t* state, int16_t* first_child,
+                               int16_t* next_sib) {
   using namespace tree_off;
-  int16_t first_child[SD_TREE_MAX_ROWS], next_sib[SD_TREE_MAX_ROWS];
   int n_nodes = 0, n_paths = 0;
   int root_first = -1;
   bool overflow = false;
@@ -282,34 +285,67 @@ __device__ void tree_build_dev(const int32_t* per_head, const Widths& W, int K, 
     tr[TOK + r] = pending < 0 ? 0 : pending;
     tr[POS + r] = (int32_t)base_pos;
   }
-  // ancestor-closure row masks over request rows (row 0 = root)
-  for (int r = 0; r < T; ++r) {
+  if (overflow && state) state[SD_ST_ERROR] |= 2;
+}
+
+// ancestor-closure row masks over request rows (row 0 = root), one row per thread
+__device__ void tree_masks_dev(int32_t* tr) {
+  using namespace tree_off;
+  const int T = tr[tree_off::T];
+  for (int r = threadIdx.x; r < T; r += blockDim.x) {
     uint32_t bits[SD_MASK_WORDS];
     for (int w = 0; w < SD_MASK_WORDS; ++w) bits[w] = 0;
     bits[0] = 1u;
     for (int x = r - 1; x >= 0; x = tr[PARENT + x]) bits[(x + 1) >> 5] |= 1u << ((x + 1) & 31);
     for (int w = 0; w < SD_MASK_WORDS; ++w) tr[MASK + r * SD_MASK_WORDS + w] = (int32_t)bits[w];
   }
-  if (overflow && state) state[SD_ST_ERROR] |= 2;
+}
+
+// The record is assembled in shared memory (zeroed first, so every field the
+// build does not set reads as 0) and written out with 16-byte stores.
+constexpr int TREE_THREADS = 128;
+static_assert(tree_off::TOTAL % 4 == 0, "tree record copied as int4");
+
+__device__ void tree_stage_zero(int32_t* str) {
+  for (int i = threadIdx.x; i < tree_off::TOTAL / 4; i += blockDim.x)
+    reinterpret_cast<int4*>(str)[i] = make_int4(0, 0, 0, 0);
+  __syncthreads();
+}
+__device__ void tree_stage_out(const int32_t* str, int32_t* tree) {
+  __syncthreads();
+  tree_masks_dev(const_cast<int32_t*>(str));
+  __syncthreads();
+  for (int i = threadIdx.x; i < tree_off::TOTAL / 4; i += blockDim.x)
+    reinterpret_cast<int4*>(tree)[i] = reinterpret_cast<const int4*>(str)[i];
 }
 
 __global__ void tree_build_kernel(const int32_t* per_head, Widths W, int K, const int32_t* grams,
                                   const int32_t* n_grams_dev, int n_grams_host, const int64_t* state,
                                   int64_t base_pos, int32_t* tree) {
+  __shared__ __align__(16) int32_t str[tree_off::TOTAL];
+  __shared__ int16_t fc[SD_TREE_MAX_ROWS], nsib[SD_TREE_MAX_ROWS];
   if (base_pos < 0) base_pos = state[SD_ST_BASE];
-  if (threadIdx.x || blockIdx.x) return;
-  const int ng = n_grams_dev ? *n_grams_dev : n_grams_host;
-  const int pending = state ? (int)state[SD_ST_PENDING] : -1;
-  tree_build_dev(per_head, W, K, grams, ng, pending, base_pos, tree, (int64_t*)state);
+  tree_stage_zero(str);
+  if (threadIdx.x == 0) {
+    const int ng = n_grams_dev ? *n_grams_dev : n_grams_host;
+    const int pending = state ? (int)state[SD_ST_PENDING] : -1;
+    tree_build_dev(per_head, W, K, grams, ng, pending, base_pos, str, (int64_t*)state, fc, nsib);
+  }
+  tree_stage_out(str, tree);
 }
 
 __global__ void draft_tree_kernel(const void* ngram, int k, const int32_t* per_head, Widths W, int K,
                                   const int64_t* state, int64_t base_pos, int32_t* grams, int32_t* tree) {
+  __shared__ __align__(16) int32_t str[tree_off::TOTAL];
+  __shared__ int16_t fc[SD_TREE_MAX_ROWS], nsib[SD_TREE_MAX_ROWS];
   if (base_pos < 0) base_pos = state[SD_ST_BASE];
-  if (threadIdx.x || blockIdx.x) return;
-  int ng = 0;
-  if (ngram && k > 0) ng = ng_retrieve_dev(ngram, per_head[0], k, grams);
-  tree_build_dev(per_head, W, K, grams, ng, (int)state[SD_ST_PENDING], base_pos, tree, (int64_t*)state);
+  tree_stage_zero(str);
+  if (threadIdx.x == 0) {
+    int ng = 0;
+    if (ngram && k > 0) ng = ng_retrieve_dev(ngram, per_head[0], k, grams);
+    tree_build_dev(per_head, W, K, grams, ng, (int)state[SD_ST_PENDING], base_pos, str, (int64_t*)state, fc, nsib);
+  }
+  tree_stage_out(str, tree);
 }
 
 // ----------------------------------------------------- accept + commit -----
@@ -460,7 +496,7 @@ int sd_tree_build(const int32_t* per_head, const int32_t* widths_host, int depth
                   const int32_t* n_grams_dev, int n_grams_host, const int64_t* state, int64_t base_pos,
                   int32_t* tree, sd_stream_t stream) {
   SD_REQUIRE(depth >= 1 && depth <= SD_TREE_MAX_DEPTH, "sd_tree_build: depth");
-  tree_build_kernel<<<1, 32, 0, as_stream(stream)>>>(per_head, widths_from(widths_host, depth), depth, grams,
+  tree_build_kernel<<<1, TREE_THREADS, 0, as_stream(stream)>>>(per_head, widths_from(widths_host, depth), depth, grams,
                                                      n_grams_dev, n_grams_host, state, base_pos, tree);
   return check_launch("sd_tree_build");
 }
@@ -468,7 +504,7 @@ int sd_tree_build(const int32_t* per_head, const int32_t* widths_host, int depth
 int sd_draft_tree(const void* ngram_table, int k, const int32_t* per_head, const int32_t* widths_host, int depth,
                   const int64_t* state, int64_t base_pos, int32_t* grams_scratch, int32_t* tree, sd_stream_t stream) {
   SD_REQUIRE(depth >= 1 && depth <= SD_TREE_MAX_DEPTH && k >= 0 && k <= 64, "sd_draft_tree: depth/k");
-  draft_tree_kernel<<<1, 32, 0, as_stream(stream)>>>(ngram_table, k, per_head, widths_from(widths_host, depth),
+  draft_tree_kernel<<<1, TREE_THREADS, 0, as_stream(stream)>>>(ngram_table, k, per_head, widths_from(widths_host, depth),
                                                      depth, state, base_pos, grams_scratch, tree);
   return check_launch("sd_draft_tree");
 }
