@@ -371,26 +371,45 @@ __global__ void accept_commit_kernel(const int32_t* __restrict__ tr, const int32
                                      int32_t* result) {
   using namespace tree_off;
   __shared__ int best[SD_TREE_MAX_PATHS];
-  if (threadIdx.x || blockIdx.x) return;
+  if (blockIdx.x) return;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x >= 32) return;
   if (n < 0) n = state[SD_ST_BASE] + 1;  // device-resident step (graph replay)
   const int P = tr[NPATHS];
-  int best_v = -1, nb = 0;
-  for (int p = 0; p < P; ++p) {
-    int expect = y[0], v = 0;
-    for (int j = 0; j < K; ++j) {
-      const int node = tr[PNODES + p * SD_TREE_MAX_DEPTH + j];
-      if (tr[TOK + 1 + node] != expect) break;
-      ++v;
-      expect = y[1 + node];
+  // path validity, one path per lane; the longest valid prefix and the paths that
+  // reach it, in ascending path order (ballot compaction)
+  constexpr int PK = SD_TREE_MAX_PATHS / 32;
+  int vloc[PK];
+  int best_v = -1;
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    const int p = k * 32 + lane;
+    int v = -1;
+    if (k * 32 < P && p < P) {
+      int expect = y[0];
+      v = 0;
+      for (int j = 0; j < K; ++j) {
+        const int node = tr[PNODES + p * SD_TREE_MAX_DEPTH + j];
+        if (tr[TOK + 1 + node] != expect) break;
+        ++v;
+        expect = y[1 + node];
+      }
     }
-    if (v > best_v) {
-      best_v = v;
-      nb = 0;
-      best[nb++] = p;
-    } else if (v == best_v) {
-      best[nb++] = p;
-    }
+    vloc[k] = v;
+    best_v = max(best_v, v);
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) best_v = max(best_v, __shfl_xor_sync(0xffffffffu, best_v, o));
+  int nb = 0;
+#pragma unroll
+  for (int k = 0; k < PK; ++k) {
+    const bool hit = k * 32 + lane < P && vloc[k] == best_v;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (hit) best[nb + __popc(m & ((1u << lane) - 1u))] = k * 32 + lane;
+    nb += __popc(m);
+  }
+  __syncwarp();
+  if (lane) return;  // the commit below is sequential
   const int pick = best[(int)(uniform_at(select_seed, (uint64_t)n) * (double)nb)];
   int a = bonus ? (best_v + 1 < K ? best_v + 1 : K) : (best_v > 1 ? best_v : 1);
   int ys[SD_TREE_MAX_DEPTH], keep[SD_TREE_MAX_DEPTH];
