@@ -56,6 +56,13 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
                                    int64_t split_stride) {
   __shared__ float red[32];
   pdl_trigger();
+  // the gains are weights (never written by a kernel): loaded before the wait
+  float4 g[PER];
+#pragma unroll
+  for (int k = 0; k < PER; ++k) {
+    const int i = (threadIdx.x + k * blockDim.x) * 4;
+    if (i < d) g[k] = *reinterpret_cast<const float4*>(gain + i);
+  }
   pdl_wait();
   const int64_t base = (int64_t)blockIdx.x * d;
   float4 v[PER];
@@ -82,10 +89,9 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
 #pragma unroll
   for (int k = 0; k < PER; ++k) {
     const int i = (threadIdx.x + k * blockDim.x) * 4;
-    if (i < d) {
-      const float4 g = *reinterpret_cast<const float4*>(gain + i);
-      store4<XT>(x, base + i, v[k].x * (g.x * inv), v[k].y * (g.y * inv), v[k].z * (g.z * inv), v[k].w * (g.w * inv));
-    }
+    if (i < d)
+      store4<XT>(x, base + i, v[k].x * (g[k].x * inv), v[k].y * (g[k].y * inv), v[k].z * (g[k].z * inv),
+                 v[k].w * (g[k].w * inv));
   }
 }
 

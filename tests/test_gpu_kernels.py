@@ -490,19 +490,23 @@ def test_verify_sampler_tree_rows_match_oracle_node_masks(lib):
         assert y.cpu().tolist() == want
 
 
-def test_draft_topw_matches_stable_argsort(lib):
+@pytest.mark.parametrize("V,widths", [(5000, [1, 3, 3, 3]), (20, [8, 5, 16, 2]), (151936, [16, 9, 4, 1]),
+                                      (64, [16, 16, 16, 16])])
+def test_draft_topw_matches_stable_argsort(lib, V, widths):
+    """Per-head top-w over an 8-CTA cluster (vocabulary slices, some shorter than
+    w): penalised scaled logits, ties -> lower id across slices (engine.py:207-215)."""
     g = np.random.default_rng(2)
-    V = 5000
     logits = g.normal(scale=3, size=(4, V)).astype(np.float32)
-    logits[1, 17] = logits[1, 4000] = logits[1].max() + 1  # exact tie -> lower id first
+    logits[1, 17 % V] = logits[1, (4000 % V) or 1] = logits[1].max() + 1  # exact tie -> lower id first
+    logits[2, V // 2: 2 * (V // 2)] = logits[2, : V // 2]  # equal logits in different slices (ties when both
+    # have the same window membership)
     cnt = np.zeros(V, dtype=np.int32)
-    cnt[g.integers(0, V, size=300)] = 1
+    cnt[g.integers(0, V, size=max(1, V // 16))] = 1
     smp = OS.SamplerConfig(temperature=1.0, theta=1.2, window=64)
     probs = OS.penalized_probs_masked(logits.astype(np.float64), np.broadcast_to(cnt > 0, (4, V)), smp)
-    widths = [1, 3, 3, 3]
     want = [int(t) for k in range(4) for t in np.argsort(-probs[k], kind="stable")[: widths[k]]]
     from paper_2502_18890_b200 import _lib as Lb
-    out = torch.empty(10, dtype=torch.int32, device="cuda")
+    out = torch.empty(sum(widths), dtype=torch.int32, device="cuda")
     lt = torch.as_tensor(logits, device="cuda")
     ct = torch.as_tensor(cnt, device="cuda")
     Lb.call("sd_draft_topw", Lb.ptr(lt), 4, V, Lb.ptr(ct), 1.0, 1.2, 0, Lb.host_i32(widths), Lb.ptr(out), Lb.stream())
