@@ -249,7 +249,7 @@ def main():
         "metric": metric_name(args.config),
         "value": tokens / dev_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights; random prompt prefilled; synthetic KV beyond the prefix)",
         "config": {"workload": workload_name(args.config, c, ctx), "ctx": ctx, "global_batch": 1,
                    "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (12.4 GB weights + KV per step)"},
