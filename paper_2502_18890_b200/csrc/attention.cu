@@ -974,8 +974,13 @@ __global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnPa
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  if (warp < G) {
-    const int row = kvh * G + warp;  // T == 1: row = head
+  // every warp takes (head row, part of the chunk range); parts summed in order
+  const int parts = DR_WARPS / G, gi = warp % G, part = warp / G;
+  const bool active = part < parts;
+  const int row = kvh * G + gi;  // T == 1: row = head
+  float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float L = 0.f;
+  if (active) {
     float lv[3], wv[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -983,16 +988,15 @@ __global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnPa
       lv[k] = c < nc ? __ldcg(p.ws_lse + (int64_t)c * p.H + row) : -INFINITY;
     }
     const float M = warp_max(fmaxf(lv[0], fmaxf(lv[1], lv[2])));
-    float L = 0.f;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       wv[k] = lv[k] == -INFINITY ? 0.f : __expf(lv[k] - M);
       L += wv[k];
     }
     L = warp_sum(L);
-    float4 o4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int ca = part * nc / parts, cb = (part + 1) * nc / parts;
 #pragma unroll 8
-    for (int c = 0; c < nc; ++c) {
+    for (int c = ca; c < cb; ++c) {
       const float w = __shfl_sync(0xffffffffu, c < 32 ? wv[0] : (c < 64 ? wv[1] : wv[2]), c & 31);
       const float4 o = __ldcg(reinterpret_cast<const float4*>(p.ws_o + ((int64_t)c * p.H + row) * DH) + lane);
       if (w != 0.f) {
@@ -1002,8 +1006,17 @@ __global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnPa
         o4.w = fmaf(w, o.w, o4.w);
       }
     }
+    *reinterpret_cast<float4*>(&So[part][gi][lane * 4]) = o4;
+  }
+  __syncthreads();
+  if (warp < G) {
+    float4 t = *reinterpret_cast<const float4*>(&So[0][gi][lane * 4]);
+    for (int q = 1; q < parts; ++q) {
+      const float4 u = *reinterpret_cast<const float4*>(&So[q][gi][lane * 4]);
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
     const float inv = L > 0.f ? 1.f / L : 0.f;
-    store4<__nv_bfloat16>(out + (int64_t)row * DH + lane * 4, o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
+    store4<__nv_bfloat16>(out + (int64_t)row * DH + lane * 4, t.x * inv, t.y * inv, t.z * inv, t.w * inv);
   }
   if (tid == 0) counters[kvh] = 0;  // ready for the next launch / graph replay
 }
