@@ -76,7 +76,10 @@ int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int 
  * apart, summed in slice order.
  * rows_dev (nullable): rows t >= *rows_dev are skipped. row_offset < 0: rows go
  * to positions[0] + t (device-resident offset; k_raw / k_rot / v then point
- * at row 0 of the layer). */
+ * at row 0 of the layer). Launched as a programmatic dependent: positions,
+ * rows_dev and the tables are read before the dependency wait, so they must
+ * come from an ordinary launch or copy (tree record, host fill), not from a
+ * kernel of the same programmatic-dependent chain; qkv may. */
 int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t* positions,
                   const float* rope_cos, const float* rope_sin, float q_scale,
                   void* q_rot, int q_dtype, float* q_pre,

@@ -178,8 +178,13 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
                                   const int32_t* __restrict__ rows_dev, int splits, int64_t split_stride) {
   const int t = blockIdx.x;
   pdl_trigger();
-  pdl_wait();
-  if (rows_dev && t >= *rows_dev) return;
+  // positions / rows_dev come from the tree record or a host fill (never from a
+  // programmatic-dependent kernel), and cos/sin are tables: all read before the
+  // wait, so only the projection output waits for the kernel before
+  if (rows_dev && t >= *rows_dev) {
+    pdl_wait();
+    return;
+  }
   const int half = dh >> 1;
   const int width = (H + 2 * Hk) * dh;
   const float* row = qkv + (int64_t)t * width;
@@ -188,7 +193,20 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   // committed cache; device-resident step under graph replay)
   const int64_t dst_row = (row_offset >= 0 ? row_offset : (int64_t)positions[0]) + t;
   const int quads_rot = (H + Hk) * dh / 4, quads_all = width / 4;
-  for (int u = threadIdx.x; u < quads_all; u += blockDim.x) {
+  constexpr int PF = 4;  // rotation tables prefetched for a thread's first PF quads
+  float2 pc[PF], ps[PF];
+#pragma unroll
+  for (int k = 0; k < PF; ++k) {
+    const int u = threadIdx.x + k * blockDim.x;
+    if (u < quads_rot) {
+      const int j = ((4 * u) % dh) >> 1;
+      pc[k] = *reinterpret_cast<const float2*>(cosT + pos * half + j);
+      ps[k] = *reinterpret_cast<const float2*>(sinT + pos * half + j);
+    }
+  }
+  pdl_wait();
+  int k = 0;
+  for (int u = threadIdx.x; u < quads_all; u += blockDim.x, ++k) {
     float4 x = *reinterpret_cast<const float4*>(row + 4 * u);
     for (int s = 1; s < splits; ++s) {  // split-K slices of the QKV GEMM, summed in order
       const float4 e = *reinterpret_cast<const float4*>(row + s * split_stride + 4 * u);
@@ -197,8 +215,18 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
     const int col = 4 * u, head = col / dh, e = col - head * dh;
     if (u < quads_rot) {
       const int j = e >> 1;  // pair index of x.x/x.y; x.z/x.w is j + 1
-      const float2 c = *reinterpret_cast<const float2*>(cosT + pos * half + j);
-      const float2 s = *reinterpret_cast<const float2*>(sinT + pos * half + j);
+      float2 c, s;
+      if (k < PF) {
+#pragma unroll
+        for (int q = 0; q < PF; ++q)
+          if (q == k) {
+            c = pc[q];
+            s = ps[q];
+          }
+      } else {
+        c = *reinterpret_cast<const float2*>(cosT + pos * half + j);
+        s = *reinterpret_cast<const float2*>(sinT + pos * half + j);
+      }
       const float r0 = x.x * c.x - x.y * s.x, r1 = x.x * s.x + x.y * c.x;
       const float r2 = x.z * c.y - x.w * s.y, r3 = x.z * s.y + x.w * c.y;
       if (head < H) {
