@@ -42,9 +42,6 @@ constexpr int WARPS = 8;
 #ifndef SD_GEMV_TMA_DEFAULT
 #define SD_GEMV_TMA_DEFAULT 1
 #endif
-#ifndef SD_GEMV_PIPE
-#define SD_GEMV_PIPE 0
-#endif
 constexpr int UNROLL = SD_GEMV_UNROLL;  // weight rows in flight per warp
 
 __device__ __forceinline__ void fma8(float* acc, float xv, const uint4& w) {
@@ -85,35 +82,11 @@ __global__ void __launch_bounds__(WARPS * 32, SD_GEMV_MINB) gemv_kernel(const __
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#if SD_GEMV_PIPE
-  // register double buffer: batch i+1's loads are in flight while batch i is consumed
-  if (first) {
-    uint4 cur[UNROLL];
-#pragma unroll
-    for (int u = 0; u < UNROLL; ++u) cur[u] = w0[u];
-    for (;;) {
-      const int kn = k + UNROLL * WARPS;
-      const bool more = kn + (UNROLL - 1) * WARPS < k1;
-      uint4 nxt[UNROLL];
-      if (more) {
-#pragma unroll
-        for (int u = 0; u < UNROLL; ++u) nxt[u] = __ldcs(reinterpret_cast<const uint4*>(wp + (int64_t)(kn + u * WARPS) * N));
-      }
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) fma8(acc, xs[k + u * WARPS - k0], cur[u]);
-      k = kn;
-      if (!more) break;
-#pragma unroll
-      for (int u = 0; u < UNROLL; ++u) cur[u] = nxt[u];
-    }
-  }
-#else
   if (first) {
 #pragma unroll
     for (int u = 0; u < UNROLL; ++u) fma8(acc, xs[k + u * WARPS - k0], w0[u]);
     k += UNROLL * WARPS;
   }
-#endif
   if (live) {
     for (; k + (UNROLL - 1) * WARPS < k1; k += UNROLL * WARPS) {
       uint4 w[UNROLL];
