@@ -145,6 +145,7 @@ int sd_debug_tc_trace(void* trace_dev, int force_chunks);
  * once before first use — the kernel leaves it zeroed). */
 #define SD_GEMM_EPI_F32 0
 #define SD_GEMM_EPI_SILU_BF16 1
+#define SD_GEMM_EPI_ADDNORM 2 /* internal to sd_gemv_addnorm */
 int sd_tile_weight(const void* w, int K, int N, void* w_tiled, sd_stream_t stream);
 int sd_make_weight_tmap(const void* w_tiled, int K, int N, void* tmap_out_host);
 int sd_gemm_splits(int M, int N, int K, int epi);
@@ -162,6 +163,12 @@ int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi
 size_t sd_gemv_workspace_bytes(int K, int N);
 int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
             sd_stream_t stream);
+/* Projection fused with the residual add + RMSNorm that follows it
+ * (model.py:278, 306-311): h[N] += x[K] . W[K][N]; x_out = h * gain / rms(h)
+ * (x_dtype SD_BF16 / SD_F32). The last column block to finish normalises the
+ * row, so the pair is one launch; same workspace as sd_gemv. */
+int sd_gemv_addnorm(const void* x, int K, const void* w, int N, float* h, const float* gain, float eps, void* x_out,
+                    int x_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
 
 /* ---- Eq. 2 importance (kvcache.py:243-265) ----
  * scores[l][p - start] = sum_k sum_g q_sum[l][k*G+g] . K_raw[l][k][p], p in [start, end),

@@ -29,6 +29,8 @@ namespace sd {
 namespace gv {
 
 constexpr int COLS = 256;    // columns per CTA (32 lanes x 8)
+constexpr int WS_HEAD_INTS = 1024;
+constexpr int ADDNORM_PER = 24, ADDNORM_MAX_N = ADDNORM_PER * 256;  // fused add+norm row length limit  // counter head: per column block, the last int is the row counter
 constexpr int WARPS = 8;
 #ifndef SD_GEMV_UNROLL
 #define SD_GEMV_UNROLL 8
@@ -171,9 +173,21 @@ constexpr int TR = SD_GEMV_TR, NS = SD_GEMV_NS;
 constexpr int STAGE_BYTES = TR * COLS * 2;
 constexpr int RPW = TR / WARPS;  // stage rows per consumer warp
 
+// Residual add + RMSNorm of the whole output row (model.py:278, 306-311), run by
+// the last column block to finish: h += y; x = h * gain / rms(h). Replaces the
+// separate sd_add_rmsnorm launch after a single-row projection.
+struct AddNorm {
+  float* h;           // [N] residual stream, updated in place
+  const float* gain;  // [N]
+  float eps;
+  void* x;            // [N] normalised output
+  int x_bf16;         // 1: bf16 x, 0: fp32 x
+};
+
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     gemv_tma_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ x, int K, int N,
-                    int splits, int epi, void* __restrict__ y, float* __restrict__ part, int* __restrict__ counters) {
+                    int splits, int epi, void* __restrict__ y, float* __restrict__ part, int* __restrict__ counters,
+                    AddNorm an) {
   extern __shared__ __align__(1024) uint8_t gsm[];
   uint8_t* ring = gsm;                                    // NS stages
   float* xs = reinterpret_cast<float*>(gsm + NS * STAGE_BYTES);  // K slice of x
@@ -234,29 +248,68 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
   const int gcol = cb * COLS + c;
   auto store = [&](float sum) {
     if (gcol >= N) return;
-    if (epi == SD_GEMM_EPI_F32)
-      ((float*)y)[gcol] = sum;
-    else
+    if (epi == SD_GEMM_EPI_SILU_BF16)
       ((__nv_bfloat16*)y)[gcol] = __float2bfloat16_rn(sum / (1.f + __expf(-sum)));
+    else
+      ((float*)y)[gcol] = sum;  // F32, or the row scratch of ADDNORM
   };
-  if (splits == 1) {
-    store(v);
-    return;
+  if (splits > 1) {
+    if (gcol < N) part[(int64_t)split * N + gcol] = v;
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
+    if (tid == 0) s_last = atomicAdd(&counters[cb], 1) == splits - 1;
+    asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
+    if (!s_last) return;
+    __threadfence();
+    v = 0.f;
+#pragma unroll 8
+    for (int sp = 0; sp < splits; ++sp) v += gcol < N ? __ldcg(part + (int64_t)sp * N + gcol) : 0.f;
+    if (tid == 0) counters[cb] = 0;
   }
-  if (gcol < N) part[(int64_t)split * N + gcol] = v;
+  store(v);
+  if (epi != SD_GEMM_EPI_ADDNORM) return;
+  // ---- the last column block to finish normalises the whole row ----
+  const int blocks = gridDim.x;
+  int* row_counter = counters + (WS_HEAD_INTS - 1);
   __threadfence();
   asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
-  if (tid == 0) s_last = atomicAdd(&counters[cb], 1) == splits - 1;
+  if (tid == 0) s_last = atomicAdd(row_counter, 1) == blocks - 1;
   asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
   if (!s_last) return;
   __threadfence();
-  if (gcol < N) {
-    float sum = 0.f;
-#pragma unroll 8
-    for (int sp = 0; sp < splits; ++sp) sum += __ldcg(part + (int64_t)sp * N + gcol);
-    store(sum);
+  // all loads of the row issued at once (N <= ADDNORM_MAX_N): one round trip, not N/256
+  const float* yr = (const float*)y;
+  float hv[ADDNORM_PER], gv_[ADDNORM_PER];
+#pragma unroll
+  for (int k = 0; k < ADDNORM_PER; ++k) {
+    const int i = tid + k * WARPS * 32;
+    hv[k] = i < N ? an.h[i] + __ldcg(yr + i) : 0.f;
+    gv_[k] = i < N ? an.gain[i] : 0.f;
   }
-  if (tid == 0) counters[cb] = 0;
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < ADDNORM_PER; ++k) ss += hv[k] * hv[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if (lane == 0) red[0][warp] = ss;
+  asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < WARPS; ++w) tot += red[0][w];
+  const float inv = rsqrtf(tot / (float)N + an.eps);
+#pragma unroll
+  for (int k = 0; k < ADDNORM_PER; ++k) {
+    const int i = tid + k * WARPS * 32;
+    if (i < N) {
+      an.h[i] = hv[k];
+      const float xv = hv[k] * (gv_[k] * inv);
+      if (an.x_bf16)
+        ((__nv_bfloat16*)an.x)[i] = __float2bfloat16_rn(xv);
+      else
+        ((float*)an.x)[i] = xv;
+    }
+  }
+  if (tid == 0) *row_counter = 0;
 }
 
 static int tma_splits(int K, int N) {
@@ -317,6 +370,56 @@ static int weight_map(const void* w, int K, int N, CUtensorMap* out) {
   return 0;
 }
 
+// one launch of the TMA kernel; false when its shared memory would not fit
+static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace,
+                       const AddNorm& an, cudaStream_t st, int* rc) {
+  const int blocks = (N + COLS - 1) / COLS;
+  const int s = tma_splits(K, N);
+  const size_t smem = (size_t)NS * STAGE_BYTES + ((K + s - 1) / s + 1) * sizeof(float);
+  if (!use_tma() || smem > 212 * 1024) return false;
+  CUtensorMap m;
+  if (weight_map(w, K, N, &m)) {
+    *rc = SD_ECUDA;
+    return true;
+  }
+  // the attribute only grows: graph nodes captured with a larger size must still
+  // launch after a smaller shape was captured (kernel replay re-checks it)
+  static size_t attr = 0;
+  if (smem > attr) {
+    cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  launch_pdl(gemv_tma_kernel, dim3(blocks, s), dim3((WARPS + 1) * 32), smem, st, m, (const __nv_bfloat16*)x, K, N,
+             s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an);
+  *rc = check_launch("sd_gemv");
+  return true;
+}
+
+static int launch_ld(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace,
+                     cudaStream_t st) {
+  const int blocks = (N + COLS - 1) / COLS;
+  const int s = splits_for(K, N);
+  const int kslice = (K + s - 1) / s + 1;
+  const size_t smem = (size_t)kslice * sizeof(float);
+  SD_REQUIRE(smem <= 200 * 1024, "sd_gemv: K slice too long");
+  static size_t attr = 48 * 1024;  // only grows (see above)
+  if (smem > attr) {
+    cudaFuncSetAttribute(gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  launch_pdl(gemv_kernel, dim3(blocks, s), dim3(WARPS * 32), smem, st, (const __nv_bfloat16*)x,
+             (const __nv_bfloat16*)w, K, N, s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr,
+             (int*)workspace);
+  return check_launch("sd_gemv");
+}
+
+static size_t partial_bytes(int K, int N) {
+  int s = splits_for(K, N);
+  const int st = tma_splits(K, N);
+  if (st > s) s = st;  // either implementation fits
+  return s > 1 ? (size_t)s * N * sizeof(float) : 0;
+}
+
 }  // namespace gv
 }  // namespace sd
 
@@ -326,10 +429,8 @@ extern "C" {
 
 size_t sd_gemv_workspace_bytes(int K, int N) {
   if (K <= 0 || N <= 0) return 0;
-  int s = gv::splits_for(K, N);
-  const int st = gv::tma_splits(K, N);
-  if (st > s) s = st;  // either implementation fits
-  return gv::WS_HEAD + (s > 1 ? (size_t)s * N * sizeof(float) : 0);
+  // counter head | split partials | one fp32 row (the add+norm epilogue's scratch)
+  return gv::WS_HEAD + gv::partial_bytes(K, N) + (size_t)N * sizeof(float);
 }
 
 int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
@@ -338,42 +439,35 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
   SD_REQUIRE(((uintptr_t)w % 16) == 0, "sd_gemv: W must be 16-byte aligned");
   SD_REQUIRE(epi == SD_GEMM_EPI_F32 || epi == SD_GEMM_EPI_SILU_BF16, "sd_gemv: epilogue");
   const int blocks = (N + gv::COLS - 1) / gv::COLS;
-  SD_REQUIRE((size_t)blocks * sizeof(int) <= gv::WS_HEAD, "sd_gemv: N=%d too wide for the counter head", N);
-  const int s_tma = gv::tma_splits(K, N);
-  const size_t smem_tma = (size_t)gv::NS * gv::STAGE_BYTES + ((K + s_tma - 1) / s_tma + 1) * sizeof(float);
-  if (gv::use_tma() && smem_tma <= 212 * 1024) {  // else: the register-streaming kernel below
-    const int s = s_tma;
-    const size_t smem = smem_tma;
-    SD_REQUIRE(s == 1 || (workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N)), "sd_gemv: workspace");
-    CUtensorMap m;
-    if (gv::weight_map(w, K, N, &m)) return SD_ECUDA;
-    // the attribute only grows: graph nodes captured with a larger size must still
-    // launch after a smaller shape was captured (kernel replay re-checks it)
-    static size_t attr = 0;
-    if (smem > attr) {
-      cudaFuncSetAttribute(gv::gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
-    }
-    launch_pdl(gv::gemv_tma_kernel, dim3(blocks, s), dim3((gv::WARPS + 1) * 32), smem, as_stream(stream), m,
-               (const __nv_bfloat16*)x, K, N, s, epi, y, s > 1 ? (float*)((char*)workspace + gv::WS_HEAD) : nullptr,
-               (int*)workspace);
-    return check_launch("sd_gemv");
+  SD_REQUIRE((size_t)blocks < (size_t)gv::WS_HEAD_INTS, "sd_gemv: N=%d too wide for the counter head", N);
+  SD_REQUIRE(workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N), "sd_gemv: workspace");
+  int rc = 0;
+  if (gv::launch_tma(x, K, w, N, epi, y, workspace, gv::AddNorm{}, as_stream(stream), &rc)) return rc;
+  return gv::launch_ld(x, K, w, N, epi, y, workspace, as_stream(stream));
+}
+
+int sd_gemv_addnorm(const void* x, int K, const void* w, int N, float* h, const float* gain, float eps, void* x_out,
+                    int x_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
+  SD_REQUIRE(x && w && h && gain && x_out && K > 0 && N > 0 && N % 8 == 0, "sd_gemv_addnorm: K=%d N=%d", K, N);
+  SD_REQUIRE(((uintptr_t)w % 16) == 0, "sd_gemv_addnorm: W must be 16-byte aligned");
+  SD_REQUIRE(x_dtype == SD_BF16 || x_dtype == SD_F32, "sd_gemv_addnorm: x dtype");
+  const int blocks = (N + gv::COLS - 1) / gv::COLS;
+  SD_REQUIRE((size_t)blocks < (size_t)gv::WS_HEAD_INTS, "sd_gemv_addnorm: N=%d too wide", N);
+  SD_REQUIRE(workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N), "sd_gemv_addnorm: workspace");
+  float* yrow = (float*)((char*)workspace + gv::WS_HEAD + gv::partial_bytes(K, N));
+  const gv::AddNorm an{h, gain, eps, x_out, x_dtype == SD_BF16};
+  int rc = 0;
+  if (N <= gv::ADDNORM_MAX_N &&
+      gv::launch_tma(x, K, w, N, SD_GEMM_EPI_ADDNORM, yrow, workspace, an, as_stream(stream), &rc))
+    return rc;
+  // projection, then the separate add + norm (long rows, or the register-streaming kernel)
+  if (gv::launch_tma(x, K, w, N, SD_GEMM_EPI_F32, yrow, workspace, gv::AddNorm{}, as_stream(stream), &rc)) {
+    if (rc) return rc;
+  } else {
+    rc = gv::launch_ld(x, K, w, N, SD_GEMM_EPI_F32, yrow, workspace, as_stream(stream));
   }
-  const int s = gv::splits_for(K, N);
-  SD_REQUIRE(s == 1 || (workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N)), "sd_gemv: workspace");
-  const size_t head = gv::WS_HEAD;
-  const int kslice = (K + s - 1) / s + 1;
-  const size_t smem = (size_t)kslice * sizeof(float);
-  SD_REQUIRE(smem <= 200 * 1024, "sd_gemv: K slice too long");
-  static size_t attr = 48 * 1024;  // only grows (see above)
-  if (smem > attr) {
-    cudaFuncSetAttribute(gv::gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
-  launch_pdl(gv::gemv_kernel, dim3(blocks, s), dim3(gv::WARPS * 32), smem, as_stream(stream),
-             (const __nv_bfloat16*)x, (const __nv_bfloat16*)w, K, N, s, epi, y,
-             s > 1 ? (float*)((char*)workspace + head) : nullptr, (int*)workspace);
-  return check_launch("sd_gemv");
+  if (rc) return rc;
+  return sd_add_rmsnorm(h, yrow, 1, N, gain, eps, x_out, x_dtype, 1, 0, stream);
 }
 
 }  // extern "C"

@@ -717,6 +717,33 @@ def test_gemv_vs_fp32_reference(lib, K, N, gemv_impl):
     torch.testing.assert_close(ysil.float(), torch.nn.functional.silu(want), rtol=1e-2, atol=1e-2)
 
 
+@pytest.mark.parametrize("K,N", [(4096, 4096), (16384, 4096), (13824, 5120), (256, 512), (64, 40)])
+@pytest.mark.parametrize("xdt", [torch.bfloat16, torch.float32])
+def test_gemv_addnorm_vs_fp32_reference(lib, K, N, xdt, gemv_impl):
+    """Projection + residual add + RMSNorm in one launch (model.py:278, 306-311):
+    h += x . W, x_out = h * gain / rms(h); the row counter is left zeroed so a
+    second call (graph replay) works."""
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(K * 7 + N)
+    x = torch.randn((1, K), generator=g, device=dev).to(torch.bfloat16)
+    w = (torch.randn((K, N), generator=g, device=dev) * K ** -0.5).to(torch.bfloat16)
+    gain = torch.rand((N,), generator=g, device=dev) + 0.5
+    h0 = torch.randn((1, N), generator=g, device=dev)
+    ws = torch.zeros(lib.load().sd_gemv_workspace_bytes(K, N), dtype=torch.uint8, device=dev)
+    h = h0.clone()
+    for rep in range(2):
+        out = torch.empty((1, N), dtype=xdt, device=dev)
+        lib.call("sd_gemv_addnorm", lib.ptr(x), K, lib.ptr(w), N, lib.ptr(h), lib.ptr(gain), 1e-6, lib.ptr(out),
+                 lib.dcode(xdt), lib.ptr(ws), ws.numel(), lib.stream())
+        want_h = h0 + (rep + 1) * (x.float() @ w.float())
+        torch.testing.assert_close(h, want_h, rtol=1e-4, atol=1e-4)
+        want_x = want_h * torch.rsqrt(want_h.pow(2).mean() + 1e-6) * gain
+        tol = 1e-2 if xdt == torch.bfloat16 else 1e-4
+        torch.testing.assert_close(out.float(), want_x, rtol=tol, atol=tol)
+    assert torch.count_nonzero(ws[:4096]) == 0  # counters left zeroed
+
+
 def test_gemv_shared_workspace_across_shapes(lib, gemv_impl):
     """One zeroed workspace serves every shape (the model shares it across
     layers): a narrow split call's partials must not land in a wider call's
