@@ -184,6 +184,7 @@ struct AddNorm {
   int x_bf16;         // 1: bf16 x, 0: fp32 x
 };
 
+template <bool ADDNORM>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     gemv_tma_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ x, int K, int N,
                     int splits, int epi, void* __restrict__ y, float* __restrict__ part, int* __restrict__ counters,
@@ -267,7 +268,8 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     if (tid == 0) counters[cb] = 0;
   }
   store(v);
-  if (epi != SD_GEMM_EPI_ADDNORM) return;
+  if constexpr (!ADDNORM) return;
+  else {
   // ---- the last column block to finish normalises the whole row ----
   const int blocks = gridDim.x;
   int* row_counter = counters + (WS_HEAD_INTS - 1);
@@ -310,6 +312,7 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     }
   }
   if (tid == 0) *row_counter = 0;
+  }
 }
 
 static int tma_splits(int K, int N) {
@@ -384,12 +387,14 @@ static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void
   }
   // the attribute only grows: graph nodes captured with a larger size must still
   // launch after a smaller shape was captured (kernel replay re-checks it)
-  static size_t attr = 0;
-  if (smem > attr) {
-    cudaFuncSetAttribute(gemv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
+  auto kern = epi == SD_GEMM_EPI_ADDNORM ? gemv_tma_kernel<true> : gemv_tma_kernel<false>;
+  static size_t attr[2] = {0, 0};
+  size_t& at = attr[epi == SD_GEMM_EPI_ADDNORM];
+  if (smem > at) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    at = smem;
   }
-  launch_pdl(gemv_tma_kernel, dim3(blocks, s), dim3((WARPS + 1) * 32), smem, st, m, (const __nv_bfloat16*)x, K, N,
+  launch_pdl(kern, dim3(blocks, s), dim3((WARPS + 1) * 32), smem, st, m, (const __nv_bfloat16*)x, K, N,
              s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an);
   *rc = check_launch("sd_gemv");
   return true;
