@@ -32,6 +32,22 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const T* __restric
   for (int i = threadIdx.x; i < d; i += blockDim.x) h[(int64_t)t * d + i] = to_f(row[i]);
 }
 
+// bf16 rows, 8 elements (one 16-byte load) per thread
+__global__ void embed8_kernel(const int32_t* __restrict__ tok, const __nv_bfloat16* __restrict__ E, int d,
+                              float* __restrict__ h) {
+  const int t = blockIdx.x;
+  const uint4* row = reinterpret_cast<const uint4*>(E + (int64_t)tok[t] * d);
+  float4* out = reinterpret_cast<float4*>(h + (int64_t)t * d);
+  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    const uint4 v = row[i];
+    const __nv_bfloat162* p = reinterpret_cast<const __nv_bfloat162*>(&v);
+    const float2 a = __bfloat1622float2(p[0]), b = __bfloat1622float2(p[1]);
+    const float2 c = __bfloat1622float2(p[2]), e = __bfloat1622float2(p[3]);
+    out[2 * i] = make_float4(a.x, a.y, b.x, b.y);
+    out[2 * i + 1] = make_float4(c.x, c.y, e.x, e.y);
+  }
+}
+
 // one block per row: h += delta; x = h * gain / sqrt(mean(h^2) + eps).
 // float4 vectors: every thread issues its loads before the reduction.
 template <typename XT>
@@ -269,7 +285,10 @@ const char* sd_last_error(void) { return sd::g_err; }
 int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, float* h, sd_stream_t stream) {
   SD_REQUIRE(T > 0 && d > 0, "sd_embed: bad sizes");
   auto st = as_stream(stream);
-  if (dtype == SD_BF16)
+  if (dtype == SD_BF16 && d % 8 == 0 && ((uintptr_t)embed % 16) == 0 && ((uintptr_t)h % 16) == 0)
+    embed8_kernel<<<T, d / 8 < 512 ? ((d / 8 + 31) / 32) * 32 : 512, 0, st>>>(tokens, (const __nv_bfloat16*)embed,
+                                                                          d, h);
+  else if (dtype == SD_BF16)
     embed_kernel<<<T, 256, 0, st>>>(tokens, (const __nv_bfloat16*)embed, d, h);
   else if (dtype == SD_F32)
     embed_kernel<<<T, 256, 0, st>>>(tokens, (const float*)embed, d, h);

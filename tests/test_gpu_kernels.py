@@ -803,3 +803,17 @@ def test_cluster_sampler_equals_row_sampler(lib, V, trunc, pad):
         assert outs[-2] == outs[-1], (trunc, V, trial)
         assert all(0 <= t < V for t in outs[-1][:41])
         assert all(t == -1 for t in outs[-2][41:])
+
+
+@pytest.mark.parametrize("d", [4096, 5120, 40, 8])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_embed_rows(lib, d, dtype):
+    """Embedding gather (model.py:234-236): 16-byte bf16 loads when d % 8 == 0,
+    scalar otherwise; fp32 out."""
+    dev = torch.device("cuda")
+    V = 1000
+    E = torch.randn((V, d), device=dev).to(dtype)
+    tok = torch.tensor([5, 999, 0, 5, 123], dtype=torch.int32, device=dev)
+    h = torch.full((5, d), float("nan"), device=dev)
+    lib.call("sd_embed", lib.ptr(tok), 5, lib.ptr(E), lib.dcode(dtype), d, lib.ptr(h), lib.stream())
+    assert torch.equal(h, E[tok.long()].float())
