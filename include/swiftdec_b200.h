@@ -103,8 +103,10 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
  * taken from k_cache / v_cache right after the live rows (k_tree / v_tree are
  * ignored). With ctx_dev every argument is step-invariant, so the call can be
  * captured once in a CUDA graph and replayed as the cache grows.
- * CUDA-core split boundaries depend on ctx only (bitwise identical across GPU
- * counts); the tensor-core path splits by SM count. The tensor-core and draft
+ * Split boundaries depend on ctx only — the tensor-core path also on
+ * kv_heads_total, the model's kv heads over all shards (0 = Hk) — so a kv
+ * head's output is bitwise identical for any number of GPUs sharing the heads
+ * (SURVEY H7). The tensor-core and draft
  * kernels are programmatic dependent launches: rows_dev, ctx_dev, ranks and
  * the committed cache rows are read before the dependency wait, so they must
  * not be written by the kernel launched immediately before (q, the tree rows
@@ -118,7 +120,7 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
                  int ctx, const int32_t* ranks, const float* rope_cos, const float* rope_sin,
                  const void* k_tree, const void* v_tree, int64_t tree_head_stride,
                  const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev, const int32_t* ctx_dev,
-                 const void* tmap_k_host, const void* tmap_v_host, int layer,
+                 const void* tmap_k_host, const void* tmap_v_host, int layer, int kv_heads_total,
                  void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
 /* 128-byte TMA descriptor (CUtensorMap) over a whole [L][Hk][cap][128] bf16
  * cache array. When sd_attention gets descriptors for K_rot and V (and the

@@ -123,8 +123,11 @@ class TinyTransformer:
             hs.append(hs[-1] @ p[f"head{i + 1}"] + hs[-1])
         return np.stack([h @ p["embed"].T for h in hs], axis=-2)
 
-    def forward(self, tokens, positions, cache, mask=None, heads_needed=None):
-        """Returns (bundles (T, gamma+1, V), queries (T, L, H, dh) pre-rotation)."""
+    def forward(self, tokens, positions, cache, mask=None, heads_needed=None, logit_rows=None):
+        """Returns (bundles (T, gamma+1, V), queries (T, L, H, dh) pre-rotation).
+        logit_rows (test convenience, not in the reference): compute the head
+        logits only for these rows (the others stay -inf), so a teacher-forced
+        check over a long sequence does not materialise T x V logits it ignores."""
         c, p = self.config, self.params
         T = len(tokens)
         if T == 0:
@@ -170,7 +173,12 @@ class TinyTransformer:
             h = h + (a / (1.0 + np.exp(-a))) @ p[f"l{l}.w2"]
         h0 = rmsnorm(h, p["ln_f"])
         heads = c.gamma + 1 if heads_needed is None else min(heads_needed, c.gamma + 1)
-        bundles = np.full((T, c.gamma + 1, c.vocab_size), -np.inf)
-        bundles[:, :heads] = self.chained_logits(h0, heads)
+        if logit_rows is None:
+            bundles = np.full((T, c.gamma + 1, c.vocab_size), -np.inf)
+            bundles[:, :heads] = self.chained_logits(h0, heads)
+        else:
+            rows = np.asarray(logit_rows, dtype=np.int64)
+            bundles = np.full((len(rows), c.gamma + 1, c.vocab_size), -np.inf)
+            bundles[:, :heads] = self.chained_logits(h0[rows], heads)
         cache.commit_rows(positions)
         return bundles, queries

@@ -57,7 +57,7 @@ _SIGS = {
     "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, INT, I64, P]),
     "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P, P,
-                           P, P, INT, P, INT, P, SZ, P]),
+                           P, P, INT, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
     "sd_gemv_workspace_bytes": (SZ, [INT, INT]),
     "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),

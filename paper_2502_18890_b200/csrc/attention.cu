@@ -1023,11 +1023,11 @@ __global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnPa
 
 int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
 int tc_set_trace(void* dev_ptr, int force_chunks);
-int tc_n_chunks(int ctx, int Hk);
-int tc_chunk_len(int ctx, int n);
+int tc_split_target(int kv_heads_total);
+int tc_grid_chunks(int ctx_bound, int n_target);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st);
+                     float* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st);
 template <int DH, typename OT>
 __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
                                   int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out);
@@ -1067,7 +1067,8 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
                  const float* rope_cos, const float* rope_sin, const void* k_tree, const void* v_tree,
                  int64_t tree_head_stride, const uint32_t* mask_bits, int mask_words, const int32_t* rows_dev,
                  const int32_t* ctx_dev, const void* tmap_k_host, const void* tmap_v_host, int layer,
-                 void* out, int out_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
+                 int kv_heads_total, void* out, int out_dtype, void* workspace, size_t workspace_bytes,
+                 sd_stream_t stream) {
   SD_REQUIRE(T > 0 && T <= SD_TREE_MAX_ROWS, "sd_attention: T=%d out of range", T);
   SD_REQUIRE(H > 0 && Hk > 0 && H % Hk == 0, "sd_attention: heads");
   SD_REQUIRE(ctx >= 0, "sd_attention: ctx");
@@ -1106,16 +1107,13 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
   auto st = as_stream(stream);
   if (use_tc(tmap_k_host, tmap_v_host, q_dtype, kv_dtype, out_dtype, dh, src_kind, ctx)) {
     // cache chunks + the masked tree rows on tcgen05, then the chunk merge
-    int nc = tc_n_chunks(ctx, Hk);
-    const int chunk = tc_chunk_len(ctx, nc);
-    nc = (ctx + chunk - 1) / chunk;
+    // ctx (host) or its upper bound (ctx_dev) sizes the grid; the splits
+    // themselves are resolved in the kernel from the live context
+    const int n_target = tc_split_target(kv_heads_total > 0 ? kv_heads_total : Hk);
+    const int nc = tc_grid_chunks(ctx, n_target);
     float* ws_lse = p.ws_o + (size_t)nc * T * H * dh;
-    if (ctx_dev) {  // device-resident context: fixed grid, chunking resolved in the kernel
-      nc = tc_n_chunks(ctx, Hk);
-      ws_lse = p.ws_o + (size_t)nc * T * H * dh;
-    }
     int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, ctx_dev, mask_bits,
-                              mask_words, p.ws_o, ws_lse, nc, chunk, st);
+                              mask_words, p.ws_o, ws_lse, nc, n_target, st);
     if (rc) return rc;
     launch_merge<__nv_bfloat16>(p.ws_o, ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out, 128, st);
     return check_launch("sd_attention(tc merge)");

@@ -60,10 +60,18 @@ constexpr uint32_t COL_O = 0;
 constexpr uint32_t COL_S = 256;
 constexpr uint32_t TMEM_COLS = 512;
 
+// keys per split: ctx spread over n_target splits, at least MIN_CHUNK, whole tiles
+__host__ __device__ __forceinline__ int chunk_len(int ctx, int n_target) {
+  int c = (ctx + n_target - 1) / n_target;
+  c = (c + BN - 1) / BN * BN;
+  return c < MIN_CHUNK ? MIN_CHUNK : c;
+}
+
 struct Params {
   const __nv_bfloat16* q;  // [T][H][128]
   int T, H, G;
-  int layer, ctx, chunk, n_chunks;
+  int layer, ctx, n_target;  // n_target: chunks per kv head the split aims for (a function of the
+                             // model's total kv heads, not of the shard: SURVEY H7)
   const int32_t* rows_dev;
   const int32_t* ctx_dev;  // nullable: live cache length (chunking resolved per launch on device)
   const uint32_t* mask;    // [T][mask_words] tree rows (NULL = causal)
@@ -134,22 +142,21 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int rg = blockIdx.z * ROWS;
   if (rg >= GT) return;
   if (tid == 0) trace(0, 60, 0);
-  int ctx = p.ctx, chunk = p.chunk, n_live = p.n_chunks;
-  if (p.ctx_dev) {  // device-resident context: chunk the live length over the fixed grid
-    ctx = *p.ctx_dev;
-    chunk = (ctx + p.n_chunks - 1) / p.n_chunks;
-    chunk = chunk < MIN_CHUNK ? MIN_CHUNK : (chunk + BN - 1) / BN * BN;
-    n_live = ctx > 0 ? (ctx + chunk - 1) / chunk : 1;
-    if ((int)blockIdx.x >= n_live) {  // empty split: weight 0 in the merge
-      for (int r = tid; r < ROWS; r += THREADS) {
-        const int rho = rg + r;
-        if (rho < GT) {
-          const int t = rho / p.G, g = rho - t * p.G;
-          p.ws_lse[((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g] = -INFINITY;
-        }
+  // Split boundaries are a function of the live context and n_target only
+  // (tc_chunk_len), identical for the host- and device-resident context and for
+  // any number of GPUs sharing the kv heads: bitwise cross-P determinism (H7).
+  const int ctx = p.ctx_dev ? *p.ctx_dev : p.ctx;
+  const int chunk = chunk_len(ctx, p.n_target);
+  const int n_live = ctx > 0 ? (ctx + chunk - 1) / chunk : 1;
+  if ((int)blockIdx.x >= n_live) {  // empty split: weight 0 in the merge
+    for (int r = tid; r < ROWS; r += THREADS) {
+      const int rho = rg + r;
+      if (rho < GT) {
+        const int t = rho / p.G, g = rho - t * p.G;
+        p.ws_lse[((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g] = -INFINITY;
       }
-      return;
     }
+    return;
   }
   const bool last = (int)blockIdx.x == n_live - 1;
   const int key_begin = blockIdx.x * chunk;
@@ -566,25 +573,25 @@ int tc_set_trace(void* dev_ptr, int force_chunks) {
   return e == cudaSuccess ? SD_OK : SD_ECUDA;
 }
 
-int tc_n_chunks(int ctx, int Hk) {
+// chunks per kv head the split aims for: one wave of one CTA per SM when the
+// model's kv heads all sit on one GPU (148 SMs); a function of the model, never
+// of the shard, so every GPU count computes the same splits
+int tc_split_target(int kv_heads_total) {
   if (g_force_chunks > 0) return g_force_chunks;
-  // one wave of one CTA per SM over (chunks x kv heads); >= MIN_CHUNK keys per
-  // chunk (short chunks cost more in the split merge than they save)
-  int want = 148 / Hk;
-  const int max_by_tiles = (ctx + tc::MIN_CHUNK - 1) / tc::MIN_CHUNK;
-  if (want > max_by_tiles) want = max_by_tiles;
-  if (want > 148) want = 148;
-  return want < 1 ? 1 : want;
+  const int t = 148 / (kv_heads_total > 0 ? kv_heads_total : 1);
+  return t < 1 ? 1 : t;
 }
 
-int tc_chunk_len(int ctx, int n) {
-  int c = (ctx + n - 1) / n;
-  return (c + tc::BN - 1) / tc::BN * tc::BN;
+// grid width covering every live split of any context <= ctx_bound
+int tc_grid_chunks(int ctx_bound, int n_target) {
+  const int by_ctx = (ctx_bound + tc::MIN_CHUNK - 1) / tc::MIN_CHUNK;
+  const int n = by_ctx < n_target ? by_ctx : n_target;
+  return n < 1 ? 1 : n;
 }
 
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     float* ws_o, float* ws_lse, int n_chunks, int chunk, cudaStream_t st) {
+                     float* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
@@ -597,8 +604,7 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   p.G = H / Hk;
   p.layer = layer;
   p.ctx = ctx;
-  p.chunk = chunk;
-  p.n_chunks = n_chunks;
+  p.n_target = n_target;
   p.rows_dev = rows_dev;
   p.ctx_dev = ctx_dev;
   p.mask = mask;

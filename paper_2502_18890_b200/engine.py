@@ -147,6 +147,15 @@ class Session:
         self.attn_out_v = torch.zeros((self.Tmax, model.H * model.dh), dtype=model.dtype, device=dev)
         self.attn_out_d = torch.zeros((1, model.H * model.dh), dtype=model.dtype, device=dev)
         self.partial: PartialCache | None = None
+        # Session-owned attention workspace (split partials + the draft kernel's
+        # arrival counters, zeroed once): sized for the largest verify context and
+        # the draft slot range up front, so the captured graph never sees it move
+        # and sessions sharing a model never share scratch.
+        slot_cap = config.budget + L.TREE_MAX_DEPTH
+        lib = L.load()
+        self.attn_ws = torch.zeros(max(lib.sd_attention_workspace_bytes(self.Tmax, model.H, model.dh, cap),
+                                       lib.sd_attention_workspace_bytes(1, model.H, model.dh, max(slot_cap, cap))),
+                                   dtype=torch.uint8, device=dev)
         self.result[L.RES_PENDING] = self.tokens[-1]
         self.state[L.ST_PENDING] = self.tokens[-1]
         self.state[L.ST_BASE] = len(self.tokens) - 1
@@ -250,12 +259,12 @@ class Session:
         m, cfg, smp = self.model, self.config, self.config.sampler
         part = self.partial
         q_rot, kt, vt, out = self.q_rot_d, self.kt, self.vt, self.attn_out_d
-        hi = part.slot_cap if graph else part.hi
+        hi = part.slot_cap  # whole slot range (holes masked): eager and replay split the draft identically
 
         def attend(l, qkv, q_pre):
             m.rope_stage(qkv, 1, self.draft_pos, q_rot, None, None, kt, vt, m.dh, 0)
             m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt,
-                        m.dh, None, None, out)
+                        m.dh, None, None, out, ws=self.attn_ws)
             return out
 
         pend = self.result[L.RES_PENDING:L.RES_PENDING + 1]
@@ -292,14 +301,14 @@ class Session:
             def attend(l, qkv, q_pre):
                 m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l], F.k_rot[l], F.v[l], F.head_stride, -1, rows_dev)
                 m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, ctx_max, None, None, None,
-                            F.head_stride, bits, rows_dev, out, F.tmaps, l, ctx_dev=ctx_dev)
+                            F.head_stride, bits, rows_dev, out, F.tmaps, l, ctx_dev=ctx_dev, ws=self.attn_ws)
                 return out
         else:
             def attend(l, qkv, q_pre):
                 m.rope_stage(qkv, T, pos, q_rot, q_pre, F.k_raw[l, :, base:], F.k_rot[l, :, base:],
                              F.v[l, :, base:], F.head_stride, 0, rows_dev)
                 m.attention(q_rot, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                            F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l)
+                            F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l, ws=self.attn_ws)
                 return out
 
         h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
@@ -362,7 +371,9 @@ class Session:
         a = r[L.RES_ACCEPTED]
         ys = r[L.RES_YS:L.RES_YS + a]
         best_v, pick, origin, rows = r[L.RES_BEST], r[L.RES_PICK], r[L.RES_ORIGIN], r[L.RES_ROWS]
-        self.full.positions = self.full.positions[:base] + list(range(base, base + a))
+        pos = self.full.positions  # engine positions are range(len): trim + extend, no O(ctx) rebuild
+        del pos[base:]
+        pos.extend(range(base, base + a))
         self.partial.admit_evict(n - 1, a, self.full, protected=a)
         self.tokens.extend(ys)
         self.emitted.extend(ys)
@@ -383,10 +394,6 @@ class Session:
         launch arguments; see the module docstring). Capture does not run the
         work: step() replays the graph right after."""
         m, F = self.model, self.full
-        # size every workspace for the largest context first: no allocation may
-        # move under the captured pointers
-        m.workspace(max(L.load().sd_attention_workspace_bytes(self.Tmax, m.H, m.dh, F.capacity),
-                        L.load().sd_attention_workspace_bytes(1, m.H, m.dh, self.partial.slot_cap)))
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
         n = len(self.tokens)

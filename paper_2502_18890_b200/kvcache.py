@@ -224,21 +224,68 @@ class PartialCache:
                L.ptr(self.pv), self.layer_stride, self.head_stride, self.num_kv_heads, self.head_dim, L.stream())
 
     # ---- maintenance (kvcache.py:215-225, 332-354) ----
+    # One sd_partial_update launch moves at most SD_TREE_MAX_DEPTH (8) entries
+    # each way; larger admit / evict bursts are split into launches of <= 8
+    # (evictions first, then admissions in position order), which is the same
+    # final state as one launch. All checks run before any host state changes.
+    _BATCH = L.TREE_MAX_DEPTH
+
+    def _launch(self, full: FullCache | None, first_pos: int, new_slots: list[int], evicted: list[int],
+                count_before: int) -> None:
+        B = self._BATCH
+        cnt = count_before
+        for i in range(0, len(evicted), B):
+            gone = evicted[i:i + B]
+            cnt -= len(gone)
+            L.call("sd_partial_update", self.num_layers, self.hi, cnt, 0, 0, L.host_i32([]), len(gone),
+                   L.host_i32(gone), L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap, None,
+                   None, L.dcode(self.dtype), 0, 0, None, None, self.layer_stride, self.head_stride,
+                   self.num_kv_heads, self.head_dim, L.stream())
+        for i in range(0, len(new_slots), B):
+            new = new_slots[i:i + B]
+            cnt += len(new)
+            L.call("sd_partial_update", self.num_layers, self.hi, cnt, first_pos + i, len(new), L.host_i32(new), 0,
+                   L.host_i32([]), L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap,
+                   L.ptr(full.k_raw), L.ptr(full.v), L.dcode(self.dtype), full.layer_stride, full.head_stride,
+                   L.ptr(self.pk), L.ptr(self.pv), self.layer_stride, self.head_stride, self.num_kv_heads,
+                   self.head_dim, L.stream())
+
     def _launch_update(self, full: FullCache, first_pos: int, new_slots: list[int], evicted: list[int]) -> None:
+        """Engine path (<= 8 each way): evict + admit in one launch."""
         L.call("sd_partial_update", self.num_layers, self.hi, self.count, first_pos, len(new_slots),
                L.host_i32(new_slots), len(evicted), L.host_i32(evicted), L.ptr(self.ppos), L.ptr(self.prank),
                L.ptr(self.pscore), self.slot_cap, L.ptr(full.k_raw), L.ptr(full.v), L.dcode(self.dtype),
                full.layer_stride, full.head_stride, L.ptr(self.pk), L.ptr(self.pv), self.layer_stride,
                self.head_stride, self.num_kv_heads, self.head_dim, L.stream())
 
+    def _grow(self, need: int) -> None:
+        """Reallocate the slot arrays for a burst beyond slot_cap (API path only:
+        the engine admits <= 8 per step into budget + 8 slots and never grows, so
+        pointers captured in its CUDA graph stay valid)."""
+        cap = max(need, 2 * self.slot_cap)
+        L_, Hk, dh = self.num_layers, self.num_kv_heads, self.head_dim
+        pk = torch.zeros((L_, Hk, cap, dh), dtype=self.dtype, device=self.device)
+        pv = torch.zeros_like(pk)
+        pk[:, :, :self.slot_cap] = self.pk
+        pv[:, :, :self.slot_cap] = self.pv
+        meta = []
+        for t, fill in ((self.ppos, -1), (self.prank, -1), (self.pscore, float("nan"))):
+            n = torch.full((L_, cap), fill, dtype=t.dtype, device=self.device)
+            n[:, :self.slot_cap] = t
+            meta.append(n)
+        self.pk, self.pv = pk, pv
+        self.ppos, self.prank, self.pscore = meta
+        self.slot_cap = cap
+
     def _take_slots(self, a: int) -> list[int]:
+        short = a - len(self.free) - (self.slot_cap - self.hi)
+        if short > 0:
+            self._grow(self.slot_cap + short)
         out = []
         for _ in range(a):
             if self.free:
                 out.append(self.free.pop())
             else:
-                if self.hi >= self.slot_cap:
-                    raise SinkViolation("partial cache slot capacity exhausted")
                 out.append(self.hi)
                 self.hi += 1
         return out
@@ -250,9 +297,10 @@ class PartialCache:
             return
         if positions != list(range(positions[0], positions[0] + len(positions))):
             raise ValueError("admitted positions must be consecutive")
+        before = self.count
         slots = self._take_slots(len(positions))
         self.count += len(slots)
-        self._launch_update(full, positions[0], slots, [])
+        self._launch(full, positions[0], slots, [], before)
         self.body.extendleft(reversed(slots))
 
     def evict(self, protected: int = 0) -> None:
@@ -262,28 +310,22 @@ class PartialCache:
         if self.count - self.sink_size - over < protected:
             raise SinkViolation("eviction would reach protected entries; body capacity "
                                 f"{self.capacity} is smaller than one iteration's acceptance")
+        before = self.count
         gone = [self.body.pop() for _ in range(over)]
         self.count -= over
-        self._launch_update_evict(gone)
+        self._launch(None, 0, [], gone, before)
         self.free.extend(gone)
-
-    def _launch_update_evict(self, gone):
-        # evict-only: no full-cache copy needed
-        L.call("sd_partial_update", self.num_layers, self.hi, self.count, 0, 0, L.host_i32([]), len(gone),
-               L.host_i32(gone), L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap, None, None,
-               L.dcode(self.dtype), 0, 0, None, None, self.layer_stride, self.head_stride, self.num_kv_heads,
-               self.head_dim, L.stream())
 
     def admit_evict(self, first_pos: int, a: int, full: FullCache, protected: int) -> None:
         """Engine path: admit a consecutive positions and trim to budget in one launch."""
         over = self.count + a - self.budget
-        gone = []
-        if over > 0:
-            if self.count + a - self.sink_size - over < protected:
-                raise SinkViolation("eviction would reach protected entries; body capacity "
-                                    f"{self.capacity} is smaller than one iteration's acceptance")
-            gone = [self.body.pop() for _ in range(over)]
-            self.free.extend(gone)
+        if over > 0 and self.count + a - self.sink_size - over < protected:
+            raise SinkViolation("eviction would reach protected entries; body capacity "
+                                f"{self.capacity} is smaller than one iteration's acceptance")
+        if a > self._BATCH or max(over, 0) > self._BATCH:
+            raise ValueError(f"admit_evict moves at most {self._BATCH} entries each way per step")
+        gone = [self.body.pop() for _ in range(over)] if over > 0 else []
+        self.free.extend(gone)
         slots = self._take_slots(a)
         self.count += a - len(gone)
         self._launch_update(full, first_pos, slots, gone)

@@ -406,19 +406,24 @@ class TinyTransformer:
         return all_gather_heads(o, self.world, self.group)
 
     def attention(self, q_rot, T, src_kind, k_cache, v_cache, head_stride, ctx, ranks, k_tree, v_tree,
-                  tree_head_stride, mask_bits, rows_dev, out, tmaps=None, layer=0, ctx_dev=None):
+                  tree_head_stride, mask_bits, rows_dev, out, tmaps=None, layer=0, ctx_dev=None, ws=None):
         """sd_attention; with `tmaps` (FullCache.tmaps) and bf16/dh=128 the cache
         chunks run on the tcgen05 kernel of `layer`. With `ctx_dev` the live
-        context is read on device and `ctx` is its upper bound (graph replay)."""
+        context is read on device and `ctx` is its upper bound (graph replay).
+        `ws`: caller-owned workspace (a Session's, sized once and captured in its
+        graph); default the model's scratch, which may be reallocated."""
         nbytes = L.load().sd_attention_workspace_bytes(T, self.H, self.dh, ctx)
-        ws = self.workspace(nbytes)
+        if ws is None:
+            ws = self.workspace(nbytes)
+        elif ws.numel() < nbytes:
+            raise ValueError(f"attention workspace {ws.numel()} B < {nbytes} B")
         kd = L.dcode(self.dtype)
         tk, tv = tmaps if (tmaps is not None and self.use_tc) else (None, None)
         L.call("sd_attention", L.ptr(q_rot), kd, T, self.H, self.Hk, self.dh, src_kind, L.ptr(k_cache),
                L.ptr(v_cache), kd, head_stride, ctx, L.ptr(ranks), L.ptr(self.rope_cos), L.ptr(self.rope_sin),
                L.ptr(k_tree), L.ptr(v_tree), tree_head_stride, L.ptr(mask_bits),
-               L.MASK_WORDS if mask_bits is not None else 0, L.ptr(rows_dev), L.ptr(ctx_dev), tk, tv, layer, L.ptr(out), kd,
-               L.ptr(ws), ws.numel(), L.stream())
+               L.MASK_WORDS if mask_bits is not None else 0, L.ptr(rows_dev), L.ptr(ctx_dev), tk, tv, layer,
+               self.config.num_kv_heads, L.ptr(out), kd, L.ptr(ws), ws.numel(), L.stream())
 
     def rope_stage(self, qkv, T, positions_dev, q_rot, q_pre, k_raw, k_rot, v, head_stride, row_offset,
                    rows_dev=None):

@@ -75,7 +75,7 @@ def test_verify_attention_tree(lib, dtype, ctx, T, H, Hk, dh):
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, T, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, lib.ptr(bits), lib.MASK_WORDS,
-             None, None, None, None, 0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+             None, None, None, None, 0, 0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
     # oracle on the same (rounded) inputs
     Kr = kt.double().cpu().numpy().transpose(1, 0, 2)
     Vr = vt.double().cpu().numpy().transpose(1, 0, 2)
@@ -120,7 +120,7 @@ def test_verify_attention_tcgen05(lib, ctx, T, H, Hk, layer):
         lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
                  F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
                  F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, tm[0], tm[1],
-                 layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
+                 layer, 0, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
         outs.append(out.double().cpu().numpy().reshape(T, H, dh))
     Kr = F.k_rot[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
     Vr = F.v[layer].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
@@ -169,11 +169,11 @@ def test_attention_ctx_dev_matches_host_ctx(lib, tc, ctx):
             lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
                      F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(),
                      F.v[layer, :, ctx:].data_ptr(), F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, tm[0],
-                     tm[1], layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
+                     tm[1], layer, 0, lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
         else:
             lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
                      F.head_stride, upper, None, None, None, None, None, F.head_stride, lib.ptr(bits), lib.MASK_WORDS,
-                     None, lib.ptr(ctx_dev), tm[0], tm[1], layer, lib.ptr(out), 1, lib.ptr(ws), ws.numel(),
+                     None, lib.ptr(ctx_dev), tm[0], tm[1], layer, 0, lib.ptr(out), 1, lib.ptr(ws), ws.numel(),
                      lib.stream())
         outs.append(out.float())
     assert torch.isfinite(outs[1]).all()
@@ -204,7 +204,7 @@ def test_attention_rows_dev_padding(lib):
         ws = torch.zeros(lib.load().sd_attention_workspace_bytes(TT, H, dh, ctx), dtype=torch.uint8, device=dev)
         lib.call("sd_attention", lib.ptr(qt), 0, TT, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), 0, cap * dh, ctx, None,
                  None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, lib.ptr(rd),
-                 None, None, None, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
+                 None, None, None, 0, 0, lib.ptr(out), 0, lib.ptr(ws), ws.numel(), lib.stream())
         outs.append(out)
     assert torch.equal(outs[0][:Tl], outs[1])
     assert torch.all(outs[0][Tl:] == 0)
@@ -268,7 +268,7 @@ def test_decode_attention_full_cache(lib, dtype, ctx):
     kd = lib.dcode(dtype)
     lib.call("sd_attention", lib.ptr(qt), kd, 1, H, Hk, dh, 0, lib.ptr(kt), lib.ptr(vt), kd, cap * dh, ctx, None,
              None, None, kt[:, ctx:].data_ptr(), vt[:, ctx:].data_ptr(), cap * dh, None, 0, None, None, None, None, 0,
-             lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
+             0, lib.ptr(out), kd, lib.ptr(ws), ws.numel(), lib.stream())
     Kr = kt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]
     Vr = vt.double().cpu().numpy().transpose(1, 0, 2)[: ctx + 1]
     want = attend_oracle(qt.double().cpu().numpy(), Kr, Vr, np.ones((1, ctx + 1), dtype=bool))

@@ -1,0 +1,350 @@
+"""Parity of the timed product path at production head shapes.
+
+Everything bench.py times runs here at the LLaMA3.1-8B head layout (cfg3:
+d=4096, H=32, Hk=8, G=4, dh=128, V=128256, reference architecture, bf16
+weights drawn by the reference initialiser, model.py:195-205) with 2 layers,
+so the kernels that only engage at dh=128 / bf16 — tcgen05 verification
+attention (causal prefill blocks and tree rows), the rank-RoPE draft kernel,
+the cluster sampler, single-row weight streaming, CUDA-graph replay with PDL —
+are checked against the fp64 oracle running the same bf16-rounded weights
+(SURVEY §8(c) layering (2) and (3)):
+
+* logits / queries within 1e-2 relative (north star, bf16);
+* the greedy token sequence identical wherever the oracle's top-1 margin
+  exceeds 2e-2, checked at every position by teacher forcing
+  (oracle/checks.py; reference guarantee engine.py:13-18,
+  tests/test_engine.py:112-162);
+* graph replay == eager step bit for bit at this shape, across refreshes,
+  with a second session prefilling on the same model in between (sessions
+  own their attention workspace).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import checks as OC
+from oracle import kvcache as OK
+from oracle import model as OM
+from oracle import sampling as OS
+
+pytestmark = pytest.mark.gpu
+
+CFG3_2L = dict(vocab_size=128256, num_layers=2, hidden_dim=4096, num_heads=32, num_kv_heads=8, gamma=3,
+               max_positions=8192, init_seed=0)
+BF16_TOL = 1e-2      # north star: logits within 1e-2 relative in bf16
+MARGIN_TOL = 2e-2    # a token is decided when its oracle top-1 margin exceeds 2x that
+
+
+def rel_err(got, want):
+    got, want = np.asarray(got, dtype=np.float64), np.asarray(want, dtype=np.float64)
+    return float(np.max(np.abs(got - want)) / max(1e-30, np.max(np.abs(want))))
+
+
+@pytest.fixture(scope="module")
+def prod():
+    import paper_2502_18890_b200 as sd
+    m = sd.TinyTransformer(sd.ModelConfig(**CFG3_2L), dtype=torch.bfloat16, init="reference")
+    om = OM.TinyTransformer(OM.ModelConfig(**CFG3_2L), params=m.parameters_host())
+    return m, om
+
+
+def engine_cfgs(target, budget=160, sink=32, k=20):
+    import paper_2502_18890_b200 as sd
+    smp = sd.SamplerConfig(theta=1.2, window=1024, truncation=sd.Truncation.min_p(1.0))
+    dcfg = sd.EngineConfig(target_length=target, sink_size=sink, budget=budget, tree=sd.TreeConfig((1, 3, 3, 3)),
+                           k=k, sampler=smp)
+    osmp = OS.SamplerConfig(theta=1.2, window=1024, truncation=OS.Truncation.min_p(1.0))
+    return dcfg, osmp
+
+
+def test_prefill_and_tree_forward_cfg3_heads(prod):
+    """Batched causal prefill (tcgen05 causal blocks, 128 rows each) and a
+    41-row tree forward (tcgen05 tree mask) vs the oracle forward."""
+    import paper_2502_18890_b200 as sd
+    from oracle.tree import closure
+    m, om = prod
+    V = CFG3_2L["vocab_size"]
+    P = 600
+    prompt = sd.rng.random_prompt(P, V, seed=3)
+    cache = m.new_cache(P + 64)
+    r = m.forward(sd.ForwardRequest(tokens=prompt, positions=list(range(P)), cache=cache, heads_needed=1))
+    rows = [0, 127, 128, 300, P - 2, P - 1]
+    ocache = om.new_cache()
+    ob, oq = om.forward(prompt, list(range(P)), ocache, heads_needed=1, logit_rows=rows)
+    assert rel_err(r.queries.cpu().numpy(), oq) < BF16_TOL
+    assert rel_err(r.bundles[rows, 0].cpu().numpy(), ob[:, 0]) < BF16_TOL
+    # tree of the engine's shape: [1,3,3,3] trie (DFS order), 40 nodes + root
+    par, depth = [-1], [0]
+    for a in range(3):
+        par.append(0); depth.append(1); pa = len(par) - 1
+        for b in range(3):
+            par.append(pa); depth.append(2); pb = len(par) - 1
+            for c in range(3):
+                par.append(pb); depth.append(3)
+    T = len(par)
+    assert T == 41
+    g = np.random.default_rng(7)
+    toks = [int(t) for t in g.integers(0, V, size=T)]
+    mask = np.zeros((T, P + T), dtype=bool)
+    mask[:, :P] = True
+    mask[:, P:] = closure(par)
+    pos = [P + d for d in depth]
+    r2 = m.forward(sd.ForwardRequest(tokens=toks, positions=pos, cache=cache, attention_mask=mask, heads_needed=1))
+    ob2, oq2 = om.forward(toks, pos, ocache, mask, heads_needed=1)
+    assert rel_err(r2.bundles[:, 0].cpu().numpy(), ob2[:, 0]) < BF16_TOL
+    assert rel_err(r2.queries.cpu().numpy(), oq2) < BF16_TOL
+
+
+def test_session_greedy_tokens_vs_oracle_cfg3_heads(prod):
+    """The timed path (graph replay + PDL, tcgen05 verify, draft kernel over a
+    budgeted partial cache with refreshes) emits the oracle's greedy tokens
+    wherever the oracle's margin decides them."""
+    import paper_2502_18890_b200 as sd
+    m, om = prod
+    dcfg, osmp = engine_cfgs(target=320)
+    prompt = sd.rng.random_prompt(520, CFG3_2L["vocab_size"], seed=1)
+    s = sd.Session(m, prompt, dcfg)
+    while not s.done:
+        s.step()
+    assert s._graph is not None and s.device_error() == 0
+    assert sum(r.refreshed for r in s.records) >= 2
+    assert sum(r.accepted for r in s.records) == len(s.emitted)
+    bad, undecided = OC.greedy_mismatches(om, prompt, s.emitted, osmp, MARGIN_TOL)
+    assert not bad, f"decided tokens differ (i, device, oracle, margin): {bad[:5]}"
+    assert undecided < len(s.emitted) // 4, f"{undecided} of {len(s.emitted)} positions undecided"
+
+
+def _rec(r):
+    return [r.accepted, r.ngram_accepted, r.origin, r.matched, list(r.tokens), r.refreshed, r.draft_ctx,
+            r.verify_ctx, r.verify_rows, r.path_index]
+
+
+def test_graph_replay_equals_eager_cfg3_heads(prod):
+    """Graph replay (device-resident context, fixed grids, PDL) is the same
+    computation as the eager step at dh=128 / bf16 — bit for bit — and a
+    second session prefilling on the same model after the capture does not
+    disturb the captured session (per-session workspace)."""
+    import paper_2502_18890_b200 as sd
+    m, _ = prod
+    dcfg, _ = engine_cfgs(target=220)
+    prompt = sd.rng.random_prompt(540, CFG3_2L["vocab_size"], seed=2)
+    a = sd.Session(m, prompt, dcfg, graph=False)
+    b = sd.Session(m, prompt, dcfg, graph=True)
+    other = None
+    while not a.done:
+        ra, rb = a.step(), b.step()
+        assert _rec(ra) == _rec(rb), f"step {ra.step}"
+        if len(b.records) == 3:
+            assert b._graph is not None
+            # a longer prompt: its causal prefill needs more attention scratch than the
+            # captured verify step, which used to reallocate the shared buffer
+            other = sd.Session(m, sd.rng.random_prompt(900, CFG3_2L["vocab_size"], seed=9), dcfg)
+    assert a.emitted == b.emitted
+    assert a.partial.positions == b.partial.positions
+    assert torch.equal(a.q_sum, b.q_sum)
+    n = len(a.full)
+    assert torch.equal(a.full.k_rot[:, :, :n], b.full.k_rot[:, :, :n])
+    assert torch.equal(a.full.v[:, :, :n], b.full.v[:, :, :n])
+    assert other is not None and other.device_error() == 0
+
+
+def _tc_attention(lib, F, layer, qt, T, H, Hk, ctx, bits, kv_total=0):
+    dh = 128
+    out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
+    ws = torch.zeros(lib.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
+    lib.call("sd_attention", lib.ptr(qt), 1, T, H, Hk, dh, 0, lib.ptr(F.k_rot[layer]), lib.ptr(F.v[layer]), 1,
+             F.head_stride, ctx, None, None, None, F.k_rot[layer, :, ctx:].data_ptr(), F.v[layer, :, ctx:].data_ptr(),
+             F.head_stride, lib.ptr(bits), lib.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], layer, kv_total,
+             lib.ptr(out), 1, lib.ptr(ws), ws.numel(), lib.stream())
+    return out
+
+
+def _random_tree_bits(g, T):
+    from paper_2502_18890_b200.model import mask_bits_from_bool
+    parent = [-1] + [int(g.integers(0, i)) for i in range(1, T)]
+    mask = np.zeros((T, T), dtype=bool)
+    for i in range(T):
+        j = i
+        while j >= 0:
+            mask[i, j] = True
+            j = parent[j]
+    return mask, torch.as_tensor(mask_bits_from_bool(mask), device="cuda")
+
+
+@pytest.mark.parametrize("ctx,T,H,Hk", [(54096, 41, 32, 8), (104000, 41, 32, 8), (54096, 101, 32, 8),
+                                         (12000, 41, 12, 2), (20000, 101, 12, 2), (30000, 41, 40, 8)])
+def test_tcgen05_verify_long_context(ctx, T, H, Hk):
+    """tcgen05 verification at the contexts a 100K generation reaches (and
+    cfg2's G=6 / Hk=2, cfg5's G=5) vs the fp64 oracle, per kv head sampled."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200 import _lib as lib
+    g = np.random.default_rng(ctx + T)
+    dh = 128
+    cap = ctx + T + 8
+    F = FullCache(1, Hk, dh, capacity=cap, dtype=torch.bfloat16)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(ctx)
+    F.k_rot.normal_(generator=gen)
+    F.v.normal_(generator=gen)
+    mask, bits = _random_tree_bits(g, T)
+    qt = (torch.randn((T, H, dh), generator=gen, device="cuda") * (2.0 / np.sqrt(dh))).to(torch.bfloat16)
+    out = _tc_attention(lib, F, 0, qt, T, H, Hk, ctx, bits).double().cpu().numpy().reshape(T, H, dh)
+    G = H // Hk
+    vis = np.zeros((T, ctx + T), dtype=bool)
+    vis[:, :ctx] = True
+    vis[:, ctx:] = mask
+    q = qt.double().cpu().numpy()
+    for kvh in sorted({0, Hk - 1}):
+        K = F.k_rot[0, kvh, :ctx + T].double().cpu().numpy()
+        Vv = F.v[0, kvh, :ctx + T].double().cpu().numpy()
+        qh = q[:, kvh * G:(kvh + 1) * G].reshape(T * G, dh)
+        s = qh @ K.T
+        s = np.where(np.repeat(vis, G, axis=0), s, -np.inf)
+        w = np.exp(s - s.max(-1, keepdims=True))
+        want = (w @ Vv) / w.sum(-1, keepdims=True)
+        got = out[:, kvh * G:(kvh + 1) * G].reshape(T * G, dh)
+        assert rel_err(got, want) < BF16_TOL, f"kv head {kvh}"
+
+
+def test_tcgen05_splits_independent_of_shard_count():
+    """H7: a kv head's output is bitwise identical whether the call holds all 8
+    kv heads or a 2- / 4-head shard of them (kv_heads_total fixes the split)."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200 import _lib as lib
+    g = np.random.default_rng(1)
+    ctx, T, G, Hk, dh = 30000, 41, 4, 8, 128
+    F = FullCache(1, Hk, dh, capacity=ctx + T + 8, dtype=torch.bfloat16)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(1)
+    F.k_rot.normal_(generator=gen)
+    F.v.normal_(generator=gen)
+    _, bits = _random_tree_bits(g, T)
+    qt = (torch.randn((T, G * Hk, dh), generator=gen, device="cuda") * 0.2).to(torch.bfloat16)
+    full = _tc_attention(lib, F, 0, qt, T, G * Hk, Hk, ctx, bits).view(T, Hk, G * dh)
+    for P in (2, 4):
+        hl = Hk // P
+        for r in range(P):
+            Fs = FullCache(1, hl, dh, capacity=F.capacity, dtype=torch.bfloat16)
+            Fs.k_rot.copy_(F.k_rot[:, r * hl:(r + 1) * hl])
+            Fs.v.copy_(F.v[:, r * hl:(r + 1) * hl])
+            qs = qt[:, r * hl * G:(r + 1) * hl * G].contiguous()
+            part = _tc_attention(lib, Fs, 0, qs, T, hl * G, hl, ctx, bits, kv_total=Hk).view(T, hl, G * dh)
+            assert torch.equal(part, full[:, r * hl:(r + 1) * hl]), (P, r)
+
+
+def test_importance_scores_dh128_and_topk_at_scale():
+    """Eq. 2 scoring at cfg3 head shapes over a 50K-row full cache vs the
+    oracle (kvcache.py:243-265), and the top-K selection of those scores vs
+    the oracle's (-score, pos) order (kvcache.py:286), bit-exact."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200 import _lib as lib
+    from paper_2502_18890_b200.kvcache import layer_scores
+    Lr, Hk, H, dh, n, sink, budget = 2, 8, 32, 128, 50000, 32, 4096
+    F = FullCache(Lr, Hk, dh, capacity=n + 8, dtype=torch.bfloat16)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(5)
+    F.k_raw.normal_(generator=gen)
+    q = torch.randn((Lr, H, dh), generator=gen, device="cuda")
+    sc = layer_scores(F, q, H, sink, n)
+    for l in range(Lr):
+        K = F.k_raw[l, :, sink:n].double().cpu().numpy().transpose(1, 0, 2)  # [n-sink, Hk, dh]
+        want = OK.importance_scores(q[l].double().cpu().numpy(), K, H // Hk)
+        assert rel_err(sc[l].cpu().numpy(), want) < 1e-5
+    part = sd_partial(F, sc, sink, budget, n)
+    got = part.ppos[:, :budget].cpu().numpy()
+    for l in range(Lr):
+        s64 = sc[l].double().cpu().numpy()
+        want = list(range(sink)) + OK.select_body(s64, sink, n, budget - sink)
+        assert got[l].tolist() == want
+        kk = part.pk[l, :, :budget].cpu()
+        assert torch.equal(kk, F.k_raw[l, :, torch.as_tensor(want)].cpu())
+
+
+def sd_partial(F, scores, sink, budget, upto):
+    from paper_2502_18890_b200.kvcache import PartialCache
+    p = PartialCache(sink, budget, F.num_layers, F.num_kv_heads, F.head_dim, F.dtype, F.device)
+    p.build_topk(F, scores, upto)
+    return p
+
+
+def test_partial_admit_burst_like_reference():
+    """admit of more than 8 positions at once and the eviction after it
+    behave like the reference (kvcache.py:215-225, 332-354): no device cap."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200.kvcache import SinkViolation, evict_to_budget, mirror_partial
+    F = FullCache(2, 2, 16, capacity=200, dtype=torch.float32)
+    F.k_raw.normal_()
+    F.v.normal_()
+    F.commit_rows(range(100))
+    part = mirror_partial(F, 4, 40, upto=30)
+    oF = OK.FullCache(2, 2, 16, cap=200)
+    oF.reserve(100)
+    for l in range(2):
+        oF.k_raw[l, :100] = F.k_raw[l, :, :100].permute(1, 0, 2).double().cpu().numpy()
+        oF.v[l, :100] = F.v[l, :, :100].permute(1, 0, 2).double().cpu().numpy()
+    oF.commit_rows(range(100))
+    ref = OK.mirror_partial(oF, 4, 40, upto=30)
+    assert part.positions == ref.positions
+    part.admit(range(30, 55), F)  # 25 at once
+    ref.admit(list(range(30, 55)), oF)
+    assert len(part) == 55 and part.positions == ref.positions
+    evict_to_budget(part, protected=25)
+    OK.evict_to_budget(ref, protected=25)
+    assert part.positions == ref.positions
+    for l in range(2):
+        np.testing.assert_array_equal(part.k[l].double().cpu().numpy(), ref.k[l])
+        np.testing.assert_array_equal(part.v[l].double().cpu().numpy(), ref.v[l])
+    with pytest.raises(SinkViolation):
+        part.admit(range(55, 100), F)
+        evict_to_budget(part, protected=45)
+
+
+def test_cluster_sampler_vs_oracle_tree_rows():
+    """The engine-path sampler (8-CTA cluster per row) against the oracle's
+    node masks + penalised softmax + truncation + inverse-CDF draw at full
+    vocabulary (engine.py:155-181, 237-245; sampling.py:142-224)."""
+    from oracle.tree import build_tree
+    from paper_2502_18890_b200 import _lib as Lb
+    from paper_2502_18890_b200.sampling import PenaltyWindow
+    g = np.random.default_rng(11)
+    V, W, depth = 128256, 1024, 4
+    st = torch.zeros(16, dtype=torch.int64, device="cuda")
+    dw = PenaltyWindow(W, V, state=st)
+    hist = g.integers(0, 2000, size=1100).tolist()  # ring wrapped, repeated tokens
+    dw.push_many(hist)
+    ow = OS.PenaltyWindow(W, V)
+    for t in hist:
+        ow.push(t)
+    per_head = [[int(x) for x in g.choice(2000, w, replace=False)] for w in (1, 3, 3, 3)]
+    tree = build_tree(per_head, [], (1, 3, 3, 3))
+    rec = torch.zeros(Lb.tree_layout()["TOTAL"], dtype=torch.int32, device="cuda")
+    flat = torch.tensor([t for c in per_head for t in c], dtype=torch.int32, device="cuda")
+    n = 5000
+    Lb.call("sd_tree_build", Lb.ptr(flat), Lb.host_i32([1, 3, 3, 3]), depth, None, None, 0, None, n - 1,
+            Lb.ptr(rec), Lb.stream())
+    T = 41
+    masks = OS.node_masks(ow, tree.tokens, tree.parent, depth)
+    for trunc, val in (("min_p", 0.1), ("top_p", 0.9), ("min_p", 1.0)):
+        logits = g.normal(scale=4.0, size=(T, V)).astype(np.float32)
+        # sharpen a few rows so truncation bites at a handful of tokens
+        logits[::5, :50] += 12.0
+        smp = OS.SamplerConfig(temperature=1.0, theta=1.2, window=W, truncation=OS.Truncation(trunc, val), seed=4)
+        dists = OS.penalized_probs_masked(logits.astype(np.float64), masks, smp)
+        want = []
+        for r in range(T):
+            pos = n if r == 0 else n + tree.depth[r - 1] + 1
+            want.append(OS.sample_at(OS.truncate(dists[r], smp.truncation), pos, smp.seed))
+        y = torch.full((T,), -1, dtype=torch.int32, device="cuda")
+        a = Lb.SampleArgs()
+        a.rows, a.V, a.in_kind = T, V, Lb.IN_LOGITS_F32
+        a.temperature, a.theta, a.ctrl_style = 1.0, 1.2, 0
+        a.member_kind = Lb.MEMBER_TREE
+        a.win_count, a.win_ring, a.state, a.window = Lb.ptr(dw.count), Lb.ptr(dw.ring), Lb.ptr(st), W
+        a.tree, a.depth = Lb.ptr(rec), depth
+        a.trunc_kind = {"min_p": Lb.TRUNC_MIN_P, "top_p": Lb.TRUNC_TOP_P}[trunc]
+        a.trunc_value, a.eta_alpha = val, -1.0
+        a.seed, a.n = 4, n
+        a.token_out = Lb.ptr(y)
+        Lb.call("sd_sample_rows", Lb.ptr(torch.as_tensor(logits, device="cuda")), a, Lb.stream())
+        assert y.cpu().tolist() == want, trunc

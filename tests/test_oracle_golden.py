@@ -154,3 +154,26 @@ def test_ar_golden():
     from dataclasses import replace
     ar = OE.generate_ar(model, run["prompt"], replace(ecfg, target_length=len(run["ar"])))
     assert ar == run["ar"]
+
+
+def test_teacher_forced_check_on_oracle_ar():
+    """oracle/checks.py: the oracle's own AR output passes its teacher-forced
+    check at every position (and a corrupted token is caught)."""
+    from oracle import checks as OC
+    from oracle import engine as OE
+    from oracle import model as OM
+    from oracle import sampling as OS
+    mc = OM.ModelConfig(vocab_size=97, num_layers=2, hidden_dim=32, num_heads=4, num_kv_heads=2, gamma=3, init_seed=4)
+    om = OM.TinyTransformer(mc)
+    smp = OS.SamplerConfig(theta=1.2, window=16, truncation=OS.Truncation.min_p(1.0))
+    cfg = OE.EngineConfig(target_length=40, sink_size=4, budget=16, sampler=smp)
+    prompt = [int(x) for x in np.random.default_rng(0).integers(0, 97, size=12)]
+    out = OE.generate_ar(om, prompt, cfg)
+    res = OC.teacher_forced(om, prompt, out, smp)
+    assert [w for _, w, _ in res] == out
+    bad, _ = OC.greedy_mismatches(om, prompt, out, smp, 0.0)
+    assert bad == []
+    wrong = list(out)
+    wrong[5] = (wrong[5] + 1) % 97
+    bad, _ = OC.greedy_mismatches(om, prompt, wrong, smp, 0.0)
+    assert bad and bad[0][0] == 5

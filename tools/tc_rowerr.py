@@ -20,7 +20,7 @@ ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=tor
 L.call("sd_debug_tc_trace", None, force)
 L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
        None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
-       L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
+       L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
 got = out.double().cpu().numpy().reshape(T, H, dh)
 K = F.k_rot[0].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]
 V = F.v[0].double().cpu().numpy().transpose(1, 0, 2)[: ctx + T]

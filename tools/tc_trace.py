@@ -29,7 +29,7 @@ tr = torch.zeros((4, 64, 8), dtype=torch.int64, device="cuda")
 def run():
     L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
            None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
-           L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
+           L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
 
 
 L.call("sd_debug_tc_trace", None, force)

@@ -13,7 +13,7 @@ for (ctx, T, Hk) in [(54096, 41, 8), (54096, 20, 8), (54096, 101, 8), (4096, 41,
     def run():
         L.call("sd_attention", L.ptr(q), 1, T, H, Hk, dh, 0, L.ptr(F.k_rot[0]), L.ptr(F.v[0]), 1, F.head_stride, ctx, None,
                None, None, F.k_rot[0, :, ctx:].data_ptr(), F.v[0, :, ctx:].data_ptr(), F.head_stride, L.ptr(bits),
-               L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
+               L.MASK_WORDS, None, None, F.tmaps[0], F.tmaps[1], 0, 0, L.ptr(out), 1, L.ptr(ws), ws.numel(), L.stream())
     for _ in range(3): run()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(); e0.record()
