@@ -75,13 +75,13 @@ def test_prefill_and_tree_forward_cfg3_heads(prod):
     assert rel_err(r.queries.cpu().numpy(), oq) < BF16_TOL
     assert rel_err(r.bundles[rows, 0].cpu().numpy(), ob[:, 0]) < BF16_TOL
     # tree of the engine's shape: [1,3,3,3] trie (DFS order), 40 nodes + root
-    par, depth = [-1], [0]
+    par, depth = [-1, 0], [0, 1]  # row 0 = pending token, row 1 = the width-1 first draft level
     for a in range(3):
-        par.append(0); depth.append(1); pa = len(par) - 1
+        par.append(1); depth.append(2); pa = len(par) - 1
         for b in range(3):
-            par.append(pa); depth.append(2); pb = len(par) - 1
+            par.append(pa); depth.append(3); pb = len(par) - 1
             for c in range(3):
-                par.append(pb); depth.append(3)
+                par.append(pb); depth.append(4)
     T = len(par)
     assert T == 41
     g = np.random.default_rng(7)
