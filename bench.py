@@ -240,6 +240,7 @@ def main():
     alg_flops = 4 * rows * H * dh * ctx
     achieved = alg_bytes / attn["avg_s"] / 1e9
     bound = "hbm" if (alg_flops / (tflops * 1e12)) < (alg_bytes / (hbm * 1e9)) else "tensor"
+    kernels = {"draft_attention": time_draft_attention(sess, model, hbm, reps=args.attn_reps)}
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -263,6 +264,7 @@ def main():
                      "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes, "alg_flops_per_launch": alg_flops,
                      "avg_launch_us": attn["avg_s"] * 1e6, "rows": rows,
                      "share_of_step": attn["avg_s"] * model.config.num_layers / (dev_s / args.steps)},
+        "kernels": kernels,
         "clocks": clocks,
         "alpha": statistics.mean(r.accepted for r in recs) / 4.0,
         "mean_verify_rows": statistics.mean(r.verify_rows for r in recs),
@@ -306,6 +308,54 @@ def time_verify_attention(sess, model, rows, ctx, reps=3):
     e1.record(st)
     torch.cuda.synchronize()
     return {"avg_s": e0.elapsed_time(e1) / 1e3 / n, "launches": n}
+
+
+def _graph_time(fn, reps):
+    """Seconds per call of fn() (a run of kernel launches), captured once in a
+    CUDA graph and replayed `reps` times between CUDA events on the replay
+    stream: device time without the host's per-launch overhead."""
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s):
+        fn()  # warm on the capture stream
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(s)
+        for _ in range(reps):
+            g.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def time_draft_attention(sess, model, hbm, reps=3):
+    """CUDA-event time of the draft attention alone (the step's own call: whole
+    slot range, rank-RoPE, fused merge), one launch per layer, back to back."""
+    import torch
+    part = sess.partial
+    q = torch.randn((1, model.H, model.dh), device="cuda").mul_(0.1).to(model.dtype)
+    out = torch.empty((1, model.H * model.dh), dtype=model.dtype, device="cuda")
+    kt = torch.randn((model.Hk, model.dh), device="cuda").to(model.dtype)
+    vt = torch.randn_like(kt)
+    hi = part.slot_cap
+
+    def one(l):
+        model.attention(q, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt, model.dh,
+                        None, None, out, part.tmaps, l, ws=sess.attn_ws)
+    avg = _graph_time(lambda: [one(l) for l in range(model.config.num_layers)], reps) / model.config.num_layers
+    m = part.count
+    alg = 2 * (m + 1) * model.Hk * model.dh * 2 + 2 * model.H * model.dh * 2
+    return {"bound": "hbm", "achieved": alg / avg / 1e9, "peak": hbm, "unit": "GB/s", "frac": alg / avg / 1e9 / hbm,
+            "avg_launch_us": avg * 1e6, "alg_bytes_per_launch": alg, "live_slots": m, "slot_range": hi,
+            "kernel": "sd_attention draft (tensor-core, rank-RoPE, fused merge), one layer"}
 
 
 if __name__ == "__main__":

@@ -128,6 +128,13 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh,
  * tcgen05 tensor-core kernel (TMA-fed, accumulators in TMEM) of `layer`;
  * k_cache / v_cache must then be that layer's slice of the described arrays. */
 int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host);
+/* Same descriptor with 64-slot boxes, over a partial cache's K_raw / V slot
+ * arrays [L][Hk][slot_cap][128] bf16. When sd_attention gets these with
+ * src_kind 1 (T == 1, bf16, head_dim 128, H / Hk <= 16), the draft attention
+ * runs on the TMA-fed warp-level tensor-core kernel of `layer` (rank-RoPE in
+ * registers, split merge and the pending row fused; replaces the reference's
+ * draft_view + causal forward, kvcache.py:227-240, model.py:301-305). */
+int sd_make_slot_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host);
 /* DEBUG ONLY (the one piece of global state): route clock64 event stamps of
  * the tensor-core kernel's first CTA to int64 [4][64][8] at trace_dev (NULL
  * disables); force_chunks > 0 overrides the chunk count. Not used by the

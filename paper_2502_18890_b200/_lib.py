@@ -12,7 +12,7 @@ import os
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libswiftdec_b200.so")
+LIB_PATH = os.environ.get("SD_LIB_OVERRIDE") or os.path.join(HERE, "libswiftdec_b200.so")  # override: tools/ experiments only
 
 SD_F32, SD_BF16, SD_F64 = 0, 1, 2
 TREE_MAX_ROWS, TREE_MAX_PATHS, TREE_MAX_DEPTH, MASK_WORDS = 256, 512, 8, 8
@@ -59,6 +59,7 @@ _SIGS = {
     "sd_attention": (INT, [P, INT, INT, INT, INT, INT, INT, P, P, INT, I64, INT, P, P, P, P, P, I64, P, INT, P, P,
                            P, P, INT, INT, P, INT, P, SZ, P]),
     "sd_make_kv_tmap": (INT, [P, INT, INT, INT, INT, P]),
+    "sd_make_slot_tmap": (INT, [P, INT, INT, INT, INT, P]),
     "sd_gemv_workspace_bytes": (SZ, [INT, INT]),
     "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_gemv_addnorm": (INT, [P, INT, P, INT, P, P, F32, P, INT, P, SZ, P]),
@@ -126,7 +127,7 @@ def require_cuda():
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
-              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
+              "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_make_slot_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
               "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes"}
 launch_count = 0
 

@@ -1021,7 +1021,10 @@ __global__ void __launch_bounds__(256, GM == 4 ? 2 : 1) draft_attn_kernel(AttnPa
   if (tid == 0) counters[kvh] = 0;  // ready for the next launch / graph replay
 }
 
-int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out);
+int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out, int box_rows);
+int launch_draft_mma(const void* tmap_k, const void* tmap_v, const void* q, int H, int Hk, int kv_heads_total,
+                     int layer, int hi, const int32_t* ranks, const void* k_self, const void* v_self,
+                     int64_t self_stride, float* ws_o, int* counters, void* out, cudaStream_t st);
 int tc_set_trace(void* dev_ptr, int force_chunks);
 int tc_split_target(int kv_heads_total);
 int tc_grid_chunks(int ctx_bound, int n_target);
@@ -1059,7 +1062,12 @@ int sd_debug_tc_trace(void* trace_dev, int force_chunks) { return tc_set_trace(t
 
 int sd_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host) {
   SD_REQUIRE(base && tmap_out_host && dh == 128 && L > 0 && Hk > 0 && cap > 0, "sd_make_kv_tmap: args");
-  return tc_make_kv_tmap(base, L, Hk, cap, dh, tmap_out_host);
+  return tc_make_kv_tmap(base, L, Hk, cap, dh, tmap_out_host, 128);
+}
+
+int sd_make_slot_tmap(const void* base, int L, int Hk, int cap, int dh, void* tmap_out_host) {
+  SD_REQUIRE(base && tmap_out_host && dh == 128 && L > 0 && Hk > 0 && cap > 0, "sd_make_slot_tmap: args");
+  return tc_make_kv_tmap(base, L, Hk, cap, dh, tmap_out_host, 64);
 }
 
 int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int src_kind, const void* k_cache,
@@ -1117,6 +1125,13 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     if (rc) return rc;
     launch_merge<__nv_bfloat16>(p.ws_o, ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out, 128, st);
     return check_launch("sd_attention(tc merge)");
+  }
+  if (T == 1 && src_kind == 1 && dh == 128 && p.G <= 16 && !rows_dev && !ctx_dev && tmap_k_host && tmap_v_host &&
+      q_dtype == SD_BF16 && kv_dtype == SD_BF16 && out_dtype == SD_BF16 && Hk * sizeof(int) <= SD_ATTN_WS_HEAD) {
+    // draft attention on the warp-level tensor path: TMA-staged slots, rank-RoPE in
+    // registers, split merge + pending row fused (last CTA per kv head)
+    return launch_draft_mma(tmap_k_host, tmap_v_host, q, H, Hk, kv_heads_total, layer, ctx, ranks, k_tree, v_tree,
+                            tree_head_stride, p.ws_o, counters, out, st);
   }
   if (T == 1 && src_kind == 1 && dh == 128 && p.G <= 8 && !rows_dev && q_dtype == kv_dtype &&
       out_dtype == SD_BF16 && kv_dtype == SD_BF16 && (ctx + DR_CHUNK - 1) / DR_CHUNK <= DR_MAX_CHUNKS &&

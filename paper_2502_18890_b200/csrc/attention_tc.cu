@@ -540,7 +540,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   return fn;
 }
 
-int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out) {
+int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out, int box_rows) {
   auto enc = get_encode();
   if (!enc) {
     set_error("cuTensorMapEncodeTiled unavailable");
@@ -549,7 +549,7 @@ int tc_make_kv_tmap(const void* base, int L, int Hk, int cap, int dh, void* out)
   CUtensorMap* m = reinterpret_cast<CUtensorMap*>(out);
   cuuint64_t dims[4] = {(cuuint64_t)dh, (cuuint64_t)cap, (cuuint64_t)Hk, (cuuint64_t)L};
   cuuint64_t strides[3] = {(cuuint64_t)dh * 2, (cuuint64_t)cap * dh * 2, (cuuint64_t)Hk * cap * dh * 2};
-  cuuint32_t box[4] = {64, (cuuint32_t)tc::SLOT_KEYS, 1, 1};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

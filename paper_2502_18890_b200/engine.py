@@ -264,7 +264,7 @@ class Session:
         def attend(l, qkv, q_pre):
             m.rope_stage(qkv, 1, self.draft_pos, q_rot, None, None, kt, vt, m.dh, 0)
             m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt,
-                        m.dh, None, None, out, ws=self.attn_ws)
+                        m.dh, None, None, out, part.tmaps, l, ws=self.attn_ws)
             return out
 
         pend = self.result[L.RES_PENDING:L.RES_PENDING + 1]

@@ -142,11 +142,24 @@ class PartialCache:
         self.ppos = torch.full((num_layers, self.slot_cap), -1, dtype=torch.int32, device=self.device)
         self.prank = torch.full((num_layers, self.slot_cap), -1, dtype=torch.int32, device=self.device)
         self.pscore = torch.full((num_layers, self.slot_cap), float("nan"), dtype=torch.float32, device=self.device)
+        self.tmaps = None
+        self._make_tmaps()
         self.body: deque[int] = deque()  # slot ids in importance order (shared by all layers)
         self.free: list[int] = []        # holes below `hi`
         self.hi = 0                      # slots [0, hi) scanned by the draft kernel
         self.count = 0
         self.mark = 0
+
+    def _make_tmaps(self) -> None:
+        # TMA descriptors (64-slot boxes) for the tensor-core draft attention
+        if self.dtype == torch.bfloat16 and self.head_dim == 128:
+            import ctypes
+            tk, tv = ctypes.create_string_buffer(128), ctypes.create_string_buffer(128)
+            L.call("sd_make_slot_tmap", L.ptr(self.pk), self.num_layers, self.num_kv_heads, self.slot_cap,
+                   self.head_dim, tk)
+            L.call("sd_make_slot_tmap", L.ptr(self.pv), self.num_layers, self.num_kv_heads, self.slot_cap,
+                   self.head_dim, tv)
+            self.tmaps = (tk, tv)
 
     @property
     def head_stride(self) -> int:
@@ -276,6 +289,7 @@ class PartialCache:
         self.pk, self.pv = pk, pv
         self.ppos, self.prank, self.pscore = meta
         self.slot_cap = cap
+        self._make_tmaps()
 
     def _take_slots(self, a: int) -> list[int]:
         short = a - len(self.free) - (self.slot_cap - self.hi)

@@ -408,7 +408,8 @@ class TinyTransformer:
     def attention(self, q_rot, T, src_kind, k_cache, v_cache, head_stride, ctx, ranks, k_tree, v_tree,
                   tree_head_stride, mask_bits, rows_dev, out, tmaps=None, layer=0, ctx_dev=None, ws=None):
         """sd_attention; with `tmaps` (FullCache.tmaps) and bf16/dh=128 the cache
-        chunks run on the tcgen05 kernel of `layer`. With `ctx_dev` the live
+        chunks run on the tcgen05 kernel of `layer` (PartialCache.tmaps: the
+        tensor-core draft kernel). With `ctx_dev` the live
         context is read on device and `ctx` is its upper bound (graph replay).
         `ws`: caller-owned workspace (a Session's, sized once and captured in its
         graph); default the model's scratch, which may be reallocated."""
@@ -549,6 +550,7 @@ class TinyTransformer:
         def attend(l, qkv, q_pre):
             self.rope_stage(qkv, T, pos, q_rot, q_pre, None, kt, vt, T * self.dh, 0)
             self.attention(q_rot, T, 1, partial.pk[l], partial.pv[l], partial.head_stride, partial.hi,
-                           partial.prank[l], kt, vt, T * self.dh, None, None, out)
+                           partial.prank[l], kt, vt, T * self.dh, None, None, out,
+                           partial.tmaps if T == 1 else None, l)
             return out
         return attend

@@ -238,8 +238,19 @@ def test_draft_attention_rank_rope_with_holes(lib, dtype, H, Hk, dh, cap, hi):
     qt = torch.as_tensor(q, dtype=dtype, device=dev)
     kt = torch.as_tensor(ks.transpose(1, 0, 2), dtype=dtype, device=dev).contiguous()
     vt = torch.as_tensor(v_self.transpose(1, 0, 2), dtype=dtype, device=dev).contiguous()
+    outs = []
     out = torch.empty((1, H * dh), dtype=dtype, device=dev)
     mdl.attention(qt, 1, 1, pk, pv, cap * dh, hi, rk, kt, vt, dh, None, None, out)
+    outs.append(out)
+    if dtype == torch.bfloat16 and dh == 128:
+        # the product path: TMA slot descriptors -> tensor-core draft kernel
+        import ctypes
+        tk, tv = ctypes.create_string_buffer(128), ctypes.create_string_buffer(128)
+        lib.call("sd_make_slot_tmap", lib.ptr(pk), 1, Hk, cap, dh, tk)
+        lib.call("sd_make_slot_tmap", lib.ptr(pv), 1, Hk, cap, dh, tv)
+        out2 = torch.empty((1, H * dh), dtype=dtype, device=dev)
+        mdl.attention(qt, 1, 1, pk, pv, cap * dh, hi, rk, kt, vt, dh, None, None, out2, (tk, tv), 0)
+        outs.append(out2)
     # oracle: keys sorted by rank, rotated at rank
     order = live[np.argsort(ranks[live])]
     Kr = pk.double().cpu().numpy()[:, order].transpose(1, 0, 2)
@@ -248,8 +259,10 @@ def test_draft_attention_rank_rope_with_holes(lib, dtype, H, Hk, dh, cap, hi):
     Kall = np.concatenate([Krot, kt.double().cpu().numpy().transpose(1, 0, 2)])
     Vall = np.concatenate([Vr, vt.double().cpu().numpy().transpose(1, 0, 2)])
     want = attend_oracle(qt.double().cpu().numpy(), Kall, Vall, np.ones((1, m + 1), dtype=bool))
-    tol = 1e-5 if dtype == torch.float32 else 2e-2
-    np.testing.assert_allclose(out.double().cpu().numpy().reshape(1, H, dh), want, rtol=tol, atol=tol)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    for o in outs:
+        got = o.double().cpu().numpy().reshape(1, H, dh)
+        assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < tol
 
 
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
