@@ -114,6 +114,79 @@ __device__ __forceinline__ void trace(int role, int j, int ev) {
 #endif
 }
 
+// MMA issue stream of one M-tile (warps 1 / 2; the whole warp runs the loop,
+// one elected lane issues). TMEM base is 0: the CTA owns all 512 columns.
+//   S[MT][j%2] = Q[MT] K(j)^T (8 K=16 steps), O[MT] += P(j) V(j) (4 steps)
+template <int MT>
+__device__ __forceinline__ void issue_loop(uint8_t* smem, int n_tiles, uint32_t p_bar_count, uint64_t* k_full,
+                                           uint64_t* k_empty, uint64_t* v_full, uint64_t* v_empty, uint64_t* s_full,
+                                           uint64_t* pv_done, uint64_t* o_final) {
+  __syncwarp();
+  const bool leader = elect_one();
+  constexpr uint32_t id_qk = idesc_bf16(BN, false);
+  constexpr uint32_t id_pv = idesc_bf16(DH, true);
+  constexpr uint32_t O_COL = COL_O + 128 * MT;
+  const uint32_t sb = smem_u32(smem);
+  const uint32_t q_base = sb + OFF_Q + MT * 32768;
+  auto issue_qk = [&](int j) {
+    const int s = (j >> 1) % KST, b = j & 1;
+    const uint32_t k_base = sb + OFF_K + s * KV_SLOT + (j & 1) * (BN * 128);
+    if (leader) {
+#pragma unroll
+      for (int ks = 0; ks < DH / 16; ++ks) {
+        const uint32_t half = ks >> 2, in = (ks & 3) * 32;
+        if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA)
+          umma_bf16(COL_S + 128 * MT + 64 * b, umma_desc(q_base + half * 16384 + in, 16, 1024),
+                    umma_desc(k_base + half * HALF + in, 16, 1024), id_qk, ks > 0);
+      }
+      tc_signal(&s_full[2 * MT + b]);
+      if ((j & 1) || j == n_tiles - 1) tc_signal(&k_empty[s]);  // slot's last sub-tile
+    }
+    __syncwarp();
+  };
+  auto wait_k = [&](int j) {
+    if (j & 1) return;  // the odd sub-tile shares its slot with the even one
+    if (MT == 0) trace(1, j, 0);
+    const int q = j >> 1;
+    mbar_wait(&k_full[q % KST], (q / KST) & 1);
+    if (MT == 0) trace(1, j, 1);
+    tc_fence_after();
+  };
+  for (int j0 = 0; j0 < 2 && j0 < n_tiles; ++j0) {
+    wait_k(j0);
+    issue_qk(j0);
+  }
+  for (int j = 0; j < n_tiles; ++j) {
+    const int q = j >> 1, s = q % VST, b = j & 1;
+    if (MT == 0) trace(1, j, 3);
+    if (!(j & 1)) mbar_wait(&v_full[s], (q / VST) & 1);
+    const uint32_t v_base = sb + OFF_V + s * KV_SLOT + (j & 1) * (BN * 128);
+#if SD_TC_EXPERIMENT != 9
+    asm volatile("bar.sync %0, %1;" ::"r"(2 + 2 * MT + b), "r"(p_bar_count) : "memory");  // P(j) written
+#endif
+    if (MT == 0) trace(1, j, 4);
+    tc_fence_after();
+    if (leader) {
+#pragma unroll
+      for (int ks = 0; ks < BN / 16; ++ks)  // V tile [64 keys][dh] (MN-major B): dh halves LBO apart
+        if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA)
+          umma_bf16_ts(O_COL, COL_S + 128 * MT + 64 * b + 8 * ks, umma_desc(v_base + ks * 16 * 128, HALF, 1024),
+                       id_pv, (j > 0 || ks > 0) ? 1u : 0u);
+      tc_signal(&pv_done[2 * MT + b]);
+      if (j == n_tiles - 1) tc_signal(&o_final[MT]);
+      if ((j & 1) || j == n_tiles - 1) tc_signal(&v_empty[s]);
+    }
+    __syncwarp();
+    if (MT == 0) trace(1, j, 6);
+    // S(j+2) into buffer b: issued after PV(j) by this thread, so it is
+    // ordered after PV(j)'s reads of P(j) (same-thread tcgen05.mma order)
+    if (j + 2 < n_tiles) {
+      wait_k(j + 2);
+      issue_qk(j + 2);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
     verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                           Params p) {
@@ -280,79 +353,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int mt = warp - 1;
 #if SD_TC_EXPERIMENT == 8
     if (lane == 0 && mt < nm) mbar_arrive(&o_final[mt]);
-    if (false) {
 #else
-    if (mt < nm) {
+    // M-tile as a template argument: every descriptor and TMEM address of the
+    // issue stream is then warp-uniform (uniform datapath, no per-MMA R2UR /
+    // ELECT waterfall); one elected lane issues.
+    if (mt == 0)
+      issue_loop<0>(smem, n_tiles, 32u * (uint32_t)(act[0] + 1), k_full, k_empty, v_full, v_empty, s_full, pv_done,
+                    o_final);
+    else if (mt < nm)
+      issue_loop<1>(smem, n_tiles, 32u * (uint32_t)(act[1] + 1), k_full, k_empty, v_full, v_empty, s_full, pv_done,
+                    o_final);
 #endif
-      const uint32_t p_bar_count = 32u * (uint32_t)(act[mt] + 1);
-      const uint32_t id_qk = idesc_bf16(BN, false);
-      const uint32_t id_pv = idesc_bf16(DH, true);
-      const uint32_t q_base = smem_u32(smem + OFF_Q + mt * 32768);
-      const uint32_t o_col = tmem + COL_O + 128 * mt;
-      // S[mt][j%2] = Q[mt] K(j)^T (8 K=16 steps)
-      // sub-tile j: slot j/2 of the ring, rows 64*(j%2).. of each dh half
-      auto issue_qk = [&](int j) {
-        const int s = (j >> 1) % KST, b = j & 1;
-        const uint32_t k_base = smem_u32(smem + OFF_K + s * KV_SLOT) + (j & 1) * (BN * 128);
-#pragma unroll
-        for (int ks = 0; ks < DH / 16; ++ks) {
-          const uint32_t half = ks >> 2, in = (ks & 3) * 32;
-          const uint64_t bd = umma_desc(k_base + half * HALF + in, 16, 1024);
-          const uint64_t a = umma_desc(q_base + half * 16384 + in, 16, 1024);
-          if (SD_TC_EXPERIMENT != 3 && !SD_TC_NOMMA && lane == 0)
-            umma_bf16(tmem + COL_S + 128 * mt + 64 * b, a, bd, id_qk, ks > 0);
-        }
-        if (lane == 0) {
-          tc_signal(&s_full[2 * mt + b]);
-          if ((j & 1) || j == n_tiles - 1) tc_signal(&k_empty[s]);  // slot's last sub-tile
-        }
-        __syncwarp();
-      };
-      auto wait_k = [&](int j) {
-        if (j & 1) return;  // the odd sub-tile shares its slot with the even one
-        if (mt == 0) trace(1, j, 0);
-        const int q = j >> 1;
-        mbar_wait(&k_full[q % KST], (q / KST) & 1);
-        if (mt == 0) trace(1, j, 1);
-        tc_fence_after();
-      };
-      for (int j0 = 0; j0 < 2 && j0 < n_tiles; ++j0) {
-        wait_k(j0);
-        issue_qk(j0);
-      }
-      for (int j = 0; j < n_tiles; ++j) {
-        const int q = j >> 1, s = q % VST, b = j & 1;
-        if (mt == 0) trace(1, j, 3);
-        if (!(j & 1)) mbar_wait(&v_full[s], (q / VST) & 1);
-        const uint32_t v_base = smem_u32(smem + OFF_V + s * KV_SLOT) + (j & 1) * (BN * 128);
-#if SD_TC_EXPERIMENT != 9
-        asm volatile("bar.sync %0, %1;" ::"r"(2 + 2 * mt + b), "r"(p_bar_count) : "memory");  // P(j) written
-#endif
-        if (mt == 0) trace(1, j, 4);
-        tc_fence_after();
-        const uint32_t p_tmem = tmem + COL_S + 128 * mt + 64 * b;  // P(j) over S(j)'s first 32 columns
-#pragma unroll
-        for (int ks = 0; ks < BN / 16; ++ks) {
-          // V tile is [64 keys][dh] (MN-major B): dh halves LBO apart, 8-key groups SBO apart
-          const uint64_t bd = umma_desc(v_base + ks * 16 * 128, HALF, 1024);
-          if (SD_TC_EXPERIMENT != 2 && !SD_TC_NOMMA && lane == 0)
-            umma_bf16_ts(o_col, p_tmem + 8 * ks, bd, id_pv, (j > 0 || ks > 0) ? 1u : 0u);
-        }
-        if (lane == 0) {
-          tc_signal(&pv_done[2 * mt + b]);
-          if (j == n_tiles - 1) tc_signal(&o_final[mt]);
-          if ((j & 1) || j == n_tiles - 1) tc_signal(&v_empty[s]);
-        }
-        __syncwarp();
-        if (mt == 0) trace(1, j, 6);
-        // S(j+2) into buffer b: issued after PV(j) by this thread, so it is
-        // ordered after PV(j)'s reads of P(j) (same-thread tcgen05.mma order)
-        if (j + 2 < n_tiles) {
-          wait_k(j + 2);
-          issue_qk(j + 2);
-        }
-      }
-    }
   } else if (warp >= 4) {
     // ================= softmax warpgroups =================
     const int mt = (warp - 4) >> 2, wl = warp & 3;
@@ -421,18 +432,17 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int c = 0; c < 64; ++c)
             if (!((vis >> c) & 1ull)) sr[c] = __float_as_uint(-INFINITY);
         }
-        // tree max (short dependency chain)
-        float mx8[8];
+        // tile max: 3-input max tree (short dependency chain)
+        float m21[22];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float a0 = fmaxf(__uint_as_float(sr[c]), __uint_as_float(sr[c + 8]));
-          const float a1 = fmaxf(__uint_as_float(sr[c + 16]), __uint_as_float(sr[c + 24]));
-          const float a2 = fmaxf(__uint_as_float(sr[c + 32]), __uint_as_float(sr[c + 40]));
-          const float a3 = fmaxf(__uint_as_float(sr[c + 48]), __uint_as_float(sr[c + 56]));
-          mx8[c] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
-        }
-        const float mx = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]))) * LOG2E;
+        for (int c = 0; c < 21; ++c)
+          m21[c] = fmax3(__uint_as_float(sr[c]), __uint_as_float(sr[c + 21]), __uint_as_float(sr[c + 42]));
+        m21[21] = __uint_as_float(sr[63]);
+        float m8[8];
+#pragma unroll
+        for (int c = 0; c < 7; ++c) m8[c] = fmax3(m21[c], m21[c + 7], m21[c + 14]);
+        m8[7] = m21[21];
+        const float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7])) * LOG2E;
         float scale = 1.f;
         bool rescale = false;
         if (mx > m_used + TAU) {
@@ -442,18 +452,28 @@ __global__ void __launch_bounds__(THREADS, 1)
           l *= scale;
         }
         uint32_t pk[32];
-        float rs8[8];
         const float nm_used = m_used == -INFINITY ? 0.f : -m_used;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) rs8[c] = 0.f;
+        const uint64_t lg2 = f2(LOG2E, LOG2E), off = f2(nm_used, nm_used);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        // p = 2^(s log2e - m): packed scale, exps split between the MUFU (3 of 4
+        // pairs) and the FMA pipe (1 of 4), packed row sums
 #pragma unroll
         for (int c = 0; c < 64; c += 2) {
-          const float p0 = ex2(fmaf(__uint_as_float(sr[c]), LOG2E, nm_used));
-          const float p1 = ex2(fmaf(__uint_as_float(sr[c + 1]), LOG2E, nm_used));
-          rs8[(c >> 1) & 7] += p0 + p1;
-          pk[c >> 1] = pack_bf16(p0, p1);
+          const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
+          float2 pp;
+          if ((c >> 1) % 4 == 3) {
+            pp = exp2_poly2(x.x, x.y);
+          } else {
+            pp.x = ex2(x.x);
+            pp.y = ex2(x.y);
+          }
+          acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(pp.x, pp.y));
+          pk[c >> 1] = pack_bf16(pp.x, pp.y);
         }
-        l += ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+        {
+          const float2 a = unf2(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
+          l += a.x + a.y;
+        }
         if (role < 4) trace(role, j, 2);
         if (__any_sync(0xffffffffu, rescale)) {
           // O must be stable: wait for every earlier O += P V of this M-tile (PV(j-1) retires last)

@@ -135,6 +135,52 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// ---- packed fp32x2 arithmetic (FFMA2 / FADD2) and the 3-input max (FMNMX3), sm_100 ----
+__device__ __forceinline__ uint64_t f2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 unf2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x of a pair on the FMA pipe (FA4-style MUFU offload): round-to-nearest
+// split x = n + f (magic-number add), degree-4 fit of 2^f on [-1/2, 1/2]
+// (relative error 2.6e-6, far below the bf16 rounding of P), n added to the
+// exponent bits. x <= 127; x < -125 (incl. -inf) gives exactly 0.
+__device__ __forceinline__ float2 exp2_poly2(float x0, float x1) {
+  const uint64_t X = f2(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const uint64_t t = fadd2(X, f2(12582912.f, 12582912.f));
+  const uint64_t fi = fadd2(t, f2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(fi, f2(-1.f, -1.f), X);
+  uint64_t p = ffma2(f2(0.009571164846420288f, 0.009571164846420288f), f,
+                     f2(0.05591795593500137f, 0.05591795593500137f));
+  p = ffma2(p, f, f2(0.2402471899986267f, 0.2402471899986267f));
+  p = ffma2(p, f, f2(0.6931217908859253f, 0.6931217908859253f));
+  p = ffma2(p, f, f2(0.9999992847442627f, 0.9999992847442627f));
+  const float2 pv = unf2(p), tv = unf2(t);
+  float2 y;
+  y.x = x0 < -125.f ? 0.f : __uint_as_float(__float_as_uint(pv.x) + (__float_as_uint(tv.x) << 23));
+  y.y = x1 < -125.f ? 0.f : __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));

@@ -389,6 +389,8 @@ class TinyTransformer:
 
     # ---------------------------------------------------------- primitives --
     def mm(self, a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+        if L.DEBUG_SKIP and f"mm:{b.shape[1]}" in L.DEBUG_SKIP:  # profiling only (see _lib.DEBUG_SKIP)
+            return torch.empty((a.shape[0], b.shape[1]), dtype=torch.float32, device=a.device)
         if self.dtype == torch.bfloat16:
             return torch.mm(a, b, out_dtype=torch.float32)
         return torch.mm(a, b)
