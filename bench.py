@@ -152,6 +152,12 @@ def run_reference(args, c, ctx):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    # the unmodified reference (baseline/_ref or /root/reference): cfg1 end to
+    # end, cfgs 2-5 composed from its own functions at full shape
+    from baseline import ref_arm
+    if ref_arm.run(args, c, ctx, metric_name(args.config), workload_name(args.config, c, ctx)) is not None:
+        return
+    # reference not importable here: the oracle port, composed (kind "port")
     steps, warm = max(1, min(args.steps, 2)), 0
     vals = []
     for _ in range(steps):
