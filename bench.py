@@ -247,6 +247,11 @@ def main():
     achieved = alg_bytes / attn["avg_s"] / 1e9
     bound = "hbm" if (alg_flops / (tflops * 1e12)) < (alg_bytes / (hbm * 1e9)) else "tensor"
     kernels = {"draft_attention": time_draft_attention(sess, model, hbm, reps=args.attn_reps)}
+    if world == 1:
+        kernels["refresh"] = time_refresh(sess, model, ctx, hbm, reps=args.attn_reps)
+        acc = tokens / max(1, len(recs))
+        kernels["refresh"]["amortised_ms_per_step"] = (kernels["refresh"]["avg_launch_us"] / 1e3 * acc
+                                                       / (c["B"] - c["S"] + 1))
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -314,6 +319,32 @@ def time_verify_attention(sess, model, rows, ctx, reps=3):
     e1.record(st)
     torch.cuda.synchronize()
     return {"avg_s": e0.elapsed_time(e1) / 1e3 / n, "launches": n}
+
+
+def time_refresh(sess, model, ctx, hbm, reps=3):
+    """CUDA-event time of one partial-cache refresh at the bench context (the
+    fused score -> top-K -> gather launch, all layers; engine.py:150-151,
+    kvcache.py:243-297), on the launching stream. Algorithmic bytes per layer
+    (SURVEY §8d): score (ctx-S)*Hk*dh*2 + (ctx-S)*4, select + gather
+    (ctx-S)*4 + 2*(B-S)*Hk*dh*2*2."""
+    import torch
+    part, cfg = sess.partial, sess.config
+    st = torch.cuda.current_stream()
+    part.refresh_from(sess.full, ctx, q_sum=sess.q_sum, num_heads=model.H)  # warm
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        part.refresh_from(sess.full, ctx, q_sum=sess.q_sum, num_heads=model.H)
+    e1.record(st)
+    torch.cuda.synchronize()
+    avg = e0.elapsed_time(e1) / 1e3 / reps
+    S, B, Hk, dh, Ln = cfg.sink_size, cfg.budget, model.Hk, model.dh, model.config.num_layers
+    n = ctx - S
+    alg = Ln * (n * Hk * dh * 2 + n * 4 + n * 4 + 2 * (B - S) * Hk * dh * 2 * 2)
+    return {"bound": "hbm", "achieved": alg / avg / 1e9, "peak": hbm, "unit": "GB/s", "frac": alg / avg / 1e9 / hbm,
+            "avg_launch_us": avg * 1e6, "alg_bytes_per_launch": alg, "ctx": ctx, "layers": Ln,
+            "kernel": "sd_partial_refresh (fused Eq. 2 score -> radix top-K -> gather -> importance ring), all layers"}
 
 
 def _graph_time(fn, reps):

@@ -190,31 +190,58 @@ int sd_importance_scores(const float* q_sum, const void* k_raw, int kv_dtype, in
 int sd_sum_head_scores(const float* per_head, int L, int Hk, int n, float* scores, sd_stream_t stream);
 
 /* ---- partial cache build / maintenance (kvcache.py:191-354) ----
- * Partial cache per layer: slots [0, count) with pos, rank (position order),
- * score (NaN = unscored) and K_raw / V in [kv_head][slot][dh]. */
-/* top-(take) of positions [sink, sink+n_cand) by (-score, pos), per layer
- * (kvcache.py:286): slot sink+i <- i-th best; slots < sink <- sink positions. */
-size_t sd_select_workspace_bytes(int L, int n_cand);
-int sd_select_topk(const float* scores, int L, int n_cand, int sink, int take,
-                   int32_t* ppos, int32_t* prank, float* pscore, int slot_cap,
-                   void* workspace, size_t workspace_bytes, sd_stream_t stream);
-/* mirror (kvcache.py:300-319): slots sink.. hold positions upto-1 down to sink */
-int sd_mirror_positions(int L, int upto, int sink, int32_t* ppos, int32_t* prank, float* pscore,
-                        int slot_cap, sd_stream_t stream);
-/* copy K_raw/V rows at ppos[l][slot] for slots [0, count) from the full cache */
-int sd_gather_slots(int L, int count, const int32_t* ppos, int slot_cap, const void* full_k_raw,
-                    const void* full_v, int kv_dtype, int64_t full_layer_stride, int64_t full_head_stride,
-                    void* pk, void* pv, int64_t part_layer_stride, int64_t part_head_stride,
-                    int Hk, int dh, sd_stream_t stream);
-/* evict slots evict_slots_host[0..n_evict) (they become holes: pos = rank =
- * -1) and admit positions first_pos..first_pos+a-1 into new_slots_host[0..a)
- * (kvcache.py:215-225, 332-354). Slots [0, hi) are scanned; count_after =
- * live entries after the update; ranks stay a dense position order. */
-int sd_partial_update(int L, int hi, int count_after, int first_pos, int a, const int32_t* new_slots_host,
-                      int n_evict, const int32_t* evict_slots_host, int32_t* ppos, int32_t* prank,
-                      float* pscore, int slot_cap, const void* full_k_raw, const void* full_v, int kv_dtype,
-                      int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
-                      int64_t part_layer_stride, int64_t part_head_stride, int Hk, int dh, sd_stream_t stream);
+ * Device layout per layer l (slot_cap slots; every array [L][slot_cap]):
+ *   ppos / prank / pscore  slot metadata: position, rank (dense position order
+ *                          of the live slots: the draft rotation angle,
+ *                          kvcache.py:158-165), score (NaN = unscored); holes
+ *                          have pos = rank = -1
+ *   pk / pv                K_raw / V as [L][Hk][slot_cap][dh]
+ *   ring                   the body's slot ids in importance order (circular;
+ *                          head / length in meta): the reference's body list
+ *                          order (sink first, then body, kvcache.py:197)
+ *   freel                  free-slot stack (holes below hi)
+ *   meta [L][SD_PM_WORDS]  count, hi, ring head, ring length, free count, error
+ * All bookkeeping lives on the device, so the per-step admit/evict runs inside
+ * the step's CUDA graph without a host round trip. */
+#define SD_PM_COUNT 0
+#define SD_PM_HI 1
+#define SD_PM_HEAD 2
+#define SD_PM_LEN 3
+#define SD_PM_NFREE 4
+#define SD_PM_ERR 5
+#define SD_PM_WORDS 8
+size_t sd_refresh_workspace_bytes(int L, int n_cand, int take);
+/* refresh / prefill_partial (kvcache.py:268-297, 327-329; engine.py:128-151):
+ * one launch = Eq. 2 scores of positions [sink, upto) from q_sum and K_raw
+ * (or the precomputed scores_in [L][upto-sink] of a sharded refresh), the
+ * per-layer top-(budget-sink) by (-score, pos), the K_raw / V gather into
+ * slots [0, budget) (sink, then the body in position order) and the
+ * importance ring. */
+int sd_partial_refresh(const float* q_sum, const float* scores_in, int L, int H, int Hk, int dh, int upto,
+                       int sink, int budget, const void* full_k_raw, const void* full_v, int kv_dtype,
+                       int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                       int64_t part_layer_stride, int64_t part_head_stride, int slot_cap, int32_t* ppos,
+                       int32_t* prank, float* pscore, int32_t* ring, int32_t* freel, int32_t* meta,
+                       void* workspace, size_t workspace_bytes, sd_stream_t stream);
+/* mirror_partial (kvcache.py:300-319): slot s <- position s < upto, body ring
+ * newest first. */
+int sd_partial_mirror(int L, int Hk, int dh, int upto, int sink, const void* full_k_raw, const void* full_v,
+                      int kv_dtype, int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                      int64_t part_layer_stride, int64_t part_head_stride, int slot_cap, int32_t* ppos,
+                      int32_t* prank, float* pscore, int32_t* ring, int32_t* freel, int32_t* meta,
+                      sd_stream_t stream);
+/* admit (kvcache.py:215-225) of positions first..first+a-1 at the ring head,
+ * then (evict != 0) evict_to_budget (kvcache.py:332-354) from the ring tail.
+ * With `result` (engine, engine.py:281-283) a = result[SD_RES_ACCEPTED],
+ * first = result[SD_RES_BASE], protected = a, read on the device; else the
+ * host values (a <= 1024 per launch). A SinkViolation leaves the cache
+ * unchanged and sets meta[l][SD_PM_ERR]. */
+int sd_partial_step(int L, const int32_t* result, int a_host, int first_pos_host, int evict, int protected_host,
+                    int sink, int budget, int Hk, int dh, const void* full_k_raw, const void* full_v, int kv_dtype,
+                    int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                    int64_t part_layer_stride, int64_t part_head_stride, int slot_cap, int32_t* ppos,
+                    int32_t* prank, float* pscore, int32_t* ring, int32_t* freel, int32_t* meta,
+                    sd_stream_t stream);
 
 /* ---- reconcile (kvcache.py:116-127) + last_queries (engine.py:280) ----
  * keep offsets / count read from the device step result. Rows base+keep[i] ->

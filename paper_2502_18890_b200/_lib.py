@@ -23,6 +23,7 @@ GEMM_EPI_F32, GEMM_EPI_SILU_BF16 = 0, 1
 ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR, ST_BASE = 0, 1, 2, 3, 4, 5
 RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_BASE = 0, 1, 2, 3, 4, 5, 6, 7
 RES_YS, RES_KEEP = 8, 16
+PM_COUNT, PM_HI, PM_HEAD, PM_LEN, PM_NFREE, PM_ERR, PM_WORDS = 0, 1, 2, 3, 4, 5, 8
 
 P = C.c_void_p
 I32 = C.c_int32
@@ -71,12 +72,13 @@ _SIGS = {
     "sd_debug_tc_trace": (INT, [P, INT]),
     "sd_importance_scores": (INT, [P, P, INT, I64, I64, INT, INT, INT, INT, INT, INT, P, P, P]),
     "sd_sum_head_scores": (INT, [P, INT, INT, INT, P, P]),
-    "sd_select_workspace_bytes": (SZ, [INT, INT]),
-    "sd_select_topk": (INT, [P, INT, INT, INT, INT, P, P, P, INT, P, SZ, P]),
-    "sd_mirror_positions": (INT, [INT, INT, INT, P, P, P, INT, P]),
-    "sd_gather_slots": (INT, [INT, INT, P, INT, P, P, INT, I64, I64, P, P, I64, I64, INT, INT, P]),
-    "sd_partial_update": (INT, [INT, INT, INT, INT, INT, P, INT, P, P, P, P, INT, P, P, INT, I64, I64, P, P, I64,
-                                I64, INT, INT, P]),
+    "sd_refresh_workspace_bytes": (SZ, [INT, INT, INT]),
+    "sd_partial_refresh": (INT, [P, P, INT, INT, INT, INT, INT, INT, INT, P, P, INT, I64, I64, P, P, I64, I64, INT,
+                                 P, P, P, P, P, P, P, SZ, P]),
+    "sd_partial_mirror": (INT, [INT, INT, INT, INT, INT, P, P, INT, I64, I64, P, P, I64, I64, INT, P, P, P, P, P, P,
+                                P]),
+    "sd_partial_step": (INT, [INT, P, INT, INT, INT, INT, INT, INT, INT, INT, P, P, INT, I64, I64, P, P, I64, I64,
+                              INT, P, P, P, P, P, P, P]),
     "sd_reconcile": (INT, [INT, P, INT, P, P, P, INT, I64, I64, INT, INT, P, INT, INT, P, P]),
     "sd_sample_rows": (INT, [P, C.POINTER(SampleArgs), P]),
     "sd_draft_topw": (INT, [P, INT, INT, P, F64, F64, INT, P, P, P]),
@@ -126,7 +128,7 @@ def require_cuda():
 
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
-_NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_select_workspace_bytes",
+_NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_refresh_workspace_bytes",
               "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_make_slot_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
               "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes"}
 launch_count = 0

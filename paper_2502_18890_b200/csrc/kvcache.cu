@@ -1,31 +1,97 @@
-// Dynamic partial-KV maintenance: Eq. 2 scoring, exact top-K selection with
-// the reference's (-score, pos) order, slot gather, admit/evict with
-// incremental rank upkeep, and reconcile of accepted tree rows.
+// Dynamic partial-KV maintenance: Eq. 2 scoring, the fused refresh (scores ->
+// exact top-K with the reference's (-score, pos) order -> gather -> per-layer
+// importance ring), mirror build, the per-step admit/evict (device-resident
+// bookkeeping, launched inside the step's CUDA graph), and reconcile of
+// accepted tree rows.
 // Reference: kvcache.py:116-127 (reconcile), 215-225 (admit), 243-265
 // (importance), 268-319 (prefill/mirror build), 332-354 (evict);
 // engine.py:128-148 (per-layer body scores over pre-rotation keys), 280.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace sd {
 
 // ---------------------------------------------------------------- scores ----
-// grid (ceil(n/64), L), 256 threads: warp handles 8 positions, lanes over dh.
+// Eq. 2 dot products of one full-cache row, kv head by kv head. A warp covers
+// RPW head rows per 16-byte load (LPH lanes per row, VEC elements per lane);
+// a lane's VEC products are chained in ascending dim order, then summed by an
+// xor butterfly inside its LPH-lane group. The fused refresh and
+// sd_importance_scores share this exact tree, so per-head partials summed in
+// ascending head order (the sharded refresh) equal the unsharded total bit for
+// bit (reference sums every head, kvcache.py:264).
 template <int DH, typename KT>
+struct ScoreShape {
+  static constexpr int ES = sizeof(KT);
+  static constexpr int VEC = 16 / ES;            // elements per lane per load
+  static constexpr int LPH = DH / VEC;           // lanes per head row
+  static constexpr int RPW = 32 / LPH;           // head rows per warp-load
+  static_assert(DH * ES >= 16 && LPH <= 32 && 32 % LPH == 0, "row must be >= 16 B and split evenly");
+};
+
+// part(h) for all heads h < Hk of row `pos`; lane-uniform result in parts[]
+template <int DH, typename KT, int HKMAX>
+__device__ __forceinline__ void score_row(const float* __restrict__ qg, const KT* __restrict__ Kl,
+                                          int64_t head_stride, int64_t pos, int Hk, int lane, float (&parts)[HKMAX]) {
+  using S = ScoreShape<DH, KT>;
+  constexpr int NL = (HKMAX + S::RPW - 1) / S::RPW;
+  const int sub = lane / S::LPH, d0 = (lane % S::LPH) * S::VEC;
+  float p[NL];
+  uint4 raw[NL];
+#pragma unroll
+  for (int it = 0; it < NL; ++it) {  // all loads first (NL x 16 B in flight per lane)
+    const int h = it * S::RPW + sub;
+    raw[it] = make_uint4(0, 0, 0, 0);
+    if (h < Hk) raw[it] = __ldg(reinterpret_cast<const uint4*>(Kl + h * head_stride + pos * DH + d0));
+  }
+#pragma unroll
+  for (int it = 0; it < NL; ++it) {
+    const int h = it * S::RPW + sub;
+    const KT* e = reinterpret_cast<const KT*>(&raw[it]);
+    float acc = 0.f;
+    if (h < Hk) {
+#pragma unroll
+      for (int v = 0; v < S::VEC; ++v) acc = fmaf(qg[h * DH + d0 + v], to_f(e[v]), acc);
+    }
+#pragma unroll
+    for (int o = S::LPH / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    p[it] = acc;
+  }
+#pragma unroll
+  for (int h = 0; h < HKMAX; ++h) parts[h] = __shfl_sync(0xffffffffu, p[h / S::RPW], (h % S::RPW) * S::LPH);
+}
+
+// grouped query per kv head, g summed in ascending order (kvcache.py:262-264)
+__device__ __forceinline__ void load_grouped_query(const float* __restrict__ q, int H, int Hk, int dh, float* qg) {
+  const int G = H / Hk;
+  for (int i = threadIdx.x; i < Hk * dh; i += blockDim.x) {
+    const int k = i / dh, d = i - k * dh;
+    float s = 0.f;
+    for (int g = 0; g < G; ++g) s += q[(k * G + g) * dh + d];
+    qg[i] = s;
+  }
+}
+
+template <int HKMAX>
+__device__ __forceinline__ float sum_heads(const float (&parts)[HKMAX], int Hk) {
+  float t = parts[0];
+#pragma unroll
+  for (int h = 1; h < HKMAX; ++h)
+    if (h < Hk) t += parts[h];  // ascending head order
+  return t;
+}
+
+// grid (ceil(n / 64), L), 256 threads: a warp scores 8 positions
+template <int DH, typename KT, int HKMAX>
 __global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ q_sum, const KT* __restrict__ K,
                                                     int64_t layer_stride, int64_t head_stride, int H, int Hk,
                                                     int start, int end, float* __restrict__ scores,
                                                     float* __restrict__ per_head) {
-  constexpr int EPL = DH >= 32 ? DH / 32 : 1;
-  __shared__ float qg[64 * DH];  // Hk <= 64
-  const int layer = blockIdx.y, G = H / Hk;
-  const float* q = q_sum + (int64_t)layer * H * DH;
-  // grouped query per kv head, g summed in ascending order
-  for (int i = threadIdx.x; i < Hk * DH; i += blockDim.x) {
-    const int k = i / DH, d = i - k * DH;
-    float s = 0.f;
-    for (int g = 0; g < G; ++g) s += q[(k * G + g) * DH + d];
-    qg[i] = s;
-  }
+  extern __shared__ float qg[];  // [Hk][DH]
+  const int layer = blockIdx.y;
+  load_grouped_query(q_sum + (int64_t)layer * H * DH, H, Hk, DH, qg);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = end - start;
@@ -33,22 +99,14 @@ __global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ q_
   for (int r = 0; r < 8; ++r) {
     const int i = blockIdx.x * 64 + warp * 8 + r;
     if (i >= n) break;
-    const int64_t pos = start + i;
-    float total = 0.f;
-    for (int k = 0; k < Hk; ++k) {
-      float part = 0.f;
-      if (DH >= 32 || lane < DH) {
+    float parts[HKMAX];
+    score_row<DH, KT, HKMAX>(qg, Kl, head_stride, start + i, Hk, lane, parts);
+    if (per_head && lane < Hk) {
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) {
-          const int d = lane * EPL + e;
-          part = fmaf(qg[k * DH + d], to_f(Kl[k * head_stride + pos * DH + d]), part);
-        }
-      }
-      part = warp_sum(part);
-      if (per_head && lane == 0) per_head[((int64_t)layer * Hk + k) * n + i] = part;
-      total = k == 0 ? part : total + part;  // ascending head order
+      for (int h = 0; h < HKMAX; ++h)
+        if (h == lane) per_head[((int64_t)layer * Hk + h) * n + i] = parts[h];
     }
-    if (lane == 0 && scores) scores[(int64_t)layer * n + i] = total;
+    if (lane == 0 && scores) scores[(int64_t)layer * n + i] = sum_heads(parts, Hk);
   }
 }
 
@@ -65,214 +123,368 @@ __global__ void sum_head_scores_kernel(const float* __restrict__ per_head, int L
 
 // -------------------------------------------------------------- top-K ------
 __device__ __forceinline__ uint32_t ord_f32(float f) {
+  if (f == 0.0f) f = 0.0f;  // -0.0 ties with +0.0, as in the reference's comparison
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
-// larger key = better: higher score first, then lower position
+// larger key = better: higher score first, then lower position (kvcache.py:286)
 __device__ __forceinline__ uint64_t sel_key(float score, int pos) {
-  if (score == 0.0f) score = 0.0f;  // -0.0 ties with +0.0, as in the reference's comparison
   return ((uint64_t)ord_f32(score) << 32) | (uint64_t)(0xFFFFFFFFu - (uint32_t)pos);
 }
 
-constexpr int SEL_THREADS = 1024;
-constexpr int SEL_MAX_TAKE = 8192;
+constexpr int RF_CLUSTER = 4;     // CTAs per layer in the fused refresh
+constexpr int RF_THREADS = 512;
+constexpr int RF_MAX_TAKE = 8192;
+constexpr float QNAN = __builtin_nanf("");
 
-// one CTA per layer
-__global__ void __launch_bounds__(SEL_THREADS) select_kernel(const float* __restrict__ scores, int n, int sink,
-                                                             int take, int32_t* __restrict__ ppos,
-                                                             int32_t* __restrict__ prank, float* __restrict__ pscore,
-                                                             int slot_cap, int32_t* __restrict__ asc_ws) {
-  extern __shared__ uint64_t sk[];  // [pow2 >= take]
-  __shared__ uint32_t hist[256];
-  __shared__ uint32_t red[32];
+struct RefreshArgs {
+  const float* q_sum;        // [L][H][dh] (NULL with scores_in)
+  const float* scores_in;    // [L][n] precomputed (sharded refresh) or NULL
+  float* scores_ws;          // [L][n] scratch (scores_in == NULL)
+  uint64_t* keys_ws;         // [L][take] scratch
+  const void* fk;            // full K_raw
+  const void* fv;            // full V
+  int64_t f_ls, f_hs;        // full layer / head strides (elements)
+  void* pk;
+  void* pv;
+  int64_t p_ls, p_hs;
+  int32_t *ppos, *prank, *ring, *freel, *meta;
+  float* pscore;
+  int slot_cap;
+  int H, Hk, n, sink, take;
+};
+
+// copy the K_raw / V rows of `pos` into partial slot `slot` (all kv heads);
+// a warp moves 512 B per instruction
+template <int DH, typename KT>
+__device__ __forceinline__ void copy_rows(const RefreshArgs& a, int layer, int64_t pos, int slot, int Hk, int lane) {
+  constexpr int RW = DH * (int)sizeof(KT) / 16;  // uint4 per head row
+  const uint4* fk = reinterpret_cast<const uint4*>(static_cast<const KT*>(a.fk) + layer * a.f_ls);
+  const uint4* fv = reinterpret_cast<const uint4*>(static_cast<const KT*>(a.fv) + layer * a.f_ls);
+  uint4* pk = reinterpret_cast<uint4*>(static_cast<KT*>(a.pk) + layer * a.p_ls);
+  uint4* pv = reinterpret_cast<uint4*>(static_cast<KT*>(a.pv) + layer * a.p_ls);
+  const int64_t fhs = a.f_hs * (int64_t)sizeof(KT) / 16, phs = a.p_hs * (int64_t)sizeof(KT) / 16;
+  for (int w = lane; w < Hk * RW; w += 32) {
+    const int h = w / RW, c = w - h * RW;
+    const uint4 k = __ldg(fk + h * fhs + pos * RW + c);
+    const uint4 v = __ldg(fv + h * fhs + pos * RW + c);
+    pk[h * phs + (int64_t)slot * RW + c] = k;
+    pv[h * phs + (int64_t)slot * RW + c] = v;
+  }
+}
+
+// Fused refresh (kvcache.py:243-297 via engine.py:128-148): one cluster of
+// RF_CLUSTER CTAs per layer, each owning a contiguous 1/RF_CLUSTER of the
+// candidate positions [sink, sink+n).
+//   1. Eq. 2 score of every owned position (score_row), kept in scores_ws
+//      (L2-resident), unless precomputed scores are given;
+//   2. exact radix select of the take-th largest 64-bit key (score, ~pos):
+//      8-bit digits from the top, per-CTA shared histograms summed through
+//      distributed shared memory, stopping early once a digit bucket is taken
+//      whole; keys are unique, so exactly `take` keys are >= the threshold;
+//   3. compaction in ascending position order (cluster prefix over the CTAs'
+//      counts): body entry j lands in slot sink + j (rank = slot, position
+//      order), score kept, K_raw / V rows gathered by the CTA that owns it;
+//   4. cluster rank 0 sorts the selected keys (bitonic, descending; key low
+//      word = ~j, order-equivalent to ~pos among the selected) into the
+//      layer's importance ring: ring[i] = slot of the i-th most important body
+//      entry; the layer's meta is reset (count = hi = sink + take).
+template <int DH, typename KT, int HKMAX>
+__global__ void __cluster_dims__(RF_CLUSTER, 1, 1) __launch_bounds__(RF_THREADS)
+    refresh_kernel(RefreshArgs a) {
+  extern __shared__ __align__(16) uint8_t rf_smem[];
+  uint64_t* sk = reinterpret_cast<uint64_t*>(rf_smem);                         // [RF_MAX_TAKE] (rank 0 sort)
+  float* qg = reinterpret_cast<float*>(rf_smem + RF_MAX_TAKE * 8);             // [Hk][DH]
+  __shared__ uint32_t hist[2][256];
+  __shared__ uint32_t tot[256];
+  __shared__ uint32_t wsum[RF_THREADS / 32];
   __shared__ uint64_t s_prefix;
-  __shared__ uint32_t s_k;
-  const int layer = blockIdx.x, tid = threadIdx.x;
-  const float* sc = scores + (int64_t)layer * n;
-  int32_t* asc = asc_ws + (int64_t)layer * n;
-  int32_t* lpos = ppos + (int64_t)layer * slot_cap;
-  int32_t* lrank = prank + (int64_t)layer * slot_cap;
-  float* lsc = pscore + (int64_t)layer * slot_cap;
-  // --- radix select: the take-th largest key ---
-  uint64_t prefix = 0, pmask = 0;
-  uint32_t k = (uint32_t)take;
+  __shared__ uint32_t s_k, s_done, s_total;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int rank = (int)cluster.block_rank();
+  const int layer = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = a.n, sink = a.sink, take = a.take, Hk = a.Hk;
+  const int i0 = (int)((int64_t)n * rank / RF_CLUSTER), i1 = (int)((int64_t)n * (rank + 1) / RF_CLUSTER);
+  const float* sc = a.scores_in ? a.scores_in + (int64_t)layer * n : a.scores_ws + (int64_t)layer * n;
+
+  // ---- 1. scores ----
+  if (!a.scores_in) {
+    load_grouped_query(a.q_sum + (int64_t)layer * a.H * DH, a.H, Hk, DH, qg);
+    __syncthreads();
+    const KT* Kl = static_cast<const KT*>(a.fk) + layer * a.f_ls;
+    float* out = a.scores_ws + (int64_t)layer * n;
+    for (int i = i0 + warp * 2; i < i1; i += (RF_THREADS / 32) * 2) {
+      float p0[HKMAX], p1[HKMAX];
+      score_row<DH, KT, HKMAX>(qg, Kl, a.f_hs, sink + i, Hk, lane, p0);
+      if (i + 1 < i1) score_row<DH, KT, HKMAX>(qg, Kl, a.f_hs, sink + i + 1, Hk, lane, p1);
+      if (lane == 0) {
+        out[i] = sum_heads(p0, Hk);
+        if (i + 1 < i1) out[i + 1] = sum_heads(p1, Hk);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- 2. radix select of the take-th largest key ----
+  uint64_t prefix = 0, pmask = 0, thresh = 0;
   if (take < n) {
-    for (int shift = 56; shift >= 0; shift -= 8) {
-      for (int b = tid; b < 256; b += SEL_THREADS) hist[b] = 0;
+    uint32_t k = (uint32_t)take;
+    for (int pass = 0; pass < 8; ++pass) {
+      const int shift = 56 - 8 * pass, buf = pass & 1;
+      if (tid < 256) hist[buf][tid] = 0;
       __syncthreads();
-      for (int i = tid; i < n; i += SEL_THREADS) {
+      for (int i = i0 + tid; i < i1; i += RF_THREADS) {
         const uint64_t key = sel_key(sc[i], sink + i);
-        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        if ((key & pmask) == prefix) atomicAdd(&hist[buf][(key >> shift) & 255u], 1u);
+      }
+      cluster.sync();  // every CTA's histogram of this digit complete
+      if (tid < 256) {
+        uint32_t t = 0;
+        for (int r = 0; r < RF_CLUSTER; ++r) t += cluster.map_shared_rank(&hist[buf][0], r)[tid];
+        tot[tid] = t;
       }
       __syncthreads();
       if (tid == 0) {
         uint32_t cum = 0;
         int b = 255;
         for (; b > 0; --b) {
-          if (cum + hist[b] >= k) break;
-          cum += hist[b];
+          if (cum + tot[b] >= k) break;
+          cum += tot[b];
         }
         s_prefix = prefix | ((uint64_t)b << shift);
         s_k = k - cum;
+        s_done = (tot[b] == k - cum) ? 1u : 0u;  // the whole bucket is taken
       }
       __syncthreads();
       prefix = s_prefix;
       k = s_k;
       pmask |= (uint64_t)255 << shift;
+      if (s_done) break;
     }
+    thresh = prefix;  // lower digits zero: keys >= thresh are exactly the top `take`
   }
-  const uint64_t thresh = take < n ? prefix : 0;  // keys >= thresh selected
-  // --- compaction in ascending position order ---
-  const int seg = (n + SEL_THREADS - 1) / SEL_THREADS;
-  const int b0 = tid * seg, b1 = min(n, b0 + seg);
+
+  // ---- 3. compaction in position order + gather ----
+  const int len = i1 - i0;
+  const int seg = (len + RF_THREADS - 1) / RF_THREADS;
+  const int b0 = i0 + tid * seg, b1 = min(i1, b0 + seg);
   uint32_t cnt = 0;
   for (int i = b0; i < b1; ++i) cnt += sel_key(sc[i], sink + i) >= thresh;
-  // block exclusive scan of cnt
-  uint32_t v = cnt;
-  const int lane = tid & 31, wid = tid >> 5;
+  uint32_t v = cnt;  // block inclusive scan
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
     if (lane >= o) v += y;
   }
-  if (lane == 31) red[wid] = v;
+  if (lane == 31) wsum[warp] = v;
   __syncthreads();
-  if (wid == 0) {
-    uint32_t w = red[lane];
+  if (warp == 0) {
+    uint32_t w = lane < RF_THREADS / 32 ? wsum[lane] : 0u;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
       if (lane >= o) w += y;
     }
-    red[lane] = w;
+    if (lane < RF_THREADS / 32) wsum[lane] = w;
+    if (lane == RF_THREADS / 32 - 1) s_total = w;
+  }
+  cluster.sync();  // CTA totals published
+  uint32_t base = 0;
+  for (int r = 0; r < rank; ++r) base += *cluster.map_shared_rank(&s_total, r);
+  uint32_t off = base + v - cnt + (warp ? wsum[warp - 1] : 0u);
+  int32_t* lpos = a.ppos + (int64_t)layer * a.slot_cap;
+  int32_t* lrank = a.prank + (int64_t)layer * a.slot_cap;
+  float* lsc = a.pscore + (int64_t)layer * a.slot_cap;
+  uint64_t* keys = a.keys_ws + (int64_t)layer * take;
+  for (int i = b0; i < b1; ++i) {
+    const float s = sc[i];
+    if (sel_key(s, sink + i) >= thresh) {
+      const int slot = sink + (int)off;
+      lpos[slot] = sink + i;
+      lrank[slot] = slot;
+      lsc[slot] = s;
+      keys[off] = ((uint64_t)ord_f32(s) << 32) | (uint64_t)(0xFFFFFFFFu - off);
+      ++off;
+    }
+  }
+  if (rank == 0) {
+    for (int s = tid; s < sink; s += RF_THREADS) {
+      lpos[s] = s;
+      lrank[s] = s;
+      lsc[s] = QNAN;
+    }
+    for (int s = sink + take + tid; s < a.slot_cap; s += RF_THREADS) {  // beyond the budget: holes
+      lpos[s] = -1;
+      lrank[s] = -1;
+      lsc[s] = QNAN;
+    }
   }
   __syncthreads();
-  uint32_t off = v - cnt + (wid ? red[wid - 1] : 0);
-  for (int i = b0; i < b1; ++i)
-    if (sel_key(sc[i], sink + i) >= thresh) asc[off++] = sink + i;
-  __syncthreads();
-  // --- bitonic sort of selected keys, descending ---
+  {
+    const int j0 = (int)base, j1 = (int)(base + s_total);
+    for (int j = j0 + warp; j < j1; j += RF_THREADS / 32) copy_rows<DH, KT>(a, layer, lpos[sink + j], sink + j, Hk, lane);
+    if (rank == 0)
+      for (int s = warp; s < sink; s += RF_THREADS / 32) copy_rows<DH, KT>(a, layer, s, s, Hk, lane);
+  }
+  __threadfence();
+  cluster.sync();  // every key written (no DSMEM access after this point)
+  if (rank != 0) return;
+
+  // ---- 4. importance ring (rank 0) ----
   int N = 1;
   while (N < take) N <<= 1;
-  for (int i = tid; i < N; i += SEL_THREADS) sk[i] = i < take ? sel_key(sc[asc[i] - sink], asc[i]) : 0ull;
+  for (int i = tid; i < N; i += RF_THREADS) sk[i] = i < take ? keys[i] : 0ull;
   __syncthreads();
   for (int kk = 2; kk <= N; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < N; i += SEL_THREADS) {
+      for (int i = tid; i < N; i += RF_THREADS) {
         const int ixj = i ^ j;
         if (ixj > i) {
-          const uint64_t a = sk[i], b = sk[ixj];
-          const bool up = (i & kk) == 0;
-          if ((a < b) == up) {
-            sk[i] = b;
-            sk[ixj] = a;
+          const uint64_t x = sk[i], y = sk[ixj];
+          if ((x < y) == ((i & kk) == 0)) {  // descending
+            sk[i] = y;
+            sk[ixj] = x;
           }
         }
       }
       __syncthreads();
     }
   }
-  // --- write slots: sink first, then body in importance order ---
-  for (int j = tid; j < sink; j += SEL_THREADS) {
-    lpos[j] = j;
-    lrank[j] = j;
-    lsc[j] = __int_as_float(0x7fc00000);
-  }
-  for (int i = tid; i < take; i += SEL_THREADS) {
-    const int pos = (int)(0xFFFFFFFFu - (uint32_t)(sk[i] & 0xFFFFFFFFull));
-    int lo = 0, hi = take;  // lower_bound in asc
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (asc[mid] < pos) lo = mid + 1; else hi = mid;
-    }
-    lpos[sink + i] = pos;
-    lrank[sink + i] = sink + lo;
-    lsc[sink + i] = sc[pos - sink];
+  int32_t* ring = a.ring + (int64_t)layer * a.slot_cap;
+  for (int i = tid; i < take; i += RF_THREADS) ring[i] = sink + (int)(0xFFFFFFFFu - (uint32_t)(sk[i] & 0xFFFFFFFFull));
+  if (tid == 0) {
+    int32_t* m = a.meta + layer * SD_PM_WORDS;
+    m[SD_PM_COUNT] = sink + take;
+    m[SD_PM_HI] = sink + take;
+    m[SD_PM_HEAD] = 0;
+    m[SD_PM_LEN] = take;
+    m[SD_PM_NFREE] = 0;
+    m[SD_PM_ERR] = 0;
   }
 }
 
-__global__ void mirror_kernel(int upto, int sink, int32_t* __restrict__ ppos, int32_t* __restrict__ prank,
-                              float* __restrict__ pscore, int slot_cap) {
-  const int layer = blockIdx.y;
-  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < upto; s += gridDim.x * blockDim.x) {
-    const int pos = s < sink ? s : upto - 1 - (s - sink);
-    ppos[(int64_t)layer * slot_cap + s] = pos;
-    prank[(int64_t)layer * slot_cap + s] = pos;
-    pscore[(int64_t)layer * slot_cap + s] = __int_as_float(0x7fc00000);
+// mirror (kvcache.py:300-319): slot s <- position s for s < upto (rank = s);
+// the layer's ring lists the body newest first. grid (x, L)
+template <int DH, typename KT>
+__global__ void __launch_bounds__(256) mirror_kernel(RefreshArgs a, int upto) {
+  const int layer = blockIdx.y, lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  int32_t* lpos = a.ppos + (int64_t)layer * a.slot_cap;
+  int32_t* lrank = a.prank + (int64_t)layer * a.slot_cap;
+  float* lsc = a.pscore + (int64_t)layer * a.slot_cap;
+  int32_t* ring = a.ring + (int64_t)layer * a.slot_cap;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int s = gt; s < a.slot_cap; s += nt) {
+    const bool live = s < upto;
+    lpos[s] = live ? s : -1;
+    lrank[s] = live ? s : -1;
+    lsc[s] = QNAN;
+    if (s < upto - a.sink) ring[s] = upto - 1 - s;
+  }
+  for (int s = gw; s < upto; s += nw) copy_rows<DH, KT>(a, layer, s, s, a.Hk, lane);
+  if (gt == 0) {
+    int32_t* m = a.meta + layer * SD_PM_WORDS;
+    m[SD_PM_COUNT] = upto;
+    m[SD_PM_HI] = upto;
+    m[SD_PM_HEAD] = 0;
+    m[SD_PM_LEN] = upto > a.sink ? upto - a.sink : 0;
+    m[SD_PM_NFREE] = 0;
+    m[SD_PM_ERR] = 0;
   }
 }
 
-// copy rows (K_raw, V) of the full cache at ppos into partial slots, uint32 words
-__global__ void gather_kernel(int count, const int32_t* __restrict__ ppos, int slot_cap,
-                              const uint32_t* __restrict__ fk, const uint32_t* __restrict__ fv,
-                              int64_t f_layer_w, int64_t f_head_w, uint32_t* __restrict__ pk,
-                              uint32_t* __restrict__ pv, int64_t p_layer_w, int64_t p_head_w, int Hk, int row_w) {
-  const int layer = blockIdx.y;
-  const int64_t per_layer = (int64_t)count * Hk * row_w;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < per_layer;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int w = (int)(idx % row_w);
-    const int64_t sh = idx / row_w;
-    const int h = (int)(sh % Hk);
-    const int s = (int)(sh / Hk);
-    const int64_t pos = ppos[(int64_t)layer * slot_cap + s];
-    const int64_t src = layer * f_layer_w + h * f_head_w + pos * row_w + w;
-    const int64_t dst = layer * p_layer_w + h * p_head_w + (int64_t)s * row_w + w;
-    pk[dst] = fk[src];
-    pv[dst] = fv[src];
-  }
-}
+// ------------------------------------------------------ admit / evict ------
+constexpr int PS_MAX = 1024;  // entries moved each way per launch
 
-struct UpdateArgs {
-  int new_slots[SD_TREE_MAX_DEPTH];
-  int evict_slots[SD_TREE_MAX_DEPTH];
+struct StepArgs {
+  const int32_t* result;  // device step result (engine) or NULL (a_host / first_pos_host)
+  int a_host, first_pos_host, evict, protected_host, sink, budget;
+  RefreshArgs r;
 };
 
-// one CTA per layer over slots [0, hi): evicted slots become holes (pos = rank
-// = -1), surviving entries drop one rank per evicted entry with a smaller
-// position, admitted entries (the newest positions) take the top ranks.
-__global__ void partial_update_kernel(int hi, int count_after, int first_pos, int a, int n_evict, UpdateArgs ua,
-                                      int32_t* __restrict__ ppos, int32_t* __restrict__ prank,
-                                      float* __restrict__ pscore, int slot_cap, const uint32_t* __restrict__ fk,
-                                      const uint32_t* __restrict__ fv, int64_t f_layer_w, int64_t f_head_w,
-                                      uint32_t* __restrict__ pk, uint32_t* __restrict__ pv, int64_t p_layer_w,
-                                      int64_t p_head_w, int Hk, int row_w) {
-  __shared__ int ep[SD_TREE_MAX_DEPTH];
-  const int layer = blockIdx.x;
-  int32_t* lp = ppos + (int64_t)layer * slot_cap;
-  int32_t* lr = prank + (int64_t)layer * slot_cap;
-  float* ls = pscore + (int64_t)layer * slot_cap;
-  if ((int)threadIdx.x < n_evict) ep[threadIdx.x] = lp[ua.evict_slots[threadIdx.x]];
-  __syncthreads();
-  for (int s = threadIdx.x; s < hi; s += blockDim.x) {
-    int ni = -1;
-    bool ev = false;
-    for (int i = 0; i < a; ++i) ni = ua.new_slots[i] == s ? i : ni;
-    for (int e = 0; e < n_evict; ++e) ev |= ua.evict_slots[e] == s;
-    if (ni >= 0) {
-      lp[s] = first_pos + ni;
-      lr[s] = count_after - a + ni;
-      ls[s] = __int_as_float(0x7fc00000);
-    } else if (ev) {
-      lp[s] = -1;
-      lr[s] = -1;
-      ls[s] = __int_as_float(0x7fc00000);
-    } else {
-      const int p = lp[s];
-      if (p < 0) continue;  // hole
-      int dec = 0;
-      for (int e = 0; e < n_evict; ++e) dec += ep[e] < p;
-      lr[s] -= dec;
+// One CTA per layer (kvcache.py:215-225 admit, 332-354 evict_to_budget, as
+// called at engine.py:281-283): evict the over-budget tail of the layer's
+// importance ring (slots become holes and go to the free stack), admit the `a`
+// newly committed positions into free slots (or fresh slots at hi) at the ring
+// head in position order, keep ranks a dense position order (survivors drop
+// one rank per evicted entry with a smaller position), copy the new K_raw / V
+// rows from the full cache. Reads the accepted count and base from the device
+// step result inside the CUDA graph: no host round trip.
+template <int DH, typename KT>
+__global__ void __launch_bounds__(256) partial_step_kernel(StepArgs sa) {
+  __shared__ int ev_slot[PS_MAX], ev_pos[PS_MAX], new_slot[PS_MAX];
+  __shared__ int s_a, s_over, s_first, s_count_after, s_hi, s_bad;
+  const RefreshArgs& a = sa.r;
+  const int layer = blockIdx.x, tid = threadIdx.x, cap = a.slot_cap;
+  int32_t* lpos = a.ppos + (int64_t)layer * cap;
+  int32_t* lrank = a.prank + (int64_t)layer * cap;
+  float* lsc = a.pscore + (int64_t)layer * cap;
+  int32_t* ring = a.ring + (int64_t)layer * cap;
+  int32_t* fl = a.freel + (int64_t)layer * cap;
+  int32_t* m = a.meta + layer * SD_PM_WORDS;
+  if (tid == 0) {
+    const int na = sa.result ? sa.result[SD_RES_ACCEPTED] : sa.a_host;
+    const int first = sa.result ? sa.result[SD_RES_BASE] : sa.first_pos_host;
+    const int prot = sa.result ? na : sa.protected_host;
+    int count = m[SD_PM_COUNT], hi = m[SD_PM_HI], head = m[SD_PM_HEAD], len = m[SD_PM_LEN], nfree = m[SD_PM_NFREE];
+    int over = sa.evict ? count + na - sa.budget : 0;
+    if (over < 0) over = 0;
+    s_bad = (na > PS_MAX || over > PS_MAX || over > len || (over > 0 && count + na - sa.sink - over < prot));
+    if (!s_bad) {
+      for (int e = 0; e < over; ++e) {  // pop the least important tail
+        const int slot = ring[(head + len - 1) % cap];
+        --len;
+        ev_slot[e] = slot;
+        ev_pos[e] = lpos[slot];
+        fl[nfree++] = slot;
+      }
+      for (int i = 0; i < na; ++i) new_slot[i] = nfree > 0 ? fl[--nfree] : hi++;
+      s_bad = hi > cap;
     }
+    if (!s_bad) {
+      head = ((head - na) % cap + cap) % cap;
+      for (int i = 0; i < na; ++i) ring[(head + i) % cap] = new_slot[i];
+      len += na;
+      count += na - over;
+      m[SD_PM_COUNT] = count;
+      m[SD_PM_HI] = hi;
+      m[SD_PM_HEAD] = head;
+      m[SD_PM_LEN] = len;
+      m[SD_PM_NFREE] = nfree;
+    } else {
+      m[SD_PM_ERR] = 1;  // SinkViolation / capacity: nothing changed
+    }
+    s_a = na;
+    s_over = over;
+    s_first = first;
+    s_count_after = count;
+    s_hi = hi;
   }
-  const int per = a * Hk * row_w;
-  for (int idx = threadIdx.x; idx < per; idx += blockDim.x) {
-    const int w = idx % row_w, sh = idx / row_w, h = sh % Hk, i = sh / Hk;
-    const int64_t src = layer * f_layer_w + h * f_head_w + (int64_t)(first_pos + i) * row_w + w;
-    const int64_t dst = layer * p_layer_w + h * p_head_w + (int64_t)ua.new_slots[i] * row_w + w;
-    pk[dst] = fk[src];
-    pv[dst] = fv[src];
+  __syncthreads();
+  if (s_bad) return;
+  const int na = s_a, over = s_over, hi = s_hi;
+  if (over > 0)
+    for (int s = tid; s < hi; s += blockDim.x) {
+      const int p = lpos[s];
+      if (p < 0) continue;
+      int dec = 0;
+      for (int e = 0; e < over; ++e) dec += ev_pos[e] < p;
+      lrank[s] -= dec;
+    }
+  __syncthreads();
+  for (int e = tid; e < over; e += blockDim.x) {
+    lpos[ev_slot[e]] = -1;
+    lrank[ev_slot[e]] = -1;
+    lsc[ev_slot[e]] = QNAN;
   }
+  __syncthreads();
+  for (int i = tid; i < na; i += blockDim.x) {
+    lpos[new_slot[i]] = s_first + i;
+    lrank[new_slot[i]] = s_count_after - na + i;
+    lsc[new_slot[i]] = QNAN;
+  }
+  const int lane = tid & 31;
+  for (int i = tid >> 5; i < na; i += blockDim.x >> 5) copy_rows<DH, KT>(a, layer, s_first + i, new_slot[i], a.Hk, lane);
 }
 
 // grid (L, Hk): rows base+keep[i] -> base+i for three arrays (read all, then write)
@@ -308,20 +520,105 @@ __global__ void qsum_kernel(const int32_t* __restrict__ result, const float* __r
   }
 }
 
-template <int DH>
-static int launch_scores(const float* q_sum, const void* k_raw, int kv_dtype, int64_t ls, int64_t hs, int L, int H,
-                         int Hk, int start, int end, float* scores, float* per_head, cudaStream_t st) {
+template <int DH, typename KT>
+static int launch_scores_t(const float* q_sum, const void* k_raw, int64_t ls, int64_t hs, int L, int H, int Hk,
+                           int start, int end, float* scores, float* per_head, cudaStream_t st) {
   dim3 grid((end - start + 63) / 64, L);
-  if (kv_dtype == SD_BF16)
-    score_kernel<DH, __nv_bfloat16><<<grid, 256, 0, st>>>(q_sum, (const __nv_bfloat16*)k_raw, ls, hs, H, Hk, start,
-                                                          end, scores, per_head);
-  else
-    score_kernel<DH, float><<<grid, 256, 0, st>>>(q_sum, (const float*)k_raw, ls, hs, H, Hk, start, end, scores,
-                                                  per_head);
+  const size_t smem = (size_t)Hk * DH * 4;
+  if (Hk <= 8)
+    score_kernel<DH, KT, 8><<<grid, 256, smem, st>>>(q_sum, (const KT*)k_raw, ls, hs, H, Hk, start, end, scores,
+                                                     per_head);
+  else if (Hk <= 32)
+    score_kernel<DH, KT, 32><<<grid, 256, smem, st>>>(q_sum, (const KT*)k_raw, ls, hs, H, Hk, start, end, scores,
+                                                      per_head);
+  else {
+    set_error("sd_importance_scores: more than 32 kv heads");
+    return SD_EUNSUPPORTED;
+  }
   return check_launch("sd_importance_scores");
 }
 
+template <int DH>
+static int launch_scores(const float* q_sum, const void* k_raw, int kv_dtype, int64_t ls, int64_t hs, int L, int H,
+                         int Hk, int start, int end, float* scores, float* per_head, cudaStream_t st) {
+  if (kv_dtype == SD_BF16)
+    return launch_scores_t<DH, __nv_bfloat16>(q_sum, k_raw, ls, hs, L, H, Hk, start, end, scores, per_head, st);
+  return launch_scores_t<DH, float>(q_sum, k_raw, ls, hs, L, H, Hk, start, end, scores, per_head, st);
+}
+
 static int esize(int dtype) { return dtype == SD_BF16 ? 2 : 4; }
+
+// dispatch over (head_dim, dtype): f(DH, KT) via a templated functor
+template <template <int, typename> class F, typename... Args>
+static int dispatch_dh(int dh, int dtype, Args... args) {
+  switch (dh) {
+#define SD_CASE(D)                                                         \
+  case D:                                                                  \
+    return dtype == SD_BF16 ? F<D, __nv_bfloat16>::run(args...) : F<D, float>::run(args...);
+    SD_CASE(8) SD_CASE(16) SD_CASE(32) SD_CASE(64) SD_CASE(128)
+#undef SD_CASE
+    default:
+      set_error("partial cache: head_dim %d", dh);
+      return SD_EUNSUPPORTED;
+  }
+}
+
+template <int DH, typename KT>
+struct RefreshLaunch {
+  static int run(const RefreshArgs& a, int L, cudaStream_t st) {
+    const size_t smem = (size_t)RF_MAX_TAKE * 8 + (size_t)a.Hk * DH * 4;
+    auto kern = a.Hk <= 8 ? refresh_kernel<DH, KT, 8> : refresh_kernel<DH, KT, 32>;
+    static size_t attr8 = 0, attr32 = 0;
+    size_t& attr = a.Hk <= 8 ? attr8 : attr32;
+    if (smem > attr) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    kern<<<dim3(RF_CLUSTER, L), RF_THREADS, smem, st>>>(a);
+    return check_launch("sd_partial_refresh");
+  }
+};
+
+template <int DH, typename KT>
+struct MirrorLaunch {
+  static int run(const RefreshArgs& a, int L, int upto, cudaStream_t st) {
+    int gx = (a.slot_cap + 255) / 256;
+    if (gx > 16) gx = 16;
+    mirror_kernel<DH, KT><<<dim3(gx, L), 256, 0, st>>>(a, upto);
+    return check_launch("sd_partial_mirror");
+  }
+};
+
+template <int DH, typename KT>
+struct StepLaunch {
+  static int run(const StepArgs& a, int L, cudaStream_t st) {
+    partial_step_kernel<DH, KT><<<L, 256, 0, st>>>(a);
+    return check_launch("sd_partial_step");
+  }
+};
+
+static RefreshArgs make_refresh_args(const void* full_k_raw, const void* full_v, int64_t fls, int64_t fhs, int Hk,
+                                     void* pk, void* pv, int64_t pls, int64_t phs, int slot_cap, int32_t* ppos,
+                                     int32_t* prank, float* pscore, int32_t* ring, int32_t* freel, int32_t* meta) {
+  RefreshArgs a = {};
+  a.fk = full_k_raw;
+  a.fv = full_v;
+  a.f_ls = fls;
+  a.f_hs = fhs;
+  a.Hk = Hk;
+  a.pk = pk;
+  a.pv = pv;
+  a.p_ls = pls;
+  a.p_hs = phs;
+  a.slot_cap = slot_cap;
+  a.ppos = ppos;
+  a.prank = prank;
+  a.pscore = pscore;
+  a.ring = ring;
+  a.freel = freel;
+  a.meta = meta;
+  return a;
+}
 
 }  // namespace sd
 
@@ -332,9 +629,8 @@ extern "C" {
 int sd_importance_scores(const float* q_sum, const void* k_raw, int kv_dtype, int64_t layer_stride,
                          int64_t head_stride, int L, int H, int Hk, int dh, int start, int end, float* scores,
                          float* per_head, sd_stream_t stream) {
-  SD_REQUIRE(L > 0 && H > 0 && Hk > 0 && H % Hk == 0 && Hk <= 64, "sd_importance_scores: heads");
+  SD_REQUIRE(L > 0 && H > 0 && Hk > 0 && H % Hk == 0 && Hk <= 32, "sd_importance_scores: heads");
   SD_REQUIRE(end > start && start >= 0, "sd_importance_scores: range");
-  SD_REQUIRE(dh * Hk <= 64 * 128, "sd_importance_scores: Hk*dh too large");
   auto st = as_stream(stream);
   switch (dh) {
     case 8: return launch_scores<8>(q_sum, k_raw, kv_dtype, layer_stride, head_stride, L, H, Hk, start, end, scores, per_head, st);
@@ -352,77 +648,72 @@ int sd_sum_head_scores(const float* per_head, int L, int Hk, int n, float* score
   return check_launch("sd_sum_head_scores");
 }
 
-size_t sd_select_workspace_bytes(int L, int n_cand) { return (size_t)L * (size_t)(n_cand > 0 ? n_cand : 1) * 4; }
-
-int sd_select_topk(const float* scores, int L, int n_cand, int sink, int take, int32_t* ppos, int32_t* prank,
-                   float* pscore, int slot_cap, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
-  SD_REQUIRE(L > 0 && take > 0 && take <= n_cand, "sd_select_topk: take=%d n_cand=%d", take, n_cand);
-  SD_REQUIRE(take <= SEL_MAX_TAKE, "sd_select_topk: take %d > %d", take, SEL_MAX_TAKE);
-  SD_REQUIRE(sink + take <= slot_cap, "sd_select_topk: slot capacity");
-  SD_REQUIRE(workspace_bytes >= sd_select_workspace_bytes(L, n_cand), "sd_select_topk: workspace");
-  int N = 1;
-  while (N < take) N <<= 1;
-  const size_t smem = (size_t)N * 8;
-  static size_t attr = 0;  // only grows: earlier captured launches keep fitting
-  if (smem > attr) {
-    cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = smem;
-  }
-  select_kernel<<<L, SEL_THREADS, smem, as_stream(stream)>>>(scores, n_cand, sink, take, ppos, prank, pscore,
-                                                             slot_cap, (int32_t*)workspace);
-  return check_launch("sd_select_topk");
+size_t sd_refresh_workspace_bytes(int L, int n_cand, int take) {
+  return (size_t)L * ((size_t)(n_cand > 0 ? n_cand : 1) * 4 + (size_t)(take > 0 ? take : 1) * 8) + 16;
 }
 
-int sd_mirror_positions(int L, int upto, int sink, int32_t* ppos, int32_t* prank, float* pscore, int slot_cap,
-                        sd_stream_t stream) {
-  SD_REQUIRE(L > 0 && upto >= sink && upto <= slot_cap, "sd_mirror_positions: sizes");
-  if (upto == 0) return SD_OK;
-  dim3 grid((upto + 255) / 256, L);
-  mirror_kernel<<<grid, 256, 0, as_stream(stream)>>>(upto, sink, ppos, prank, pscore, slot_cap);
-  return check_launch("sd_mirror_positions");
+int sd_partial_refresh(const float* q_sum, const float* scores_in, int L, int H, int Hk, int dh, int upto, int sink,
+                       int budget, const void* full_k_raw, const void* full_v, int kv_dtype, int64_t full_layer_stride,
+                       int64_t full_head_stride, void* pk, void* pv, int64_t part_layer_stride,
+                       int64_t part_head_stride, int slot_cap, int32_t* ppos, int32_t* prank, float* pscore,
+                       int32_t* ring, int32_t* freel, int32_t* meta, void* workspace, size_t workspace_bytes,
+                       sd_stream_t stream) {
+  SD_REQUIRE(L > 0 && Hk > 0 && Hk <= 32 && H % Hk == 0, "sd_partial_refresh: heads");
+  SD_REQUIRE(budget > sink && sink >= 0, "sd_partial_refresh: budget %d <= sink %d", budget, sink);
+  SD_REQUIRE(upto >= budget, "sd_partial_refresh: %d entries < budget %d", upto, budget);
+  const int n = upto - sink, take = budget - sink;
+  SD_REQUIRE(take <= RF_MAX_TAKE, "sd_partial_refresh: body %d > %d", take, RF_MAX_TAKE);
+  SD_REQUIRE(budget <= slot_cap, "sd_partial_refresh: slot capacity");
+  SD_REQUIRE(q_sum || scores_in, "sd_partial_refresh: need q_sum or scores");
+  SD_REQUIRE(workspace_bytes >= sd_refresh_workspace_bytes(L, n, take), "sd_partial_refresh: workspace");
+  SD_REQUIRE((dh * esize(kv_dtype)) % 16 == 0, "sd_partial_refresh: row bytes");
+  RefreshArgs a = make_refresh_args(full_k_raw, full_v, full_layer_stride, full_head_stride, Hk, pk, pv,
+                                    part_layer_stride, part_head_stride, slot_cap, ppos, prank, pscore, ring, freel,
+                                    meta);
+  a.q_sum = q_sum;
+  a.scores_in = scores_in;
+  a.scores_ws = reinterpret_cast<float*>(workspace);
+  a.keys_ws = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(workspace) +
+                                          (((size_t)L * n * 4 + 15) & ~(size_t)15));
+  a.H = H;
+  a.n = n;
+  a.sink = sink;
+  a.take = take;
+  return dispatch_dh<RefreshLaunch>(dh, kv_dtype, a, L, as_stream(stream));
 }
 
-int sd_gather_slots(int L, int count, const int32_t* ppos, int slot_cap, const void* full_k_raw, const void* full_v,
-                    int kv_dtype, int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
-                    int64_t part_layer_stride, int64_t part_head_stride, int Hk, int dh, sd_stream_t stream) {
-  SD_REQUIRE(L > 0 && count >= 0, "sd_gather_slots: sizes");
-  if (count == 0) return SD_OK;
-  const int es = esize(kv_dtype);
-  SD_REQUIRE((dh * es) % 4 == 0, "sd_gather_slots: row bytes");
-  const int fw = 4 / es;  // elements per word
-  const int row_w = dh / fw;
-  const int64_t per = (int64_t)count * Hk * row_w;
-  int gx = (int)((per + 255) / 256);
-  if (gx > 1024) gx = 1024;
-  dim3 grid(gx, L);
-  gather_kernel<<<grid, 256, 0, as_stream(stream)>>>(count, ppos, slot_cap, (const uint32_t*)full_k_raw,
-                                                     (const uint32_t*)full_v, full_layer_stride / fw,
-                                                     full_head_stride / fw, (uint32_t*)pk, (uint32_t*)pv,
-                                                     part_layer_stride / fw, part_head_stride / fw, Hk, row_w);
-  return check_launch("sd_gather_slots");
+int sd_partial_mirror(int L, int Hk, int dh, int upto, int sink, const void* full_k_raw, const void* full_v,
+                      int kv_dtype, int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                      int64_t part_layer_stride, int64_t part_head_stride, int slot_cap, int32_t* ppos, int32_t* prank,
+                      float* pscore, int32_t* ring, int32_t* freel, int32_t* meta, sd_stream_t stream) {
+  SD_REQUIRE(L > 0 && Hk > 0 && upto >= sink && upto <= slot_cap, "sd_partial_mirror: sizes");
+  SD_REQUIRE((dh * esize(kv_dtype)) % 16 == 0, "sd_partial_mirror: row bytes");
+  RefreshArgs a = make_refresh_args(full_k_raw, full_v, full_layer_stride, full_head_stride, Hk, pk, pv,
+                                    part_layer_stride, part_head_stride, slot_cap, ppos, prank, pscore, ring, freel,
+                                    meta);
+  a.sink = sink;
+  return dispatch_dh<MirrorLaunch>(dh, kv_dtype, a, L, upto, as_stream(stream));
 }
 
-int sd_partial_update(int L, int hi, int count_after, int first_pos, int a, const int32_t* new_slots_host,
-                      int n_evict, const int32_t* evict_slots_host, int32_t* ppos, int32_t* prank, float* pscore,
-                      int slot_cap, const void* full_k_raw, const void* full_v, int kv_dtype,
-                      int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
-                      int64_t part_layer_stride, int64_t part_head_stride, int Hk, int dh, sd_stream_t stream) {
-  SD_REQUIRE(a >= 0 && a <= SD_TREE_MAX_DEPTH && n_evict >= 0 && n_evict <= SD_TREE_MAX_DEPTH,
-             "sd_partial_update: counts");
-  SD_REQUIRE(hi <= slot_cap && count_after >= a && count_after <= hi, "sd_partial_update: capacity");
-  UpdateArgs ua;
-  for (int i = 0; i < SD_TREE_MAX_DEPTH; ++i) {
-    ua.new_slots[i] = i < a ? new_slots_host[i] : -1;
-    ua.evict_slots[i] = i < n_evict ? evict_slots_host[i] : -1;
-    SD_REQUIRE(i >= a || (ua.new_slots[i] >= 0 && ua.new_slots[i] < hi), "sd_partial_update: new slot");
-    SD_REQUIRE(i >= n_evict || (ua.evict_slots[i] >= 0 && ua.evict_slots[i] < hi), "sd_partial_update: evict slot");
-  }
-  const int es = esize(kv_dtype), fw = 4 / es, row_w = dh / fw;
-  partial_update_kernel<<<L, 256, 0, as_stream(stream)>>>(
-      hi, count_after, first_pos, a, n_evict, ua, ppos, prank, pscore, slot_cap, (const uint32_t*)full_k_raw,
-      (const uint32_t*)full_v, full_layer_stride / fw, full_head_stride / fw, (uint32_t*)pk, (uint32_t*)pv,
-      part_layer_stride / fw, part_head_stride / fw, Hk, row_w);
-  return check_launch("sd_partial_update");
+int sd_partial_step(int L, const int32_t* result, int a_host, int first_pos_host, int evict, int protected_host,
+                    int sink, int budget, int Hk, int dh, const void* full_k_raw, const void* full_v, int kv_dtype,
+                    int64_t full_layer_stride, int64_t full_head_stride, void* pk, void* pv,
+                    int64_t part_layer_stride, int64_t part_head_stride, int slot_cap, int32_t* ppos, int32_t* prank,
+                    float* pscore, int32_t* ring, int32_t* freel, int32_t* meta, sd_stream_t stream) {
+  SD_REQUIRE(L > 0 && Hk > 0 && budget > sink, "sd_partial_step: sizes");
+  SD_REQUIRE(result || (a_host >= 0 && a_host <= PS_MAX), "sd_partial_step: a=%d (max %d per launch)", a_host, PS_MAX);
+  SD_REQUIRE((dh * esize(kv_dtype)) % 16 == 0, "sd_partial_step: row bytes");
+  StepArgs s = {};
+  s.result = result;
+  s.a_host = a_host;
+  s.first_pos_host = first_pos_host;
+  s.evict = evict;
+  s.protected_host = protected_host;
+  s.sink = sink;
+  s.budget = budget;
+  s.r = make_refresh_args(full_k_raw, full_v, full_layer_stride, full_head_stride, Hk, pk, pv, part_layer_stride,
+                          part_head_stride, slot_cap, ppos, prank, pscore, ring, freel, meta);
+  return dispatch_dh<StepLaunch>(dh, kv_dtype, s, L, as_stream(stream));
 }
 
 int sd_reconcile(int L, const int32_t* result, int base_len, void* k_raw, void* k_rot, void* v, int kv_dtype,

@@ -10,12 +10,13 @@ Session.step() is Algorithm 1 (engine.py:185-302) with every stage on device:
   -> sd_sample_rows (per-row window splice, penalty, truncation, draw)
   -> sd_accept_commit (paths, uniform pick, window / history / n-gram commit)
   -> sd_reconcile (accepted rows + last_queries)
-  -> one 128-byte device->host copy of the step result
-  -> sd_partial_update (admit + evict) on the next launch.
+  -> sd_partial_step (admit + evict, slot bookkeeping on device)
+  -> one 128-byte device->host copy of the step result.
 
-The only host round trip per step is that result copy; refresh decisions and
-slot bookkeeping are integer arithmetic on host scalars that mirror the
-device state exactly.
+The only host round trip per step is that result copy (the step record the
+API returns); the refresh decision is integer arithmetic on host counters
+that mirror the device state exactly, and a refresh is one fused launch
+(sd_partial_refresh) before the step's graph.
 
 Graph mode (default): every launch from the draft forward to the result copy
 takes only step-invariant arguments — the committed length lives on device
@@ -23,8 +24,7 @@ takes only step-invariant arguments — the committed length lives on device
 offset and the attention context are read from the tree record), the draft
 attention scans the whole slot range (holes are masked by rank < 0) — so the
 step is captured once as a CUDA graph and replayed; per step the host issues
-one fill (draft position), one graph launch, and after the result copy the
-partial-cache admit/evict launch (plus a refresh every B - S tokens).
+one graph launch (plus a refresh launch every B - S tokens).
 """
 
 from __future__ import annotations
@@ -35,7 +35,7 @@ from dataclasses import dataclass, field
 import torch
 
 from . import _lib as L
-from .kvcache import FullCache, PartialCache, layer_scores, needs_refresh
+from .kvcache import FullCache, PartialCache, needs_refresh
 from .metrics import IterationRecord, RunMetrics, collect_metrics
 from .model import PositionOverflow, TinyTransformer
 from .ngram import NGramTable
@@ -143,7 +143,6 @@ class Session:
         self.q_rot_d = torch.zeros((1, model.H, model.dh), dtype=model.dtype, device=dev)
         self.kt = torch.zeros((model.Hk, 1, model.dh), dtype=model.dtype, device=dev)
         self.vt = torch.zeros_like(self.kt)
-        self.draft_pos = torch.zeros(1, dtype=torch.int32, device=dev)
         self.attn_out_v = torch.zeros((self.Tmax, model.H * model.dh), dtype=model.dtype, device=dev)
         self.attn_out_d = torch.zeros((1, model.H * model.dh), dtype=model.dtype, device=dev)
         self.partial: PartialCache | None = None
@@ -227,25 +226,22 @@ class Session:
         self.partial = self._build_partial(ctx)
 
     # -------------------------------------------------------- partial cache --
-    def _scores(self, upto: int) -> torch.Tensor:
-        s = self.config.sink_size
-        m = self.model
-        if m.world == 1:
-            return layer_scores(self.full, self.q_sum, m.H, s, upto)
-        from .parallel import sharded_scores
-        return sharded_scores(self.full, self.q_sum, m, s, upto)
-
     def _build_partial(self, upto: int) -> PartialCache:
-        """engine.py:138-148: mirror below the budget, else Eq. 2 top-K."""
-        cfg = self.config
+        """engine.py:138-148: mirror below the budget, else Eq. 2 top-K. One
+        GPU: one fused score -> select -> gather launch (sd_partial_refresh);
+        sharded: per-head score partials all-gathered and summed in head order,
+        then the same launch on the summed scores."""
+        cfg, m = self.config, self.model
         part = self.partial
         if part is None:
-            part = PartialCache(cfg.sink_size, cfg.budget, self.model.config.num_layers, self.model.Hk,
-                                self.model.dh, self.model.dtype, self.dev)
+            part = PartialCache(cfg.sink_size, cfg.budget, m.config.num_layers, m.Hk, m.dh, m.dtype, self.dev)
         if upto < cfg.budget:
             part.build_mirror(self.full, upto)
+        elif m.world == 1:
+            part.refresh_from(self.full, upto, q_sum=self.q_sum, num_heads=m.H)
         else:
-            part.build_topk(self.full, self._scores(upto), upto)
+            from .parallel import sharded_scores
+            part.build_topk(self.full, sharded_scores(self.full, self.q_sum, m, cfg.sink_size, upto), upto)
         return part
 
     # ----------------------------------------------------------------- step --
@@ -262,7 +258,7 @@ class Session:
         hi = part.slot_cap  # whole slot range (holes masked): eager and replay split the draft identically
 
         def attend(l, qkv, q_pre):
-            m.rope_stage(qkv, 1, self.draft_pos, q_rot, None, None, kt, vt, m.dh, 0)
+            m.rope_stage(qkv, 1, part.count_dev(), q_rot, None, None, kt, vt, m.dh, 0)
             m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt,
                         m.dh, None, None, out, part.tmaps, l, ws=self.attn_ws)
             return out
@@ -328,6 +324,8 @@ class Session:
                int(cfg.bonus), L.ptr(self.state), L.ptr(self.window.ring), L.ptr(self.window.count), smp.window,
                L.ptr(self.history), self.ngrams.handle, L.ptr(self.result), L.stream())
         F.reconcile_device(-1 if graph else base, self.result, self.q_pre, T, m.H, self.q_sum)
+        # admit the accepted rows / evict to the budget (engine.py:281-283), on device
+        self.partial.step_device(F, self.result)
 
     def step(self) -> IterationRecord:
         if self.done:
@@ -341,7 +339,6 @@ class Session:
             self.partial = self._build_partial(len(self.full))
         t0 = time.perf_counter()
         draft_ctx = self.partial.count
-        self.draft_pos.fill_(draft_ctx)
         base = n - 1
         if len(self.full) > base:
             self.full.truncate(base)
@@ -374,7 +371,7 @@ class Session:
         pos = self.full.positions  # engine positions are range(len): trim + extend, no O(ctx) rebuild
         del pos[base:]
         pos.extend(range(base, base + a))
-        self.partial.admit_evict(n - 1, a, self.full, protected=a)
+        self.partial.account(a)  # host mirror of the device admit/evict counters
         self.tokens.extend(ys)
         self.emitted.extend(ys)
         self.window.host_len = min(self.window.capacity, self.window.host_len + a)
@@ -411,7 +408,7 @@ class Session:
                                dict(self.wall_times))
 
     def device_error(self) -> int:
-        return int(self.state[L.ST_ERROR].item())
+        return int(self.state[L.ST_ERROR].item()) or self.partial.device_error()
 
 
 def _nccl_group(group) -> bool:

@@ -10,14 +10,13 @@ HBM layout (per session, allocated once):
   metadata pos / rank / score ([L][slot_cap]). Ranks are the position order
   of the live slots, maintained incrementally on admit / evict, so the draft
   kernel rotates K_raw at its rank on load (kvcache.py:136-165) without ever
-  re-sorting. The importance order (sink, then body) is a host-side deque of
-  slot ids shared by all layers: every layer admits and evicts the same
-  number of entries at the same slot ids, only the slot contents differ.
+  re-sorting. The importance order (sink, then body) is a per-layer device
+  ring of slot ids with a free-slot stack beside it, so admit / evict is a
+  device kernel that reads the accepted count from the step result: it runs
+  inside the engine's CUDA graph with no host round trip.
 """
 
 from __future__ import annotations
-
-from collections import deque
 
 import numpy as np
 import torch
@@ -125,7 +124,16 @@ class FullCache:
 
 
 class PartialCache:
-    """Budgeted drafting cache: fixed sink + importance-ordered body, on device."""
+    """Budgeted drafting cache: fixed sink + importance-ordered body, on device.
+
+    Per layer the device holds slot metadata (pos / rank / score), the slot
+    K_raw / V rows, the body's importance order as a ring of slot ids and a
+    free-slot stack (include/swiftdec_b200.h, SD_PM_*). Every layer admits and
+    evicts the same NUMBER of entries, so the host mirrors only the counters
+    (count, hi, free count, mark); which slots move is decided on the device,
+    which lets the engine run admit/evict inside its CUDA graph."""
+
+    _BATCH = 1024  # entries moved each way per sd_partial_step launch
 
     def __init__(self, sink_size: int, budget: int, num_layers: int, num_kv_heads: int, head_dim: int,
                  dtype: torch.dtype = torch.bfloat16, device: str | torch.device = "cuda", slot_cap: int | None = None):
@@ -136,19 +144,25 @@ class PartialCache:
         self.num_kv_heads, self.head_dim, self.dtype = num_kv_heads, head_dim, dtype
         self.device = torch.device(device)
         self.slot_cap = slot_cap or (budget + L.TREE_MAX_DEPTH)
-        shape = (num_layers, num_kv_heads, self.slot_cap, head_dim)
-        self.pk = torch.zeros(shape, dtype=dtype, device=self.device)
-        self.pv = torch.zeros(shape, dtype=dtype, device=self.device)
-        self.ppos = torch.full((num_layers, self.slot_cap), -1, dtype=torch.int32, device=self.device)
-        self.prank = torch.full((num_layers, self.slot_cap), -1, dtype=torch.int32, device=self.device)
-        self.pscore = torch.full((num_layers, self.slot_cap), float("nan"), dtype=torch.float32, device=self.device)
-        self.tmaps = None
-        self._make_tmaps()
-        self.body: deque[int] = deque()  # slot ids in importance order (shared by all layers)
-        self.free: list[int] = []        # holes below `hi`
-        self.hi = 0                      # slots [0, hi) scanned by the draft kernel
+        self._alloc(self.slot_cap)
+        self.hi = 0      # slots [0, hi) scanned by the draft kernel (same on every layer)
+        self.nfree = 0   # holes below hi
         self.count = 0
         self.mark = 0
+
+    def _alloc(self, cap: int) -> None:
+        Ln, Hk, dh = self.num_layers, self.num_kv_heads, self.head_dim
+        self.pk = torch.zeros((Ln, Hk, cap, dh), dtype=self.dtype, device=self.device)
+        self.pv = torch.zeros_like(self.pk)
+        self.ppos = torch.full((Ln, cap), -1, dtype=torch.int32, device=self.device)
+        self.prank = torch.full((Ln, cap), -1, dtype=torch.int32, device=self.device)
+        self.pscore = torch.full((Ln, cap), float("nan"), dtype=torch.float32, device=self.device)
+        self.pring = torch.zeros((Ln, cap), dtype=torch.int32, device=self.device)
+        self.pfree = torch.zeros((Ln, cap), dtype=torch.int32, device=self.device)
+        self.pmeta = torch.zeros((Ln, L.PM_WORDS), dtype=torch.int32, device=self.device)
+        self.slot_cap = cap
+        self.tmaps = None
+        self._make_tmaps()
 
     def _make_tmaps(self) -> None:
         # TMA descriptors (64-slot boxes) for the tensor-core draft attention
@@ -176,133 +190,133 @@ class PartialCache:
     def __len__(self) -> int:
         return self.count
 
+    def count_dev(self) -> torch.Tensor:
+        """Device int32 view of layer 0's live-entry count: the draft row's
+        rotation position (engine.py:202-206), read inside the step graph."""
+        return self.pmeta[0, L.PM_COUNT:L.PM_COUNT + 1]
+
+    def _slot_args(self):
+        return (self.slot_cap, L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), L.ptr(self.pring),
+                L.ptr(self.pfree), L.ptr(self.pmeta))
+
     # ---- host views (reference field names; device -> host copies) ----
-    def order(self) -> list[int]:
-        return list(range(min(self.sink_size, self.count))) + list(self.body)
+    def order(self) -> list[list[int]]:
+        """Per layer: slot ids in the reference's list order (sink, then body
+        by importance, kvcache.py:197)."""
+        meta = self.pmeta.cpu().numpy()
+        ring = self.pring.cpu().numpy()
+        out = []
+        for l in range(self.num_layers):
+            head, ln = int(meta[l, L.PM_HEAD]), int(meta[l, L.PM_LEN])
+            body = [int(ring[l, (head + i) % self.slot_cap]) for i in range(ln)]
+            out.append(list(range(min(self.sink_size, self.count))) + body)
+        return out
 
     @property
     def positions(self) -> list[list[int]]:
         pos = self.ppos.cpu().numpy()
-        o = self.order()
-        return [[int(pos[l, s]) for s in o] for l in range(self.num_layers)]
+        return [[int(pos[l, s]) for s in o] for l, o in enumerate(self.order())]
 
     @property
     def scores(self) -> list[list[float | None]]:
         sc = self.pscore.cpu().numpy()
-        o = self.order()
-        return [[None if np.isnan(sc[l, s]) else float(sc[l, s]) for s in o] for l in range(self.num_layers)]
+        return [[None if np.isnan(sc[l, s]) else float(sc[l, s]) for s in o] for l, o in enumerate(self.order())]
 
     @property
     def k(self) -> list[torch.Tensor]:
-        idx = torch.as_tensor(self.order(), dtype=torch.long, device=self.device)
-        return [self.pk[l][:, idx].permute(1, 0, 2) for l in range(self.num_layers)]
+        return [self.pk[l][:, torch.as_tensor(o, dtype=torch.long, device=self.device)].permute(1, 0, 2)
+                for l, o in enumerate(self.order())]
 
     @property
     def v(self) -> list[torch.Tensor]:
-        idx = torch.as_tensor(self.order(), dtype=torch.long, device=self.device)
-        return [self.pv[l][:, idx].permute(1, 0, 2) for l in range(self.num_layers)]
+        return [self.pv[l][:, torch.as_tensor(o, dtype=torch.long, device=self.device)].permute(1, 0, 2)
+                for l, o in enumerate(self.order())]
 
     def ranks(self) -> np.ndarray:
         return self.prank.cpu().numpy()
 
-    # ---- builds (kvcache.py:268-319) ----
-    def _reset_slots(self, count: int) -> None:
-        self.count = count
-        self.hi = count
-        self.free = []
-        self.body = deque(range(self.sink_size, count))
+    def device_error(self) -> int:
+        return int(self.pmeta[:, L.PM_ERR].max().item())
+
+    # ---- builds (kvcache.py:268-329) ----
+    def _reset_counts(self, count: int, upto: int) -> None:
+        self.count = self.hi = count
+        self.nfree = 0
+        self.mark = upto
 
     def build_mirror(self, full: FullCache, upto: int) -> None:
-        L.call("sd_mirror_positions", self.num_layers, upto, self.sink_size, L.ptr(self.ppos), L.ptr(self.prank),
-               L.ptr(self.pscore), self.slot_cap, L.stream())
-        self._reset_slots(upto)
-        self._gather(full)
-        self.mark = upto
+        L.call("sd_partial_mirror", self.num_layers, self.num_kv_heads, self.head_dim, upto, self.sink_size,
+               L.ptr(full.k_raw), L.ptr(full.v), L.dcode(self.dtype), full.layer_stride, full.head_stride,
+               L.ptr(self.pk), L.ptr(self.pv), self.layer_stride, self.head_stride, *self._slot_args(), L.stream())
+        self._reset_counts(upto, upto)
+
+    def refresh_from(self, full: FullCache, upto: int, q_sum: torch.Tensor | None = None,
+                     scores: torch.Tensor | None = None, num_heads: int | None = None) -> None:
+        """Fused Eq. 2 score -> top-K -> gather (one launch): from the summed
+        last queries q_sum [L, H, dh], or from precomputed scores [L, upto-sink]
+        (sharded refresh, prefill_partial)."""
+        n, take = upto - self.sink_size, self.budget - self.sink_size
+        ws = self._refresh_ws(n, take)
+        H = num_heads if num_heads is not None else (q_sum.shape[1] if q_sum is not None else self.num_kv_heads)
+        L.call("sd_partial_refresh", L.ptr(q_sum), L.ptr(scores), self.num_layers, H, self.num_kv_heads,
+               self.head_dim, upto, self.sink_size, self.budget, L.ptr(full.k_raw), L.ptr(full.v),
+               L.dcode(self.dtype), full.layer_stride, full.head_stride, L.ptr(self.pk), L.ptr(self.pv),
+               self.layer_stride, self.head_stride, *self._slot_args(), L.ptr(ws), ws.numel(), L.stream())
+        self._reset_counts(self.budget, upto)
+
+    def _refresh_ws(self, n: int, take: int) -> torch.Tensor:
+        need = L.load().sd_refresh_workspace_bytes(self.num_layers, n, take)
+        if getattr(self, "_ws", None) is None or self._ws.numel() < need:
+            self._ws = torch.empty(int(need * 1.25) + 1024, dtype=torch.uint8, device=self.device)
+        return self._ws
 
     def build_topk(self, full: FullCache, scores: torch.Tensor, upto: int) -> None:
         """scores: [L, upto - sink] fp32 on device."""
-        take = self.budget - self.sink_size
-        n = upto - self.sink_size
-        ws = torch.empty(L.load().sd_select_workspace_bytes(self.num_layers, n), dtype=torch.uint8,
-                         device=self.device)
-        L.call("sd_select_topk", L.ptr(scores), self.num_layers, n, self.sink_size, take, L.ptr(self.ppos),
-               L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap, L.ptr(ws), ws.numel(), L.stream())
-        self._reset_slots(self.budget)
-        self._gather(full)
-        self.mark = upto
-
-    def _gather(self, full: FullCache) -> None:
-        L.call("sd_gather_slots", self.num_layers, self.count, L.ptr(self.ppos), self.slot_cap, L.ptr(full.k_raw),
-               L.ptr(full.v), L.dcode(self.dtype), full.layer_stride, full.head_stride, L.ptr(self.pk),
-               L.ptr(self.pv), self.layer_stride, self.head_stride, self.num_kv_heads, self.head_dim, L.stream())
+        self.refresh_from(full, upto, scores=scores.contiguous())
 
     # ---- maintenance (kvcache.py:215-225, 332-354) ----
-    # One sd_partial_update launch moves at most SD_TREE_MAX_DEPTH (8) entries
-    # each way; larger admit / evict bursts are split into launches of <= 8
-    # (evictions first, then admissions in position order), which is the same
-    # final state as one launch. All checks run before any host state changes.
-    _BATCH = L.TREE_MAX_DEPTH
+    def _account(self, a: int, evict: bool) -> None:
+        """Host mirror of the device counters after admitting a and (evict)
+        trimming to the budget."""
+        over = max(0, self.count + a - self.budget) if evict else 0
+        self.nfree += over
+        reuse = min(self.nfree, a)
+        self.nfree -= reuse
+        self.hi += a - reuse
+        self.count += a - over
 
-    def _launch(self, full: FullCache | None, first_pos: int, new_slots: list[int], evicted: list[int],
-                count_before: int) -> None:
-        B = self._BATCH
-        cnt = count_before
-        for i in range(0, len(evicted), B):
-            gone = evicted[i:i + B]
-            cnt -= len(gone)
-            L.call("sd_partial_update", self.num_layers, self.hi, cnt, 0, 0, L.host_i32([]), len(gone),
-                   L.host_i32(gone), L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap, None,
-                   None, L.dcode(self.dtype), 0, 0, None, None, self.layer_stride, self.head_stride,
-                   self.num_kv_heads, self.head_dim, L.stream())
-        for i in range(0, len(new_slots), B):
-            new = new_slots[i:i + B]
-            cnt += len(new)
-            L.call("sd_partial_update", self.num_layers, self.hi, cnt, first_pos + i, len(new), L.host_i32(new), 0,
-                   L.host_i32([]), L.ptr(self.ppos), L.ptr(self.prank), L.ptr(self.pscore), self.slot_cap,
-                   L.ptr(full.k_raw), L.ptr(full.v), L.dcode(self.dtype), full.layer_stride, full.head_stride,
-                   L.ptr(self.pk), L.ptr(self.pv), self.layer_stride, self.head_stride, self.num_kv_heads,
-                   self.head_dim, L.stream())
-
-    def _launch_update(self, full: FullCache, first_pos: int, new_slots: list[int], evicted: list[int]) -> None:
-        """Engine path (<= 8 each way): evict + admit in one launch."""
-        L.call("sd_partial_update", self.num_layers, self.hi, self.count, first_pos, len(new_slots),
-               L.host_i32(new_slots), len(evicted), L.host_i32(evicted), L.ptr(self.ppos), L.ptr(self.prank),
-               L.ptr(self.pscore), self.slot_cap, L.ptr(full.k_raw), L.ptr(full.v), L.dcode(self.dtype),
-               full.layer_stride, full.head_stride, L.ptr(self.pk), L.ptr(self.pv), self.layer_stride,
-               self.head_stride, self.num_kv_heads, self.head_dim, L.stream())
+    def _step(self, full: FullCache | None, a: int, first_pos: int, evict: bool, protected: int,
+              result: torch.Tensor | None = None) -> None:
+        fk = L.ptr(full.k_raw) if full is not None else None
+        fv = L.ptr(full.v) if full is not None else None
+        fls = full.layer_stride if full is not None else 0
+        fhs = full.head_stride if full is not None else 0
+        L.call("sd_partial_step", self.num_layers, L.ptr(result), a, first_pos, int(evict), protected,
+               self.sink_size, self.budget, self.num_kv_heads, self.head_dim, fk, fv, L.dcode(self.dtype), fls, fhs,
+               L.ptr(self.pk), L.ptr(self.pv), self.layer_stride, self.head_stride, *self._slot_args(), L.stream())
 
     def _grow(self, need: int) -> None:
         """Reallocate the slot arrays for a burst beyond slot_cap (API path only:
         the engine admits <= 8 per step into budget + 8 slots and never grows, so
-        pointers captured in its CUDA graph stay valid)."""
+        pointers captured in its CUDA graph stay valid). Rings are re-linearised."""
         cap = max(need, 2 * self.slot_cap)
-        L_, Hk, dh = self.num_layers, self.num_kv_heads, self.head_dim
-        pk = torch.zeros((L_, Hk, cap, dh), dtype=self.dtype, device=self.device)
-        pv = torch.zeros_like(pk)
-        pk[:, :, :self.slot_cap] = self.pk
-        pv[:, :, :self.slot_cap] = self.pv
-        meta = []
-        for t, fill in ((self.ppos, -1), (self.prank, -1), (self.pscore, float("nan"))):
-            n = torch.full((L_, cap), fill, dtype=t.dtype, device=self.device)
-            n[:, :self.slot_cap] = t
-            meta.append(n)
-        self.pk, self.pv = pk, pv
-        self.ppos, self.prank, self.pscore = meta
-        self.slot_cap = cap
-        self._make_tmaps()
-
-    def _take_slots(self, a: int) -> list[int]:
-        short = a - len(self.free) - (self.slot_cap - self.hi)
-        if short > 0:
-            self._grow(self.slot_cap + short)
-        out = []
-        for _ in range(a):
-            if self.free:
-                out.append(self.free.pop())
-            else:
-                out.append(self.hi)
-                self.hi += 1
-        return out
+        old = (self.pk, self.pv, self.ppos, self.prank, self.pscore)
+        meta = self.pmeta.clone()
+        ring = self.pring.cpu().numpy()
+        free = self.pfree.clone()
+        oc = self.slot_cap
+        self._alloc(cap)
+        self.pk[:, :, :oc], self.pv[:, :, :oc] = old[0], old[1]
+        self.ppos[:, :oc], self.prank[:, :oc], self.pscore[:, :oc] = old[2], old[3], old[4]
+        self.pfree[:, :oc] = free
+        m = meta.cpu().numpy()
+        lin = np.zeros((self.num_layers, cap), dtype=np.int32)
+        for l in range(self.num_layers):
+            head, ln = int(m[l, L.PM_HEAD]), int(m[l, L.PM_LEN])
+            lin[l, :ln] = [ring[l, (head + i) % oc] for i in range(ln)]
+        self.pring.copy_(torch.as_tensor(lin))
+        meta[:, L.PM_HEAD] = 0
+        self.pmeta.copy_(meta)
 
     def admit(self, positions, full: FullCache) -> None:
         """Copy newly committed consecutive positions to the body head."""
@@ -311,11 +325,12 @@ class PartialCache:
             return
         if positions != list(range(positions[0], positions[0] + len(positions))):
             raise ValueError("admitted positions must be consecutive")
-        before = self.count
-        slots = self._take_slots(len(positions))
-        self.count += len(slots)
-        self._launch(full, positions[0], slots, [], before)
-        self.body.extendleft(reversed(slots))
+        if self.hi + len(positions) - self.nfree > self.slot_cap:
+            self._grow(self.hi + len(positions) - self.nfree)
+        for i in range(0, len(positions), self._BATCH):
+            a = min(self._BATCH, len(positions) - i)
+            self._step(full, a, positions[i], False, 0)
+            self._account(a, False)
 
     def evict(self, protected: int = 0) -> None:
         over = self.count - self.budget
@@ -324,26 +339,33 @@ class PartialCache:
         if self.count - self.sink_size - over < protected:
             raise SinkViolation("eviction would reach protected entries; body capacity "
                                 f"{self.capacity} is smaller than one iteration's acceptance")
-        before = self.count
-        gone = [self.body.pop() for _ in range(over)]
-        self.count -= over
-        self._launch(None, 0, [], gone, before)
-        self.free.extend(gone)
+        while self.count > self.budget:
+            b = min(self._BATCH, self.count - self.budget)
+            L.call("sd_partial_step", self.num_layers, None, 0, 0, 1, 0, self.sink_size, self.count - b,
+                   self.num_kv_heads, self.head_dim, None, None, L.dcode(self.dtype), 0, 0, L.ptr(self.pk),
+                   L.ptr(self.pv), self.layer_stride, self.head_stride, *self._slot_args(), L.stream())
+            self.nfree += b
+            self.count -= b
 
     def admit_evict(self, first_pos: int, a: int, full: FullCache, protected: int) -> None:
-        """Engine path: admit a consecutive positions and trim to budget in one launch."""
+        """Engine path (eager): admit a consecutive positions and trim to budget in one launch."""
         over = self.count + a - self.budget
         if over > 0 and self.count + a - self.sink_size - over < protected:
             raise SinkViolation("eviction would reach protected entries; body capacity "
                                 f"{self.capacity} is smaller than one iteration's acceptance")
-        if a > self._BATCH or max(over, 0) > self._BATCH:
-            raise ValueError(f"admit_evict moves at most {self._BATCH} entries each way per step")
-        gone = [self.body.pop() for _ in range(over)] if over > 0 else []
-        self.free.extend(gone)
-        slots = self._take_slots(a)
-        self.count += a - len(gone)
-        self._launch_update(full, first_pos, slots, gone)
-        self.body.extendleft(reversed(slots))
+        if self.hi + a - min(self.nfree + max(over, 0), a) > self.slot_cap:
+            raise ValueError("admit_evict beyond the slot capacity")
+        self._step(full, a, first_pos, True, protected)
+        self._account(a, True)
+
+    def step_device(self, full: FullCache, result: torch.Tensor) -> None:
+        """Engine path inside the CUDA graph: a and the first position come from
+        the device step result (engine.py:281-283); call account() on the host
+        once the accepted count is known."""
+        self._step(full, -1, 0, True, 0, result=result)
+
+    def account(self, a: int) -> None:
+        self._account(a, True)
 
     def draft_view(self, before_pos: int) -> "DraftView":
         return DraftView(self, before_pos)

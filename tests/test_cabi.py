@@ -28,7 +28,7 @@ def lib():
 
 def test_header_declares_entry_points():
     syms = declared_symbols()
-    assert "sd_attention" in syms and "sd_select_topk" in syms and "sd_sample_rows" in syms
+    assert "sd_attention" in syms and "sd_partial_refresh" in syms and "sd_sample_rows" in syms
     assert len(syms) >= 25
 
 

@@ -302,44 +302,55 @@ def test_importance_scores_golden(lib):
         np.testing.assert_allclose(got, A[f"imp_s{gs}"], rtol=1e-5, atol=1e-5)
 
 
+def _scored_partial(lib, scores, sink, budget):
+    """PartialCache.build_topk over a 1-head fp32 full cache whose V rows hold
+    their own position (so gathered data can be checked slot by slot)."""
+    from paper_2502_18890_b200 import FullCache
+    from paper_2502_18890_b200.kvcache import PartialCache
+    Lr, nc = scores.shape
+    n = nc + sink
+    full = FullCache(Lr, 1, 8, capacity=n + 8, dtype=torch.float32)
+    full.v[:, :, :n] = torch.arange(n, dtype=torch.float32, device="cuda").view(1, 1, n, 1)
+    full.k_raw[:, :, :n] = -torch.arange(n, dtype=torch.float32, device="cuda").view(1, 1, n, 1)
+    full.positions = list(range(n))
+    part = PartialCache(sink, budget, Lr, 1, 8, torch.float32)
+    part.build_topk(full, torch.as_tensor(scores, dtype=torch.float32, device="cuda"), n)
+    return part
+
+
+def _check_slots(part):
+    """Slot invariants: ranks are the position order of live slots, data
+    follows slots, holes are marked."""
+    pos, rk = part.ppos.cpu().numpy(), part.ranks()
+    for l in range(part.num_layers):
+        live = [s for s in range(part.hi) if pos[l, s] >= 0]
+        assert len(live) == part.count
+        want = np.argsort(np.argsort([pos[l, s] for s in live]))
+        assert [int(rk[l, s]) for s in live] == want.tolist()
+        vals = part.pv[l, 0, live, 0].cpu().numpy()
+        assert np.array_equal(vals, pos[l, live].astype(np.float32))
+
+
 @pytest.mark.parametrize("trial", range(10))
 def test_select_topk_golden(lib, trial):
-    """Exact reference order (-score, pos) including ties (kvcache.py:286)."""
+    """Exact reference order (-score, pos) including ties (kvcache.py:286):
+    fused select + gather (sd_partial_refresh on given scores)."""
     c = J["select"][trial]
-    sc = torch.as_tensor(A[f"sel{trial}_scores"], dtype=torch.float32, device="cuda").contiguous()
-    Lr, n = sc.shape[0], c["n"]
-    take = c["budget"] - c["sink"]
-    cap = c["budget"] + 8
-    ppos = torch.full((Lr, cap), -1, dtype=torch.int32, device="cuda")
-    prank = torch.full_like(ppos, -1)
-    psc = torch.zeros((Lr, cap), dtype=torch.float32, device="cuda")
-    ws = torch.empty(lib.load().sd_select_workspace_bytes(Lr, n - c["sink"]), dtype=torch.uint8, device="cuda")
-    lib.call("sd_select_topk", lib.ptr(sc), Lr, n - c["sink"], c["sink"], take, lib.ptr(ppos), lib.ptr(prank),
-             lib.ptr(psc), cap, lib.ptr(ws), ws.numel(), lib.stream())
-    got = ppos[:, : c["budget"]].cpu().tolist()
-    assert got == c["positions"]
-    # ranks = position order among selected
-    for l in range(Lr):
-        pos = got[l]
-        want_rank = np.argsort(np.argsort(pos)).tolist()
-        assert prank[l, : c["budget"]].cpu().tolist() == want_rank
+    sc = A[f"sel{trial}_scores"].astype(np.float32)
+    part = _scored_partial(lib, sc[:, : c["n"] - c["sink"]], c["sink"], c["budget"])
+    assert part.positions == c["positions"]
+    _check_slots(part)
 
 
 def test_select_topk_large_random(lib):
     g = np.random.default_rng(5)
     Lr, n, sink, take = 3, 20000, 16, 4000
     sc = np.round(g.normal(size=(Lr, n)), 2).astype(np.float32)  # many ties
-    t = torch.as_tensor(sc, device="cuda")
-    cap = sink + take + 8
-    ppos = torch.full((Lr, cap), -1, dtype=torch.int32, device="cuda")
-    prank = torch.full_like(ppos, -1)
-    psc = torch.zeros((Lr, cap), dtype=torch.float32, device="cuda")
-    ws = torch.empty(lib.load().sd_select_workspace_bytes(Lr, n), dtype=torch.uint8, device="cuda")
-    lib.call("sd_select_topk", lib.ptr(t), Lr, n, sink, take, lib.ptr(ppos), lib.ptr(prank), lib.ptr(psc), cap,
-             lib.ptr(ws), ws.numel(), lib.stream())
+    part = _scored_partial(lib, sc, sink, sink + take)
     for l in range(Lr):
         want = list(range(sink)) + OK.select_body(sc[l].astype(np.float64), sink, sink + n, take)
-        assert ppos[l, : sink + take].cpu().tolist() == want
+        assert part.positions[l] == want
+    _check_slots(part)
 
 
 def _partial_case(L_, n, sink, budget):
@@ -385,15 +396,7 @@ def test_partial_admit_evict_matches_reference_semantics(lib):
         OK.evict_to_budget(op, protected=a)
         cur += a
         assert part.positions == op.positions
-        # ranks are the position order of live slots; data follows slots
-        rk = part.ranks()
-        pos = part.ppos.cpu().numpy()
-        for l in range(Lr):
-            live = [s for s in range(part.hi) if pos[l, s] >= 0]
-            want = np.argsort(np.argsort([pos[l, s] for s in live]))
-            assert [int(rk[l, s]) for s in live] == want.tolist()
-            vals = part.pv[l, 0, live, 0].cpu().numpy()
-            assert np.array_equal(vals, pos[l, live].astype(np.float32))
+        _check_slots(part)  # ranks are the position order of live slots; data follows slots
 
 
 def test_reconcile_and_qsum(lib):

@@ -245,6 +245,7 @@ def test_importance_scores_dh128_and_topk_at_scale():
     gen = torch.Generator(device="cuda")
     gen.manual_seed(5)
     F.k_raw.normal_(generator=gen)
+    F.v.normal_(generator=gen)
     q = torch.randn((Lr, H, dh), generator=gen, device="cuda")
     sc = layer_scores(F, q, H, sink, n)
     for l in range(Lr):
@@ -252,13 +253,23 @@ def test_importance_scores_dh128_and_topk_at_scale():
         want = OK.importance_scores(q[l].double().cpu().numpy(), K, H // Hk)
         assert rel_err(sc[l].cpu().numpy(), want) < 1e-5
     part = sd_partial(F, sc, sink, budget, n)
-    got = part.ppos[:, :budget].cpu().numpy()
+    got = part.positions
+    ks, vs = part.k, part.v
     for l in range(Lr):
         s64 = sc[l].double().cpu().numpy()
         want = list(range(sink)) + OK.select_body(s64, sink, n, budget - sink)
-        assert got[l].tolist() == want
-        kk = part.pk[l, :, :budget].cpu()
-        assert torch.equal(kk, F.k_raw[l, :, torch.as_tensor(want)].cpu())
+        assert got[l] == want
+        idx = torch.as_tensor(want)
+        assert torch.equal(ks[l].cpu(), F.k_raw[l, :, idx].permute(1, 0, 2).cpu())
+        assert torch.equal(vs[l].cpu(), F.v[l, :, idx].permute(1, 0, 2).cpu())
+    # the fused launch (scores computed in-kernel from q_sum) selects the same
+    # entries in the same order as scores -> select: one scoring tree
+    from paper_2502_18890_b200.kvcache import PartialCache
+    fused = PartialCache(sink, budget, Lr, Hk, dh, F.dtype, F.device)
+    fused.refresh_from(F, n, q_sum=q, num_heads=H)
+    assert fused.positions == got
+    assert torch.equal(fused.pk, part.pk) and torch.equal(fused.pv, part.pv)
+    assert torch.equal(fused.pscore.nan_to_num(0.0), part.pscore.nan_to_num(0.0))
 
 
 def sd_partial(F, scores, sink, budget, upto):
