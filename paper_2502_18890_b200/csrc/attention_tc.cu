@@ -41,6 +41,11 @@ constexpr int THREADS = 384;
 constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
+// 1 of every SD_POLY_DEN exp2 pairs of the softmax runs as a polynomial on the
+// FMA pipe, the rest on the MUFU (0: all MUFU)
+#ifndef SD_POLY_DEN
+#define SD_POLY_DEN 4
+#endif
 
 constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
 constexpr int KV_SLOT = SLOT_KEYS * DH * 2;     // 32 KB: [dh half][128 rows][128 B]
@@ -461,7 +466,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int c = 0; c < 64; c += 2) {
           const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
           float2 pp;
-          if ((c >> 1) % 4 == 3) {
+          if (SD_POLY_DEN > 0 && (c >> 1) % SD_POLY_DEN == SD_POLY_DEN - 1) {
             pp = exp2_poly2(x.x, x.y);
           } else {
             pp.x = ex2(x.x);

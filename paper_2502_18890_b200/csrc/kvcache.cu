@@ -31,36 +31,42 @@ struct ScoreShape {
   static_assert(DH * ES >= 16 && LPH <= 32 && 32 % LPH == 0, "row must be >= 16 B and split evenly");
 };
 
-// part(h) for all heads h < Hk of row `pos`; lane-uniform result in parts[]
-template <int DH, typename KT, int HKMAX>
-__device__ __forceinline__ void score_row(const float* __restrict__ qg, const KT* __restrict__ Kl,
-                                          int64_t head_stride, int64_t pos, int Hk, int lane, float (&parts)[HKMAX]) {
+// U consecutive rows at once (loads of all U rows first); rows >= n_valid skipped
+template <int DH, typename KT, int HKMAX, int U>
+__device__ __forceinline__ void score_rows(const float* __restrict__ qg, const KT* __restrict__ Kl, int64_t head_stride,
+                                           int64_t pos0, int n_valid, int Hk, int lane, float (&parts)[U][HKMAX]) {
   using S = ScoreShape<DH, KT>;
   constexpr int NL = (HKMAX + S::RPW - 1) / S::RPW;
   const int sub = lane / S::LPH, d0 = (lane % S::LPH) * S::VEC;
-  float p[NL];
-  uint4 raw[NL];
+  uint4 raw[U][NL];
 #pragma unroll
-  for (int it = 0; it < NL; ++it) {  // all loads first (NL x 16 B in flight per lane)
-    const int h = it * S::RPW + sub;
-    raw[it] = make_uint4(0, 0, 0, 0);
-    if (h < Hk) raw[it] = __ldg(reinterpret_cast<const uint4*>(Kl + h * head_stride + pos * DH + d0));
-  }
+  for (int u = 0; u < U; ++u)
 #pragma unroll
-  for (int it = 0; it < NL; ++it) {
-    const int h = it * S::RPW + sub;
-    const KT* e = reinterpret_cast<const KT*>(&raw[it]);
-    float acc = 0.f;
-    if (h < Hk) {
-#pragma unroll
-      for (int v = 0; v < S::VEC; ++v) acc = fmaf(qg[h * DH + d0 + v], to_f(e[v]), acc);
+    for (int it = 0; it < NL; ++it) {
+      const int h = it * S::RPW + sub;
+      raw[u][it] = make_uint4(0, 0, 0, 0);
+      if (h < Hk && u < n_valid)
+        raw[u][it] = __ldg(reinterpret_cast<const uint4*>(Kl + h * head_stride + (pos0 + u) * DH + d0));
     }
 #pragma unroll
-    for (int o = S::LPH / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    p[it] = acc;
-  }
+  for (int u = 0; u < U; ++u) {
+    float p[NL];
 #pragma unroll
-  for (int h = 0; h < HKMAX; ++h) parts[h] = __shfl_sync(0xffffffffu, p[h / S::RPW], (h % S::RPW) * S::LPH);
+    for (int it = 0; it < NL; ++it) {
+      const int h = it * S::RPW + sub;
+      const KT* e = reinterpret_cast<const KT*>(&raw[u][it]);
+      float acc = 0.f;
+      if (h < Hk) {
+#pragma unroll
+        for (int v = 0; v < S::VEC; ++v) acc = fmaf(qg[h * DH + d0 + v], to_f(e[v]), acc);
+      }
+#pragma unroll
+      for (int o = S::LPH / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      p[it] = acc;
+    }
+#pragma unroll
+    for (int h = 0; h < HKMAX; ++h) parts[u][h] = __shfl_sync(0xffffffffu, p[h / S::RPW], (h % S::RPW) * S::LPH);
+  }
 }
 
 // grouped query per kv head, g summed in ascending order (kvcache.py:262-264)
@@ -96,17 +102,22 @@ __global__ void __launch_bounds__(256) score_kernel(const float* __restrict__ q_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = end - start;
   const KT* Kl = K + layer * layer_stride;
-  for (int r = 0; r < 8; ++r) {
-    const int i = blockIdx.x * 64 + warp * 8 + r;
-    if (i >= n) break;
-    float parts[HKMAX];
-    score_row<DH, KT, HKMAX>(qg, Kl, head_stride, start + i, Hk, lane, parts);
-    if (per_head && lane < Hk) {
+  for (int r = 0; r < 8; r += 4) {
+    const int i0 = blockIdx.x * 64 + warp * 8 + r;
+    if (i0 >= n) break;
+    float parts[4][HKMAX];
+    score_rows<DH, KT, HKMAX, 4>(qg, Kl, head_stride, start + i0, n - i0, Hk, lane, parts);
 #pragma unroll
-      for (int h = 0; h < HKMAX; ++h)
-        if (h == lane) per_head[((int64_t)layer * Hk + h) * n + i] = parts[h];
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u;
+      if (i >= n) break;
+      if (per_head && lane < Hk) {
+#pragma unroll
+        for (int h = 0; h < HKMAX; ++h)
+          if (h == lane) per_head[((int64_t)layer * Hk + h) * n + i] = parts[u][h];
+      }
+      if (lane == 0 && scores) scores[(int64_t)layer * n + i] = sum_heads(parts[u], Hk);
     }
-    if (lane == 0 && scores) scores[(int64_t)layer * n + i] = sum_heads(parts, Hk);
   }
 }
 
@@ -135,6 +146,7 @@ __device__ __forceinline__ uint64_t sel_key(float score, int pos) {
 constexpr int RF_CLUSTER = 4;     // CTAs per layer in the fused refresh
 constexpr int RF_THREADS = 512;
 constexpr int RF_MAX_TAKE = 8192;
+constexpr int RF_UNROLL = 4;     // positions per warp iteration in the scoring phase
 constexpr float QNAN = __builtin_nanf("");
 
 struct RefreshArgs {
@@ -213,14 +225,14 @@ __global__ void __cluster_dims__(RF_CLUSTER, 1, 1) __launch_bounds__(RF_THREADS)
     __syncthreads();
     const KT* Kl = static_cast<const KT*>(a.fk) + layer * a.f_ls;
     float* out = a.scores_ws + (int64_t)layer * n;
-    for (int i = i0 + warp * 2; i < i1; i += (RF_THREADS / 32) * 2) {
-      float p0[HKMAX], p1[HKMAX];
-      score_row<DH, KT, HKMAX>(qg, Kl, a.f_hs, sink + i, Hk, lane, p0);
-      if (i + 1 < i1) score_row<DH, KT, HKMAX>(qg, Kl, a.f_hs, sink + i + 1, Hk, lane, p1);
-      if (lane == 0) {
-        out[i] = sum_heads(p0, Hk);
-        if (i + 1 < i1) out[i + 1] = sum_heads(p1, Hk);
-      }
+    // RF_UNROLL positions per warp iteration: all their loads are issued before
+    // the first dot product (RF_UNROLL x NL x 16 B in flight per lane)
+    for (int i = i0 + warp * RF_UNROLL; i < i1; i += (RF_THREADS / 32) * RF_UNROLL) {
+      float p[RF_UNROLL][HKMAX];
+      score_rows<DH, KT, HKMAX, RF_UNROLL>(qg, Kl, a.f_hs, sink + i, i1 - i, Hk, lane, p);
+#pragma unroll
+      for (int u = 0; u < RF_UNROLL; ++u)
+        if (lane == u && i + u < i1) out[i + u] = sum_heads(p[u], Hk);
     }
     __syncthreads();
   }
@@ -422,55 +434,75 @@ __global__ void __launch_bounds__(256) partial_step_kernel(StepArgs sa) {
   int32_t* ring = a.ring + (int64_t)layer * cap;
   int32_t* fl = a.freel + (int64_t)layer * cap;
   int32_t* m = a.meta + layer * SD_PM_WORDS;
-  if (tid == 0) {
+  if (tid < 32) {  // warp 0: the ring / free-stack bookkeeping, lanes in parallel
+    const int lane = tid;
     const int na = sa.result ? sa.result[SD_RES_ACCEPTED] : sa.a_host;
     const int first = sa.result ? sa.result[SD_RES_BASE] : sa.first_pos_host;
     const int prot = sa.result ? na : sa.protected_host;
-    int count = m[SD_PM_COUNT], hi = m[SD_PM_HI], head = m[SD_PM_HEAD], len = m[SD_PM_LEN], nfree = m[SD_PM_NFREE];
+    const int count = m[SD_PM_COUNT], hi0 = m[SD_PM_HI], head = m[SD_PM_HEAD], len = m[SD_PM_LEN];
+    const int nfree = m[SD_PM_NFREE];
     int over = sa.evict ? count + na - sa.budget : 0;
     if (over < 0) over = 0;
-    s_bad = (na > PS_MAX || over > PS_MAX || over > len || (over > 0 && count + na - sa.sink - over < prot));
-    if (!s_bad) {
-      for (int e = 0; e < over; ++e) {  // pop the least important tail
-        const int slot = ring[(head + len - 1) % cap];
-        --len;
+    const int nf = nfree + over;  // free slots after the eviction
+    const int fresh = na > nf ? na - nf : 0;
+    const bool bad = na > PS_MAX || over > PS_MAX || over > len || (over > 0 && count + na - sa.sink - over < prot) ||
+                     hi0 + fresh > cap;
+    if (!bad) {
+      for (int e = lane; e < over; e += 32) {  // pop the least important tail; push onto the free stack
+        const int slot = ring[(head + len - 1 - e) % cap];
         ev_slot[e] = slot;
         ev_pos[e] = lpos[slot];
-        fl[nfree++] = slot;
+        fl[nfree + e] = slot;
       }
-      for (int i = 0; i < na; ++i) new_slot[i] = nfree > 0 ? fl[--nfree] : hi++;
-      s_bad = hi > cap;
+      __syncwarp();
+      for (int i = lane; i < na; i += 32) {  // pop the free stack (top first), then fresh slots at hi
+        const int slot = i < nf ? fl[nf - 1 - i] : hi0 + (i - nf);
+        new_slot[i] = slot;
+        ring[((head - na + i) % cap + cap) % cap] = slot;  // ring head, in position order
+      }
     }
-    if (!s_bad) {
-      head = ((head - na) % cap + cap) % cap;
-      for (int i = 0; i < na; ++i) ring[(head + i) % cap] = new_slot[i];
-      len += na;
-      count += na - over;
-      m[SD_PM_COUNT] = count;
-      m[SD_PM_HI] = hi;
-      m[SD_PM_HEAD] = head;
-      m[SD_PM_LEN] = len;
-      m[SD_PM_NFREE] = nfree;
-    } else {
-      m[SD_PM_ERR] = 1;  // SinkViolation / capacity: nothing changed
+    if (lane == 0) {
+      if (!bad) {
+        m[SD_PM_COUNT] = count + na - over;
+        m[SD_PM_HI] = hi0 + fresh;
+        m[SD_PM_HEAD] = ((head - na) % cap + cap) % cap;
+        m[SD_PM_LEN] = len - over + na;
+        m[SD_PM_NFREE] = nf - (na < nf ? na : nf);
+      } else {
+        m[SD_PM_ERR] = 1;  // SinkViolation / capacity: nothing changed
+      }
+      s_bad = bad;
+      s_a = na;
+      s_over = over;
+      s_first = first;
+      s_count_after = count + na - over;
+      s_hi = hi0 + fresh;
     }
-    s_a = na;
-    s_over = over;
-    s_first = first;
-    s_count_after = count;
-    s_hi = hi;
   }
   __syncthreads();
   if (s_bad) return;
   const int na = s_a, over = s_over, hi = s_hi;
-  if (over > 0)
-    for (int s = tid; s < hi; s += blockDim.x) {
-      const int p = lpos[s];
-      if (p < 0) continue;
-      int dec = 0;
-      for (int e = 0; e < over; ++e) dec += ev_pos[e] < p;
-      lrank[s] -= dec;
+  if (over > 0) {
+    // survivors drop one rank per evicted entry with a smaller position; slots
+    // are read PS_U at a time so their loads are in flight together
+    constexpr int PS_U = 8;
+    for (int s0 = tid; s0 < hi; s0 += PS_U * blockDim.x) {
+      int p[PS_U], r[PS_U];
+#pragma unroll
+      for (int u = 0; u < PS_U; ++u) {
+        const int s = s0 + u * blockDim.x;
+        p[u] = s < hi ? lpos[s] : -1;
+        r[u] = s < hi ? lrank[s] : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < PS_U; ++u) {
+        if (p[u] < 0) continue;
+        int dec = 0;
+        for (int e = 0; e < over; ++e) dec += ev_pos[e] < p[u];
+        if (dec) lrank[s0 + u * blockDim.x] = r[u] - dec;
+      }
     }
+  }
   __syncthreads();
   for (int e = tid; e < over; e += blockDim.x) {
     lpos[ev_slot[e]] = -1;
