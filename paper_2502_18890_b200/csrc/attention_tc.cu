@@ -17,6 +17,12 @@
 //               online softmax in base 2 with lazy rescale (O is rescaled in TMEM
 //               only when the row max grows by > 2^8); P (bf16x2) is written back
 //               over the first 32 columns of the S buffer it came from.
+//               A second tile of <= 64 rows (T <= 48 at G = 4) runs as M=64
+//               MMAs, whose rows TMEM spreads over the four sub-partitions
+//               (lanes 0-15 of each): warps 8-11 then take 16 rows each, two
+//               threads per row (16x32bx2 accesses), so no SM sub-partition
+//               carries two full softmax warps. Full tiles take a third of
+//               their exps on the FMA pipe (degree-3 polynomial).
 // S(j+2) reuses buffer j%2, whose P(j) is still an operand of O += P(j) V(j).
 // Both MMAs come from the same issuer thread with the PV first, and tcgen05.mma
 // instructions of one thread execute in issue order (the pipelined-pair rule of
@@ -44,7 +50,7 @@ constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 // 1 of every SD_POLY_DEN exp2 pairs of the softmax runs as a polynomial on the
 // FMA pipe, the rest on the MUFU (0: all MUFU)
 #ifndef SD_POLY_DEN
-#define SD_POLY_DEN 4
+#define SD_POLY_DEN 3
 #endif
 
 constexpr int Q_BYTES = ROWS * DH * 2;          // 64 KB: [mt][dh half][128 rows][128 B]
@@ -122,14 +128,14 @@ __device__ __forceinline__ void trace(int role, int j, int ev) {
 // MMA issue stream of one M-tile (warps 1 / 2; the whole warp runs the loop,
 // one elected lane issues). TMEM base is 0: the CTA owns all 512 columns.
 //   S[MT][j%2] = Q[MT] K(j)^T (8 K=16 steps), O[MT] += P(j) V(j) (4 steps)
-template <int MT>
+template <int MT, int M>
 __device__ __forceinline__ void issue_loop(uint8_t* smem, int n_tiles, uint32_t p_bar_count, uint64_t* k_full,
                                            uint64_t* k_empty, uint64_t* v_full, uint64_t* v_empty, uint64_t* s_full,
                                            uint64_t* pv_done, uint64_t* o_final) {
   __syncwarp();
   const bool leader = elect_one();
-  constexpr uint32_t id_qk = idesc_bf16(BN, false);
-  constexpr uint32_t id_pv = idesc_bf16(DH, true);
+  constexpr uint32_t id_qk = idesc_bf16(BN, false, M);
+  constexpr uint32_t id_pv = idesc_bf16(DH, true, M);
   constexpr uint32_t O_COL = COL_O + 128 * MT;
   const uint32_t sb = smem_u32(smem);
   const uint32_t q_base = sb + OFF_Q + MT * 32768;
@@ -241,10 +247,17 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int cache_end = min(ctx, key_begin + chunk);
   const int key_end = last ? ctx + T : cache_end;  // the last chunk also takes the tree rows
   const int n_tiles = (key_end - key_begin + BN - 1) / BN;
+  // The second M-tile runs as an M=64 MMA when it holds <= 64 rows: its rows
+  // then sit in lanes 0-15 of each TMEM sub-partition (row 16k+i -> lane
+  // 32k+i), so they spread over several SM sub-partitions instead of doubling
+  // up on the first two with the first tile's rows, and each row is softmaxed
+  // by two threads (one per 32-key half: 16x32bx2 TMEM accesses).
+  const int rows1 = GT - rg - 128;
+  const bool m1_64 = rows1 > 0 && rows1 <= 64;
   int act[2];
   for (int mt = 0; mt < 2; ++mt) {
     int a = 0;
-    for (int w = 0; w < 4; ++w) a += (rg + 128 * mt + 32 * w) < GT;
+    for (int w = 0; w < 4; ++w) a += (mt == 1 && m1_64) ? (16 * w < rows1) : (rg + 128 * mt + 32 * w) < GT;
     act[mt] = a;
   }
   const int nm = act[1] > 0 ? 2 : 1;
@@ -363,12 +376,171 @@ __global__ void __launch_bounds__(THREADS, 1)
     // issue stream is then warp-uniform (uniform datapath, no per-MMA R2UR /
     // ELECT waterfall); one elected lane issues.
     if (mt == 0)
-      issue_loop<0>(smem, n_tiles, 32u * (uint32_t)(act[0] + 1), k_full, k_empty, v_full, v_empty, s_full, pv_done,
-                    o_final);
+      issue_loop<0, 128>(smem, n_tiles, 32u * (uint32_t)(act[0] + 1), k_full, k_empty, v_full, v_empty, s_full,
+                         pv_done, o_final);
+    else if (mt < nm && m1_64)
+      issue_loop<1, 64>(smem, n_tiles, 32u * (uint32_t)(act[1] + 1), k_full, k_empty, v_full, v_empty, s_full,
+                        pv_done, o_final);
     else if (mt < nm)
-      issue_loop<1>(smem, n_tiles, 32u * (uint32_t)(act[1] + 1), k_full, k_empty, v_full, v_empty, s_full, pv_done,
-                    o_final);
+      issue_loop<1, 128>(smem, n_tiles, 32u * (uint32_t)(act[1] + 1), k_full, k_empty, v_full, v_empty, s_full,
+                         pv_done, o_final);
 #endif
+  } else if (warp >= 8 && m1_64) {
+    // ================= softmax of an M=64 second tile =================
+    // warp 8+q: tile rows 16q..16q+15 (TMEM lanes 32q..32q+15); thread
+    // lane&15 -> row, lane>>4 -> key half of every 64-key tile. The two halves
+    // of a row combine their maxima with one shuffle per tile and their sums
+    // at the end; each rescales / writes its half of O and of P.
+    const int q = warp & 3, r16 = lane & 15, h = lane >> 4;
+    const int row1 = 16 * q + r16;
+    const int rho = rg + 128 + row1;
+    if (16 * q < rows1) {
+      const bool valid = row1 < rows1;
+      const int t = valid ? rho / p.G : 0;
+      const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+      uint32_t tmask[SD_MASK_WORDS];
+#pragma unroll
+      for (int w = 0; w < SD_MASK_WORDS; ++w) {
+        uint32_t bits = 0u;
+        const int lo = 32 * w;
+        if (lo <= t) {
+          bits = p.mask ? (w < p.mask_words ? p.mask[(int64_t)t * p.mask_words + w] : 0u) : 0xffffffffu;
+          const int lim = t - lo;
+          if (lim < 31) bits &= (2u << lim) - 1u;
+          if (lim < 32) bits |= 1u << lim;
+        }
+        tmask[w] = bits;
+      }
+      const uint32_t bar_count = 32u * (uint32_t)(act[1] + 1);
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < n_tiles; ++j) {
+        const int b = j & 1;
+        mbar_wait(&s_full[2 + b], (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t s_addr = tmem + lane_base + COL_S + 128 + 64 * b;
+        uint32_t sr[32];
+        tmem_ld16x2_32<32>(s_addr, sr);
+        tmem_wait_ld();
+        const int key0 = key_begin + j * BN + 32 * h;
+        const bool full = key_begin + j * BN + BN <= cache_end;  // tile-uniform
+        if (!full) {
+          uint32_t vis = 0u;
+          if (valid) {
+            for (int c = 0; c < 32; ++c) {
+              const int k = key0 + c;
+              bool on = false;
+              if (k < cache_end) {
+                on = true;
+              } else if (last && k < key_end) {
+                const int jt = k - ctx;
+                on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
+              }
+              vis |= (uint32_t)on << c;
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            if (!((vis >> c) & 1u)) sr[c] = __float_as_uint(-INFINITY);
+        }
+        float m11[11];
+#pragma unroll
+        for (int c = 0; c < 10; ++c)
+          m11[c] = fmax3(__uint_as_float(sr[c]), __uint_as_float(sr[c + 10]), __uint_as_float(sr[c + 20]));
+        m11[10] = fmaxf(__uint_as_float(sr[30]), __uint_as_float(sr[31]));
+        float mh = fmax3(fmax3(m11[0], m11[1], m11[2]), fmax3(m11[3], m11[4], m11[5]),
+                         fmax3(fmax3(m11[6], m11[7], m11[8]), m11[9], m11[10]));
+        mh = fmaxf(mh, __shfl_xor_sync(0xffffffffu, mh, 16));  // both halves of the row
+        const float mx = mh * LOG2E;
+        float scale = 1.f;
+        bool rescale = false;
+        if (mx > m_used + TAU) {
+          scale = m_used == -INFINITY ? 0.f : ex2(m_used - mx);
+          rescale = j > 0;
+          m_used = mx;
+          l *= scale;
+        }
+        uint32_t pk[16];
+        const float nm_used = m_used == -INFINITY ? 0.f : -m_used;
+        const uint64_t lg2 = f2(LOG2E, LOG2E), off = f2(nm_used, nm_used);
+        uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
+        if (full) {
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
+            float2 pp;
+            if (SD_POLY_DEN > 0 && (c >> 1) % SD_POLY_DEN == SD_POLY_DEN - 1) {
+              pp = exp2_poly3_pair(x.x, x.y);
+            } else {
+              pp.x = ex2(x.x);
+              pp.y = ex2(x.y);
+            }
+            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(pp.x, pp.y));
+            pk[c >> 1] = pack_bf16(pp.x, pp.y);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; c += 2) {
+            const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
+            const float e0 = ex2(x.x), e1 = ex2(x.y);
+            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(e0, e1));
+            pk[c >> 1] = pack_bf16(e0, e1);
+          }
+        }
+        {
+          const float2 a2 = unf2(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));
+          l += a2.x + a2.y;
+        }
+        if (__any_sync(0xffffffffu, rescale)) {
+          if (j > 0) mbar_wait(&pv_done[2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int q2 = 0; q2 < 2; ++q2) {  // this half's 64 columns of O: [64h + 32 q2, +32)
+            uint32_t o[32];
+            const uint32_t ta = tmem + lane_base + COL_O + 128 + 32 * q2;
+            tmem_ld16x2_32<64>(ta, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * (rescale ? scale : 1.f));
+            tmem_st16x2_32<64>(ta, o);
+          }
+          tmem_wait_st();
+        }
+        tmem_st16x2_16<16>(s_addr, pk);  // P(j): keys 32h.. -> columns 16h..16h+15
+        tmem_wait_st();
+        tc_fence_before();
+        asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 + b), "r"(bar_count) : "memory");
+      }
+      // ---- epilogue ----
+      for (int m2 = 0; m2 < nm; ++m2) mbar_wait(&o_final[m2], 0);
+      tc_fence_after();
+      const float lt = l + __shfl_xor_sync(0xffffffffu, l, 16);
+      const int g = rho - t * p.G;
+      const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
+      const float inv = lt > 0.f ? 1.f / lt : 0.f;
+      uint8_t* stage = smem + OFF_K + (warp - 4) * (32 * DH * 4);  // 16 rows x 512 B
+#pragma unroll
+      for (int q2 = 0; q2 < 2; ++q2) {
+        uint32_t o[32];
+        tmem_ld16x2_32<64>(tmem + lane_base + COL_O + 128 + 32 * q2, o);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const int chunk = 16 * h + 8 * q2 + c;  // 16-byte chunk of the row (4 floats)
+          *reinterpret_cast<float4*>(stage + r16 * 512 + ((chunk ^ r16) << 4)) =
+              make_float4(__uint_as_float(o[4 * c]) * inv, __uint_as_float(o[4 * c + 1]) * inv,
+                          __uint_as_float(o[4 * c + 2]) * inv, __uint_as_float(o[4 * c + 3]) * inv);
+        }
+      }
+      __syncwarp();
+      for (int rr = 0; rr < 16; ++rr) {
+        const int64_t oi_r = __shfl_sync(0xffffffffu, oi, rr);
+        const bool v_r = __shfl_sync(0xffffffffu, valid, rr);
+        if (v_r)
+          reinterpret_cast<float4*>(p.ws_o + oi_r * DH)[lane] =
+              *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
+      }
+      if (valid && h == 0) p.ws_lse[oi] = lt > 0.f ? (m_used + __log2f(lt)) / LOG2E : -INFINITY;
+    }
   } else if (warp >= 4) {
     // ================= softmax warpgroups =================
     const int mt = (warp - 4) >> 2, wl = warp & 3;
@@ -417,7 +589,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           continue;
         }
         const int key0 = key_begin + j * BN;
-        const bool full = valid && key0 + BN <= cache_end;
+        // warp-uniform: a tile wholly inside the committed cache has no masked
+        // keys (rows beyond GT hold zero queries: finite garbage, never written)
+        const bool full = key0 + BN <= cache_end;
         if (!full) {
           uint64_t vis = 0ull;  // built without indexing sr[] (keeps it in registers)
           if (valid) {
@@ -460,20 +634,37 @@ __global__ void __launch_bounds__(THREADS, 1)
         const float nm_used = m_used == -INFINITY ? 0.f : -m_used;
         const uint64_t lg2 = f2(LOG2E, LOG2E), off = f2(nm_used, nm_used);
         uint64_t acc[4] = {0ull, 0ull, 0ull, 0ull};
-        // p = 2^(s log2e - m): packed scale, exps split between the MUFU (3 of 4
-        // pairs) and the FMA pipe (1 of 4), packed row sums
+        // p = 2^(s log2e - m): packed scale, packed row sums; the exps split
+        // between the MUFU and (1 of every SD_POLY_DEN pairs) the FMA pipe: a
+        // degree-3 polynomial on full tiles, the -inf-exact one on masked tiles
+        if (full) {
 #pragma unroll
-        for (int c = 0; c < 64; c += 2) {
-          const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
-          float2 pp;
-          if (SD_POLY_DEN > 0 && (c >> 1) % SD_POLY_DEN == SD_POLY_DEN - 1) {
-            pp = exp2_poly2(x.x, x.y);
-          } else {
-            pp.x = ex2(x.x);
-            pp.y = ex2(x.y);
+          for (int c = 0; c < 64; c += 2) {
+            const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
+            float2 pp;
+            if (SD_POLY_DEN > 0 && (c >> 1) % SD_POLY_DEN == SD_POLY_DEN - 1) {
+              pp = exp2_poly3_pair(x.x, x.y);
+            } else {
+              pp.x = ex2(x.x);
+              pp.y = ex2(x.y);
+            }
+            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(pp.x, pp.y));
+            pk[c >> 1] = pack_bf16(pp.x, pp.y);
           }
-          acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(pp.x, pp.y));
-          pk[c >> 1] = pack_bf16(pp.x, pp.y);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const float2 x = unf2(ffma2(f2(__uint_as_float(sr[c]), __uint_as_float(sr[c + 1])), lg2, off));
+            float2 pp;
+            if (SD_POLY_DEN > 0 && (c >> 1) % SD_POLY_DEN == SD_POLY_DEN - 1) {
+              pp = exp2_poly2(x.x, x.y);
+            } else {
+              pp.x = ex2(x.x);
+              pp.y = ex2(x.y);
+            }
+            acc[(c >> 1) & 3] = fadd2(acc[(c >> 1) & 3], f2(pp.x, pp.y));
+            pk[c >> 1] = pack_bf16(pp.x, pp.y);
+          }
         }
         {
           const float2 a = unf2(fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3])));

@@ -97,10 +97,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
   d |= (uint64_t)2 << 61;
   return d;
 }
-// instruction descriptor, kind::f16: D f32, A/B bf16, M=128
-__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool b_mn_major) {
+// instruction descriptor, kind::f16: D f32, A/B bf16, M = 128 (or 64)
+__host__ __device__ constexpr uint32_t idesc_bf16(int N, bool b_mn_major, int M = 128) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(128 >> 4) << 24);
+         ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
@@ -181,6 +181,23 @@ __device__ __forceinline__ float2 exp2_poly2(float x0, float x1) {
   y.y = x1 < -125.f ? 0.f : __uint_as_float(__float_as_uint(pv.y) + (__float_as_uint(tv.y) << 23));
   return y;
 }
+// 2^x for a pair on the FMA pipe, for P tiles that are rounded to bf16 anyway:
+// x clamped at -127 (no exponent wrap), round-to-nearest split x = i + f with
+// f in [-1/2, 1/2], degree-3 fit of 2^f (max rel. error 1.03e-4, 20x below a
+// bf16 ulp), exponent inserted with one shift-add per value. Callers keep
+// exactly-masked (-inf) scores on the MUFU path, which returns exact zeros.
+__device__ __forceinline__ float2 exp2_poly3_pair(float x0, float x1) {
+  const uint64_t X = f2(fmaxf(x0, -127.f), fmaxf(x1, -127.f));
+  const uint64_t t = fadd2(X, f2(12582912.f, 12582912.f));
+  const uint64_t f = ffma2(fadd2(t, f2(-12582912.f, -12582912.f)), f2(-1.f, -1.f), X);
+  uint64_t p = ffma2(f2(0.055922120809555054f, 0.055922120809555054f), f,
+                     f2(0.2426406890153885f, 0.2426406890153885f));
+  p = ffma2(p, f, f2(0.6931210160255432f, 0.6931210160255432f));
+  p = ffma2(p, f, f2(0.9999244213104248f, 0.9999244213104248f));
+  const float2 pv = unf2(p), tv = unf2(t);
+  return make_float2(__uint_as_float((__float_as_uint(tv.x) << 23) + __float_as_uint(pv.x)),
+                     __uint_as_float((__float_as_uint(tv.y) << 23) + __float_as_uint(pv.y)));
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
@@ -208,7 +225,27 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
                : "memory");
 }
 
-
+// 16-lane shapes (M=64 accumulators: rows 16k..16k+15 live in lanes 0-15 of
+// sub-partition k): threads 0-15 access lanes base..base+15 at columns
+// [col, col+n), threads 16-31 the same lanes at [col+OFF, col+OFF+n)
+template <int OFF>
+__device__ __forceinline__ void tmem_ld16x2_32(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.16x32bx2.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32], %33;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+               : "r"(taddr), "n"(OFF));
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st16x2_32(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x32.b32 [%0], %33, {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]), "n"(OFF)
+               : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void tmem_st16x2_16(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.16x32bx2.x16.b32 [%0], %17, {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16};"
+               :: "r"(taddr), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "n"(OFF)
+               : "memory");
+}
 
 }  // namespace tc
 }  // namespace sd

@@ -61,3 +61,13 @@ for j in list(range(0, 6)) + list(range(20, 24)):
                 row.append(f"{['P', 'M', 'S0', 'S1'][role]}.{nm}={v - base}")
     print(f"tile {j:2d}: " + "  ".join(row))
 
+
+print("\nper-tile deltas (cycles), tiles 20..27:")
+print(" j | S0: wait  ld->exp  exp->resc  resc->P | S1: wait  ld->exp  exp->resc  resc->P | M: v->P  P->PV | S0 period")
+prev = None
+for j in range(20, 28):
+    s0, s1, m = t[2, j], t[3, j], t[1, j]
+    per = (s0[4] - prev) if prev is not None else 0
+    prev = s0[4]
+    print(f"{j:2d} | {s0[1]-s0[0]:6d} {s0[2]-s0[1]:7d} {s0[3]-s0[2]:9d} {s0[4]-s0[3]:8d} | "
+          f"{s1[1]-s1[0]:6d} {s1[2]-s1[1]:7d} {s1[3]-s1[2]:9d} {s1[4]-s1[3]:8d} | {m[4]-m[3]:5d} {m[6]-m[4]:5d} | {per}")
