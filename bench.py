@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--ctx", type=int, default=None, help="committed context at the timed steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--attn-reps", type=int, default=3)
+    ap.add_argument("--ngram-stress", action="store_true",
+                    help="SURVEY §8d stress line: before the timed steps, seed the n-gram table with k=20 unique "
+                         "frequent branches from the draft's first token, so every tree has 1+40+60 = 101 rows")
     return ap.parse_args()
 
 
@@ -209,6 +212,10 @@ def main():
     torch.cuda.synchronize()
     for _ in range(args.warmup):
         sess.step()
+    if args.ngram_stress:
+        seed_unique_ngrams(sess, model, c)
+        for _ in range(2):
+            sess.step()
     # ---- timed region: device time (events on the launching stream), max over ranks ----
     if world > 1:
         dist.barrier()
@@ -263,7 +270,9 @@ def main():
         "ms_per_step": dev_s * 1e3 / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init weights; random prompt prefilled; synthetic KV beyond the prefix)",
-        "config": {"workload": workload_name(args.config, c, ctx), "ctx": ctx, "global_batch": 1,
+        "config": {"workload": workload_name(args.config, c, ctx) + (" (n-gram stress: 101-row trees)"
+                                                                     if args.ngram_stress else ""),
+                   "ctx": ctx, "global_batch": 1,
                    "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (12.4 GB weights + KV per step)"},
         "e2e": {"value": tokens / wall, "unit": "tokens/s", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 128,
                 "note": "Session.step() wall clock incl. per-step result D2H"},
@@ -288,6 +297,22 @@ def main():
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
+
+
+def seed_unique_ngrams(sess, model, c, k=20, weight=64):
+    """Insert k grams (x, a, b, c) with random continuations, each counted
+    `weight` times, for the draft's likely first token x (random-init weights
+    repeat one token, so x is the last emitted token): retrieval then returns
+    k unique chains that do not merge with the head trie, and the verify tree
+    has its maximum 1 + 40 + 3k rows."""
+    import torch
+    g = torch.Generator()
+    g.manual_seed(7)
+    x = sess.emitted[-1] if sess.emitted else sess.tokens[-1]
+    for i in range(k):
+        tail = torch.randint(0, c["V"], (3,), generator=g).tolist()
+        for _ in range(weight):
+            sess.ngrams.update([x] + tail, [])
 
 
 def time_verify_attention(sess, model, rows, ctx, reps=3):

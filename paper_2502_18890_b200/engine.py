@@ -159,10 +159,10 @@ class Session:
         self.state[L.ST_PENDING] = self.tokens[-1]
         self.state[L.ST_BASE] = len(self.tokens) - 1
         self._ev = torch.cuda.Event()
-        # CUDA-graph replay; a sharded session captures its NCCL all-gathers with
-        # the step (NCCL supports stream capture) and falls back to eager steps
-        # if the capture is refused. gloo process groups cannot be captured.
-        self.use_graph = graph and (model.world == 1 or _nccl_group(model.group))
+        # CUDA-graph replay on one GPU. Sharded sessions step eagerly: capturing
+        # the NCCL all-gathers with the step is possible but has not been run
+        # on a multi-GPU node yet, and gloo groups cannot be captured.
+        self.use_graph = graph and model.world == 1
         self._graph: torch.cuda.CUDAGraph | None = None
         self._eager_steps = 0
         if prefill:
@@ -410,10 +410,6 @@ class Session:
     def device_error(self) -> int:
         return int(self.state[L.ST_ERROR].item()) or self.partial.device_error()
 
-
-def _nccl_group(group) -> bool:
-    import torch.distributed as dist
-    return dist.is_initialized() and dist.get_backend(group) == "nccl"
 
 
 def prefill(model: TinyTransformer, prompt: list[int], config: EngineConfig) -> Session:
