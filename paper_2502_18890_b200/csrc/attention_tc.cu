@@ -13,16 +13,17 @@
 //   warps 1, 2  one MMA-issuer thread per 128-row M-tile: S[mt][j%2] = Q K(j)^T
 //               (M=128, N=64, SS) and O[mt] += P(j) V(j) (M=128, N=128, A = P
 //               from TMEM, B = V MN-major straight from the TMA layout);
-//   warps 4-11  two softmax warpgroups, one per M-tile: thread = row = TMEM lane;
-//               online softmax in base 2 with lazy rescale (O is rescaled in TMEM
-//               only when the row max grows by > 2^8); P (bf16x2) is written back
-//               over the first 32 columns of the S buffer it came from.
-//               A second tile of <= 64 rows (T <= 48 at G = 4) runs as M=64
-//               MMAs, whose rows TMEM spreads over the four sub-partitions
-//               (lanes 0-15 of each): warps 8-11 then take 16 rows each, two
-//               threads per row (16x32bx2 accesses), so no SM sub-partition
-//               carries two full softmax warps. Full tiles take a third of
-//               their exps on the FMA pipe (degree-3 polynomial).
+//   warps 4-15  softmax, 16 rows per warp and two threads per row (one per
+//               32-key half of every 64-key tile; 16x32bx2 TMEM accesses, the
+//               halves' maxima combined by one shuffle): warps 4-11 the first
+//               128-row M-tile (two warps per TMEM sub-partition), warps 12-15
+//               the second tile. A second tile of <= 64 rows runs as M=64 MMAs,
+//               whose rows TMEM spreads over the four sub-partitions (lanes
+//               0-15 of each); a larger one keeps thread = row. Online softmax
+//               in base 2 with lazy rescale (O is rescaled in TMEM only when the
+//               row max grows by > 2^8); full tiles take a third of their exps
+//               on the FMA pipe (degree-3 polynomial); P (bf16x2) is written
+//               back over the first 32 columns of the S buffer it came from.
 // S(j+2) reuses buffer j%2, whose P(j) is still an operand of O += P(j) V(j).
 // Both MMAs come from the same issuer thread with the PV first, and tcgen05.mma
 // instructions of one thread execute in issue order (the pipelined-pair rule of
@@ -43,8 +44,11 @@ constexpr int DH = 128;
 constexpr int SLOT_KEYS = 128;
 constexpr int KST = 2;          // K ring depth (32 KB slots)
 constexpr int VST = 3;          // V ring depth (V is held until the PV of its sub-tiles)
-constexpr int THREADS = 384;
-constexpr int ROWS = 256;       // query rows per CTA (2 M-tiles)
+constexpr int THREADS = 512;    // 4 role warps + 12 softmax warps
+#ifndef SD_TC_ROWS
+#define SD_TC_ROWS 256
+#endif
+constexpr int ROWS = SD_TC_ROWS;  // query rows per CTA (2 M-tiles)
 constexpr float LOG2E = 1.4426950408889634f;
 constexpr float TAU = 8.0f;     // lazy-rescale threshold (log2 units)
 // 1 of every SD_POLY_DEN exp2 pairs of the softmax runs as a polynomial on the
@@ -254,12 +258,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   // by two threads (one per 32-key half: 16x32bx2 TMEM accesses).
   const int rows1 = GT - rg - 128;
   const bool m1_64 = rows1 > 0 && rows1 <= 64;
-  int act[2];
-  for (int mt = 0; mt < 2; ++mt) {
-    int a = 0;
-    for (int w = 0; w < 4; ++w) a += (mt == 1 && m1_64) ? (16 * w < rows1) : (rg + 128 * mt + 32 * w) < GT;
-    act[mt] = a;
-  }
+  int act[2];  // softmax warps per tile (named-barrier arrivals)
+  act[0] = 0;
+  for (int g = 0; g < 8; ++g) act[0] += rg + 16 * g < GT;
+  act[1] = 0;
+  for (int w = 0; w < 4; ++w) act[1] += m1_64 ? (16 * w < rows1) : (32 * w < rows1);
   const int nm = act[1] > 0 ? 2 : 1;
 
   // ---- barriers first, so the TMA producers start streaming at once ----
@@ -287,7 +290,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t tmem = 0;
   if (warp != 0 && warp != 3) {
     // ---- stage Q (M-tiles, K-major SW128) while the first K/V tiles are in flight ----
-    constexpr int NT = THREADS - 64;  // warps 1, 2, 4..11
+    constexpr int NT = THREADS - 64;  // warps 1, 2, 4..15
     const int qt = tid < 96 ? tid - 32 : tid - 64;
     constexpr int PER = (ROWS * (DH / 8) + NT - 1) / NT;  // 16-byte chunks per thread
     uint4 v[PER];
@@ -385,19 +388,25 @@ __global__ void __launch_bounds__(THREADS, 1)
       issue_loop<1, 128>(smem, n_tiles, 32u * (uint32_t)(act[1] + 1), k_full, k_empty, v_full, v_empty, s_full,
                          pv_done, o_final);
 #endif
-  } else if (warp >= 8 && m1_64) {
-    // ================= softmax of an M=64 second tile =================
-    // warp 8+q: tile rows 16q..16q+15 (TMEM lanes 32q..32q+15); thread
-    // lane&15 -> row, lane>>4 -> key half of every 64-key tile. The two halves
-    // of a row combine their maxima with one shuffle per tile and their sums
-    // at the end; each rescales / writes its half of O and of P.
+  } else if (warp >= 4 && (warp < 12 || m1_64)) {
+    // ================= softmax, 16 rows per warp, two threads per row =================
+    // Tile 0 (M=128): warp 4+4s+q takes tile rows 32q+16s..+15 (TMEM lanes
+    // 32q+16s..); an M=64 tile 1: warp 12+q takes rows 16q..16q+15 (lanes
+    // 32q..32q+15). Thread lane&15 -> row, lane>>4 -> 32-key half of every
+    // 64-key tile (16x32bx2 TMEM accesses). The two halves of a row combine
+    // their maxima with one shuffle per tile and their sums at the end; each
+    // rescales / writes its half of O and of P.
+    const int mt = warp >= 12 ? 1 : 0;
     const int q = warp & 3, r16 = lane & 15, h = lane >> 4;
-    const int row1 = 16 * q + r16;
-    const int rho = rg + 128 + row1;
-    if (16 * q < rows1) {
-      const bool valid = row1 < rows1;
+    const int sub = mt == 0 ? ((warp - 4) >> 2) : 0;
+    const int lane0 = 32 * q + 16 * sub;                         // first TMEM lane of this warp
+    const int row1 = mt == 0 ? lane0 + r16 : 16 * q + r16;       // row within the tile
+    const int tile_rows = mt == 0 ? min(128, GT - rg) : rows1;
+    const int rho = rg + 128 * mt + row1;
+    if (row1 - r16 < tile_rows) {
+      const bool valid = row1 < tile_rows;
       const int t = valid ? rho / p.G : 0;
-      const uint32_t lane_base = (uint32_t)(32 * q) << 16;
+      const uint32_t lane_base = (uint32_t)lane0 << 16;
       uint32_t tmask[SD_MASK_WORDS];
 #pragma unroll
       for (int w = 0; w < SD_MASK_WORDS; ++w) {
@@ -411,13 +420,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         tmask[w] = bits;
       }
-      const uint32_t bar_count = 32u * (uint32_t)(act[1] + 1);
+      const uint32_t bar_count = 32u * (uint32_t)(act[mt] + 1);
       float m_used = -INFINITY, l = 0.f;
       for (int j = 0; j < n_tiles; ++j) {
         const int b = j & 1;
-        mbar_wait(&s_full[2 + b], (j >> 1) & 1);
+        mbar_wait(&s_full[2 * mt + b], (j >> 1) & 1);
         tc_fence_after();
-        const uint32_t s_addr = tmem + lane_base + COL_S + 128 + 64 * b;
+        const uint32_t s_addr = tmem + lane_base + COL_S + 128 * mt + 64 * b;
         uint32_t sr[32];
         tmem_ld16x2_32<32>(s_addr, sr);
         tmem_wait_ld();
@@ -491,12 +500,12 @@ __global__ void __launch_bounds__(THREADS, 1)
           l += a2.x + a2.y;
         }
         if (__any_sync(0xffffffffu, rescale)) {
-          if (j > 0) mbar_wait(&pv_done[2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          if (j > 0) mbar_wait(&pv_done[2 * mt + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll
           for (int q2 = 0; q2 < 2; ++q2) {  // this half's 64 columns of O: [64h + 32 q2, +32)
             uint32_t o[32];
-            const uint32_t ta = tmem + lane_base + COL_O + 128 + 32 * q2;
+            const uint32_t ta = tmem + lane_base + COL_O + 128 * mt + 32 * q2;
             tmem_ld16x2_32<64>(ta, o);
             tmem_wait_ld();
 #pragma unroll
@@ -508,7 +517,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_st16x2_16<16>(s_addr, pk);  // P(j): keys 32h.. -> columns 16h..16h+15
         tmem_wait_st();
         tc_fence_before();
-        asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 + b), "r"(bar_count) : "memory");
+        asm volatile("bar.arrive %0, %1;" ::"r"(2 + 2 * mt + b), "r"(bar_count) : "memory");
       }
       // ---- epilogue ----
       for (int m2 = 0; m2 < nm; ++m2) mbar_wait(&o_final[m2], 0);
@@ -517,11 +526,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
       const float inv = lt > 0.f ? 1.f / lt : 0.f;
-      uint8_t* stage = smem + OFF_K + (warp - 4) * (32 * DH * 4);  // 16 rows x 512 B
+      uint8_t* stage = smem + OFF_K + (warp - 4) * (16 * DH * 4);  // 16 rows x 512 B
 #pragma unroll
       for (int q2 = 0; q2 < 2; ++q2) {
         uint32_t o[32];
-        tmem_ld16x2_32<64>(tmem + lane_base + COL_O + 128 + 32 * q2, o);
+        tmem_ld16x2_32<64>(tmem + lane_base + COL_O + 128 * mt + 32 * q2, o);
         tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 8; ++c) {
@@ -541,9 +550,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (valid && h == 0) p.ws_lse[oi] = lt > 0.f ? (m_used + __log2f(lt)) / LOG2E : -INFINITY;
     }
-  } else if (warp >= 4) {
-    // ================= softmax warpgroups =================
-    const int mt = (warp - 4) >> 2, wl = warp & 3;
+  } else if (warp >= 12) {
+    // ================= softmax of an M=128 second tile: thread = row =================
+    const int mt = 1, wl = warp & 3;
     const int row = 32 * wl + lane;
     const int rho = rg + 128 * mt + row;
     const bool warp_active = (rg + 128 * mt + 32 * wl) < GT;
@@ -706,7 +715,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int g = rho - t * p.G;
       const int64_t oi = ((int64_t)blockIdx.x * p.T + t) * p.H + kvh * p.G + g;
       const float inv = l > 0.f ? 1.f / l : 0.f;
-      uint8_t* stage = smem + OFF_K + (warp - 4) * (32 * DH * 4);
+      uint8_t* stage = smem + OFF_K + 8 * (16 * DH * 4) + (warp - 12) * (32 * DH * 4);
 #pragma unroll
       for (int q4 = 0; q4 < 4; ++q4) {
         uint32_t o[32];
