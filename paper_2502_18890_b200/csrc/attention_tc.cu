@@ -132,6 +132,36 @@ __device__ __forceinline__ void trace(int role, int j, int ev) {
 // MMA issue stream of one M-tile (warps 1 / 2; the whole warp runs the loop,
 // one elected lane issues). TMEM base is 0: the CTA owns all 512 columns.
 //   S[MT][j%2] = Q[MT] K(j)^T (8 K=16 steps), O[MT] += P(j) V(j) (4 steps)
+// word w of a row's tree-visibility bits without dynamic register indexing
+__device__ __forceinline__ uint32_t pick_word(const uint32_t (&m)[SD_MASK_WORDS], int w) {
+  uint32_t r = 0u;
+#pragma unroll
+  for (int i = 0; i < SD_MASK_WORDS; ++i) r = w == i ? m[i] : r;
+  return r;
+}
+// visibility of keys key0..key0+31 for one query row: committed-cache keys
+// (< cache_end) are all visible; in the last chunk, key ctx + j (a staged tree
+// row) is visible iff bit j of the row's ancestor-or-self mask is set (bits
+// beyond the row's own index are zero). Bit arithmetic only, no per-key loop.
+__device__ __forceinline__ uint32_t vis_bits32(int key0, int cache_end, int ctx, bool last,
+                                               const uint32_t (&m)[SD_MASK_WORDS]) {
+  const int nc = cache_end - key0;
+  uint32_t v = nc >= 32 ? 0xffffffffu : (nc <= 0 ? 0u : ((1u << nc) - 1u));
+  if (last) {
+    const int j0 = key0 - ctx;
+    uint32_t win;
+    if (j0 >= 0) {
+      const int w = j0 >> 5, o = j0 & 31;
+      const uint32_t lo = pick_word(m, w), hi = pick_word(m, w + 1);
+      win = o ? (lo >> o) | (hi << (32 - o)) : lo;
+    } else {
+      win = -j0 >= 32 ? 0u : pick_word(m, 0) << (-j0);
+    }
+    v |= win;
+  }
+  return v;
+}
+
 template <int MT, int M>
 __device__ __forceinline__ void issue_loop(uint8_t* smem, int n_tiles, uint32_t p_bar_count, uint64_t* k_full,
                                            uint64_t* k_empty, uint64_t* v_full, uint64_t* v_empty, uint64_t* s_full,
@@ -225,6 +255,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // tree record) and the committed cache rows come from earlier kernels and are
   // read at once; q and the staged tree rows only after pdl_wait.
   pdl_trigger();
+#ifdef SD_TC_TRACE
+  int64_t t_start;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+#endif
   const int T = p.rows_dev ? min(*p.rows_dev, p.T) : p.T;
   const int GT = p.G * T;
   const int rg = blockIdx.z * ROWS;
@@ -234,7 +268,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   // (tc_chunk_len), identical for the host- and device-resident context and for
   // any number of GPUs sharing the kv heads: bitwise cross-P determinism (H7).
   const int ctx = p.ctx_dev ? *p.ctx_dev : p.ctx;
-  const int chunk = chunk_len(ctx, p.n_target);
+#ifndef SD_TC_LAST_RELIEF
+#define SD_TC_LAST_RELIEF 0
+#endif
+  const int chunk = chunk_len(ctx + SD_TC_LAST_RELIEF, p.n_target);
   const int n_live = ctx > 0 ? (ctx + chunk - 1) / chunk : 1;
   if ((int)blockIdx.x >= n_live) {  // empty split: weight 0 in the merge
     for (int r = tid; r < ROWS; r += THREADS) {
@@ -433,20 +470,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int key0 = key_begin + j * BN + 32 * h;
         const bool full = key_begin + j * BN + BN <= cache_end;  // tile-uniform
         if (!full) {
-          uint32_t vis = 0u;
-          if (valid) {
-            for (int c = 0; c < 32; ++c) {
-              const int k = key0 + c;
-              bool on = false;
-              if (k < cache_end) {
-                on = true;
-              } else if (last && k < key_end) {
-                const int jt = k - ctx;
-                on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
-              }
-              vis |= (uint32_t)on << c;
-            }
-          }
+          const uint32_t vis = valid ? vis_bits32(key0, cache_end, ctx, last, tmask) : 0u;
 #pragma unroll
           for (int c = 0; c < 32; ++c)
             if (!((vis >> c) & 1u)) sr[c] = __float_as_uint(-INFINITY);
@@ -602,20 +626,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // keys (rows beyond GT hold zero queries: finite garbage, never written)
         const bool full = key0 + BN <= cache_end;
         if (!full) {
-          uint64_t vis = 0ull;  // built without indexing sr[] (keeps it in registers)
-          if (valid) {
-            for (int c = 0; c < 64; ++c) {
-              const int k = key0 + c;
-              bool on = false;
-              if (k < cache_end) {
-                on = true;
-              } else if (last && k < key_end) {
-                const int jt = k - ctx;
-                on = (tmask[jt >> 5] >> (jt & 31)) & 1u;
-              }
-              vis |= (uint64_t)on << c;
-            }
-          }
+          const uint64_t vis = valid ? ((uint64_t)vis_bits32(key0 + 32, cache_end, ctx, last, tmask) << 32) |
+                                           vis_bits32(key0, cache_end, ctx, last, tmask)
+                                     : 0ull;
 #pragma unroll
           for (int c = 0; c < 64; ++c)
             if (!((vis >> c) & 1ull)) sr[c] = __float_as_uint(-INFINITY);
@@ -744,6 +757,15 @@ __global__ void __launch_bounds__(THREADS, 1)
   tc_fence_before();
   __syncthreads();
   if (tid == 0) trace(0, 60, 6);
+#ifdef SD_TC_TRACE
+  if (tid == 0 && g_tc_trace) {  // per-CTA start / end (globaltimer, ns) after the event block
+    const int c = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    uint64_t now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+    g_tc_trace[4 * 64 * 8 + 64 + 2 * c] = t_start;
+    g_tc_trace[4 * 64 * 8 + 64 + 2 * c + 1] = (int64_t)now;
+  }
+#endif
   if (warp == 2) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");

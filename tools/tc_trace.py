@@ -23,7 +23,7 @@ q = (torch.randn((T, H, dh), device="cuda") * 0.1).to(torch.bfloat16)
 bits = torch.as_tensor(mask_bits_from_bool(np.tril(np.ones((T, T), dtype=bool))), device="cuda")
 out = torch.empty((T, H * dh), dtype=torch.bfloat16, device="cuda")
 ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, H, dh, ctx), dtype=torch.uint8, device="cuda")
-tr = torch.zeros((4, 64, 8), dtype=torch.int64, device="cuda")
+tr = torch.zeros(4 * 64 * 8 + 64 + 2 * 1024, dtype=torch.int64, device="cuda")
 
 
 def run():
@@ -46,7 +46,10 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 print(f"ctx={ctx} T={T}: {e0.elapsed_time(e1) / 10 * 1000:.1f} us per call")
-t = tr.cpu().numpy()
+allt = tr.cpu().numpy()
+t = allt[:4 * 64 * 8].reshape(4, 64, 8)
+cta = allt[4 * 64 * 8 + 64:].reshape(-1, 2)
+cta = cta[cta[:, 1] > 0]
 base = t[t > 0].min()
 print("cta(0,0,0) milestones [entry, q staged, tmem+sync, softmax loop done, o_final, epilogue done, exit]:",
       [int(x - base) if x else None for x in t[0, 60, :7]])
@@ -71,3 +74,22 @@ for j in range(20, 28):
     prev = s0[4]
     print(f"{j:2d} | {s0[1]-s0[0]:6d} {s0[2]-s0[1]:7d} {s0[3]-s0[2]:9d} {s0[4]-s0[3]:8d} | "
           f"{s1[1]-s1[0]:6d} {s1[2]-s1[1]:7d} {s1[3]-s1[2]:9d} {s1[4]-s1[3]:8d} | {m[4]-m[3]:5d} {m[6]-m[4]:5d} | {per}")
+
+print("\nK/V stream (slot q = tiles 2q, 2q+1): issue -> issuer-needs -> landed-seen; lead = need - issue, stall = seen - need")
+for q in range(4, 24):
+    j = 2 * q
+    ki, vi = t[0, q, 1], t[0, q, 2]
+    kw, kok = t[1, j, 0], t[1, j, 1]
+    vw, vok = t[1, j, 3], t[1, j, 4]
+    if ki and kw:
+        print(f"slot {q:2d}: K issue {ki - base:7d} need {kw - base:7d} seen {kok - base:7d} lead {kw - ki:6d} stall {kok - kw:5d}"
+              f" | V issue {vi - base:7d} need {vw - base:7d} (P ok {vok - base:7d}) lead {vw - vi:6d}")
+
+if len(cta):
+    t0 = cta[:, 0].min()
+    st, en = (cta[:, 0] - t0) / 1e3, (cta[:, 1] - t0) / 1e3
+    print(f"\nper-CTA (us from first start, {len(cta)} CTAs): start min {st.min():.1f} med {np.median(st):.1f} max {st.max():.1f}; "
+          f"end min {en.min():.1f} med {np.median(en):.1f} p90 {np.percentile(en, 90):.1f} max {en.max():.1f}; "
+          f"duration med {np.median(en - st):.1f} max {(en - st).max():.1f}")
+    order = np.argsort(-en)[:8]
+    print("latest CTAs (index, start, end):", [(int(i), round(float(st[i]), 1), round(float(en[i]), 1)) for i in order])
