@@ -11,6 +11,8 @@
 // is bitwise independent of how many GPUs share the heads) + 1 tree chunk,
 // y = kv head, z = query-row tile. Each CTA writes an un-normalised partial
 // (o / l, lse) per query row; sd_attention then merges chunks in fixed order.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace sd {
@@ -434,8 +436,17 @@ template <> __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16*
 #endif
 constexpr int MU = SD_MERGE_U;  // split partials in flight per warp
 
-template <typename OT>
-__global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse,
+// four consecutive partial values: fp32 (CUDA-core splits) or fp16 (tcgen05 splits)
+__device__ __forceinline__ float4 load4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 load4(const __half* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename OT, typename PT = float, int MK = 3>
+__global__ void __launch_bounds__(256) merge128_kernel(const PT* __restrict__ ws_o, const float* __restrict__ ws_lse,
                                                        int nsplit, int TH, int H, const int32_t* __restrict__ rows_dev,
                                                        OT* __restrict__ out) {
   const int lane = threadIdx.x & 31;
@@ -448,27 +459,30 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
     store4<OT>(dst, 0.f, 0.f, 0.f, 0.f);
     return;
   }
-  // lse of split c lives in lane c % 32, register c / 32 (nsplit <= 96)
-  float lv[3], wv[3];
+  // lse of split c lives in lane c % 32, register c / 32 (nsplit <= 32 * MK)
+  float lv[MK], wv[MK];
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < MK; ++k) {
     const int c = lane + 32 * k;
     lv[k] = c < nsplit ? ws_lse[(int64_t)c * TH + row] : -INFINITY;
   }
-  const float m = warp_max(fmaxf(lv[0], fmaxf(lv[1], lv[2])));
+  float m = lv[0];
+#pragma unroll
+  for (int k = 1; k < MK; ++k) m = fmaxf(m, lv[k]);
+  m = warp_max(m);
   float lsum = 0.f;
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < MK; ++k) {
     wv[k] = lv[k] == -INFINITY ? 0.f : __expf(lv[k] - m);
     lsum += wv[k];
   }
   lsum = warp_sum(lsum);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const float* base = ws_o + (int64_t)row * 128 + 4 * lane;
+  const PT* base = ws_o + (int64_t)row * 128 + 4 * lane;
   // only splits that hold data (empty ones — past a device-resident context —
   // were never written), in ascending order, MU partial loads in flight
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
+  for (int k = 0; k < MK; ++k) {
     unsigned live = __ballot_sync(0xffffffffu, lv[k] != -INFINITY);
     while (live) {
       int cs[MU];
@@ -487,7 +501,7 @@ __global__ void __launch_bounds__(256) merge128_kernel(const float* __restrict__
       }
       float4 o[MU];
 #pragma unroll
-      for (int u = 0; u < MU; ++u) o[u] = *reinterpret_cast<const float4*>(base + (int64_t)(32 * k + cs[u]) * TH * 128);
+      for (int u = 0; u < MU; ++u) o[u] = load4(base + (int64_t)(32 * k + cs[u]) * TH * 128);
 #pragma unroll
       for (int u = 0; u < MU; ++u) {
         if (u < n) {
@@ -1030,7 +1044,7 @@ int tc_split_target(int kv_heads_total);
 int tc_grid_chunks(int ctx_bound, int n_target);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     float* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st);
+                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st);
 template <int DH, typename OT>
 __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
                                   int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out);
@@ -1119,11 +1133,19 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     // themselves are resolved in the kernel from the live context
     const int n_target = tc_split_target(kv_heads_total > 0 ? kv_heads_total : Hk);
     const int nc = tc_grid_chunks(ctx, n_target);
-    float* ws_lse = p.ws_o + (size_t)nc * T * H * dh;
+    // split partials in fp16 (normalised o / l: |values| <= max |v|; 2^-11
+    // relative, below the bf16 output's own rounding), lse in fp32
+    __half* ws_oh = reinterpret_cast<__half*>(p.ws_o);
+    float* ws_lse = reinterpret_cast<float*>(ws_oh + (size_t)nc * T * H * dh);
     int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, ctx_dev, mask_bits,
-                              mask_words, p.ws_o, ws_lse, nc, n_target, st);
+                              mask_words, ws_oh, ws_lse, nc, n_target, st);
     if (rc) return rc;
-    launch_merge<__nv_bfloat16>(p.ws_o, ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out, 128, st);
+    if (nc > 160) {
+      set_error("sd_attention(tc): %d splits > 160", nc);
+      return SD_EINVAL;
+    }
+    launch_pdl(nc <= 96 ? merge128_kernel<__nv_bfloat16, __half, 3> : merge128_kernel<__nv_bfloat16, __half, 5>, dim3((T * H + 7) / 8), dim3(256), 0, st, (const __half*)ws_oh,
+               (const float*)ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out);
     return check_launch("sd_attention(tc merge)");
   }
   if (T == 1 && src_kind == 1 && dh == 128 && p.G <= 16 && !rows_dev && !ctx_dev && tmap_k_host && tmap_v_host &&

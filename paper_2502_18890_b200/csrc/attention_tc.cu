@@ -30,6 +30,8 @@
 // the tcgen05 memory model), so the write-after-read on TMEM needs no barrier:
 // the issuer never waits for an MMA to retire, and a tile costs it three
 // barrier waits (K landed, V landed, P written) and four commits.
+#include <cuda_fp16.h>
+
 #include "tc_common.cuh"
 
 namespace sd {
@@ -91,7 +93,7 @@ struct Params {
   const int32_t* ctx_dev;  // nullable: live cache length (chunking resolved per launch on device)
   const uint32_t* mask;    // [T][mask_words] tree rows (NULL = causal)
   int mask_words;
-  float* ws_o;
+  __half* ws_o;  // [split][T][H][128] fp16 partial o / l
   float* ws_lse;
 };
 
@@ -132,6 +134,10 @@ __device__ __forceinline__ void trace(int role, int j, int ev) {
 // MMA issue stream of one M-tile (warps 1 / 2; the whole warp runs the loop,
 // one elected lane issues). TMEM base is 0: the CTA owns all 512 columns.
 //   S[MT][j%2] = Q[MT] K(j)^T (8 K=16 steps), O[MT] += P(j) V(j) (4 steps)
+__device__ __forceinline__ uint2 pack_half4(float4 f) {
+  const __half2 a = __floats2half2_rn(f.x, f.y), b = __floats2half2_rn(f.z, f.w);
+  return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+}
 // word w of a row's tree-visibility bits without dynamic register indexing
 __device__ __forceinline__ uint32_t pick_word(const uint32_t (&m)[SD_MASK_WORDS], int w) {
   uint32_t r = 0u;
@@ -568,9 +574,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int rr = 0; rr < 16; ++rr) {
         const int64_t oi_r = __shfl_sync(0xffffffffu, oi, rr);
         const bool v_r = __shfl_sync(0xffffffffu, valid, rr);
-        if (v_r)
-          reinterpret_cast<float4*>(p.ws_o + oi_r * DH)[lane] =
-              *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
+        if (v_r) {
+          const float4 f = *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
+          reinterpret_cast<uint2*>(p.ws_o + oi_r * DH)[lane] = pack_half4(f);
+        }
       }
       if (valid && h == 0) p.ws_lse[oi] = lt > 0.f ? (m_used + __log2f(lt)) / LOG2E : -INFINITY;
     }
@@ -746,9 +753,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int rr = 0; rr < 32; ++rr) {
         const int64_t oi_r = __shfl_sync(0xffffffffu, oi, rr);
         const bool v_r = __shfl_sync(0xffffffffu, valid, rr);
-        if (v_r)
-          reinterpret_cast<float4*>(p.ws_o + oi_r * DH)[lane] =
-              *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
+        if (v_r) {
+          const float4 f = *reinterpret_cast<const float4*>(stage + rr * 512 + ((lane ^ rr) << 4));
+          reinterpret_cast<uint2*>(p.ws_o + oi_r * DH)[lane] = pack_half4(f);
+        }
       }
       if (valid) p.ws_lse[oi] = l > 0.f ? (m_used + __log2f(l)) / LOG2E : -INFINITY;
       if (row == 0 && mt == 0) trace(0, 60, 5);
@@ -838,7 +846,7 @@ int tc_grid_chunks(int ctx_bound, int n_target) {
 
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     float* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st) {
+                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
