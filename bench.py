@@ -75,27 +75,38 @@ def workload_name(cfg_name, c, ctx):
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    nvidia-smi takes ~0.1-0.3 s to start, so the sampler is started before the
+    warm-up (start()) and only the samples whose timestamps fall inside the
+    timed window (mark_begin() / mark_end()) are summarised."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
+        self.t_begin = self.t_end = None
+        self.lines = []
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
         return self
 
-    def __exit__(self, *exc):
-        self.lines = []
+    def mark_begin(self):
+        self.t_begin = time.time()
+
+    def mark_end(self):
+        self.t_end = time.time()
+        time.sleep(0.1)  # let the sampler flush the window's last samples
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -106,20 +117,30 @@ class ClockSampler:
             self.lines = [l for l in out.splitlines() if l.strip()]
 
     def summary(self):
-        sm, mx, reasons = [], 0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in getattr(self, "lines", []):
+        import datetime
+        sm, mx, power, reasons, n_all = [], 0, [], set(), 0
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
-                sm.append(float(f[1]))
-                mx = max(mx, float(f[2]))
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, cmax = float(f[2]), float(f[3])
             except (ValueError, IndexError):
                 continue
-            for i, n in enumerate(names):
-                if len(f) > 5 + i and f[5 + i].lower() == "active":
+            n_all += 1
+            if self.t_begin is not None and not (self.t_begin - 0.01 <= ts <= (self.t_end or ts) + 0.01):
+                continue
+            sm.append(clk)
+            mx = max(mx, cmax)
+            try:
+                power.append(float(f[4]))
+            except ValueError:
+                pass
+            for i, n in enumerate(self.NAMES):
+                if len(f) > 6 + i and f[6 + i].lower() == "active":
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "sm_min_mhz": min(sm) if sm else None, "power_w": statistics.median(power) if power else None,
+                "reasons": sorted(reasons), "samples": len(sm), "samples_total": n_all}
 
 
 def measured_peaks():
@@ -210,6 +231,7 @@ def main():
     if ctx > c["prefix"]:
         sess.set_synthetic_context(ctx)
     torch.cuda.synchronize()
+    clk = ClockSampler(local).start()
     for _ in range(args.warmup):
         sess.step()
     if args.ngram_stress:
@@ -224,16 +246,17 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n0 = len(sess.records)
     l0 = _lib.launch_count
-    with ClockSampler(local) as clk:
-        torch.cuda.nvtx.range_push("timed")
-        w0 = time.perf_counter()
-        e0.record(st)
-        for _ in range(args.steps):
-            sess.step()  # public API: includes the per-step D2H of the step result
-        e1.record(st)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - w0
-        torch.cuda.nvtx.range_pop()
+    clk.mark_begin()
+    torch.cuda.nvtx.range_push("timed")
+    w0 = time.perf_counter()
+    e0.record(st)
+    for _ in range(args.steps):
+        sess.step()  # public API: includes the per-step D2H of the step result
+    e1.record(st)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    torch.cuda.nvtx.range_pop()
+    clk.mark_end()
     if world > 1:
         dist.barrier()
     launches = _lib.launch_count - l0
