@@ -12,9 +12,10 @@ the default point, the run's mean context (4096 + 100000/2), gives the
 run-average tokens/s. The prefix is prefilled for real; the committed
 context beyond it is synthetic (random K/V, `data: synthetic`).
 
-Rank 0 prints one JSON line. --impl reference times the reference algorithm's
-CPU path (the oracle port; swiftdec is pure numpy, nothing to compile) on the
-host cores on a bounded sample of the same workload.
+Rank 0 prints one JSON line. --impl reference times the unmodified reference
+(swiftdec, pure numpy, pip-installed into baseline/_ref; baseline/ref_arm.py)
+on the host cores: cfg1 end to end, cfgs 2-5 as a bounded sample composed from
+its own functions at full shape.
 """
 
 from __future__ import annotations
@@ -160,7 +161,21 @@ def ncu_traffic():
     return json.load(open(p)).get("traffic_bytes_per_launch")
 
 
-def cpu_baseline_line(c, ctx, accepted, tree_rows):
+def cpu_baseline_line(c, ctx, accepted, tree_rows, samples=2):
+    """The unmodified reference's CPU path on the host cores, composed from its
+    own functions at full shape (baseline/ref_arm.py; kind "reference"); the
+    oracle port (kind "port") when the reference cannot be imported."""
+    from baseline import ref_arm
+    if ref_arm.import_reference()[0] is not None:
+        comp = ref_arm.Composer(c, ctx, rows=tree_rows)
+        per = [comp.sample(accepted)[0] for _ in range(samples + 1)][1:]  # first sample warms
+        it = statistics.median(per)
+        return {"value": accepted / it, "unit": "tokens/s", "cores": ref_arm.host_cores(), "kind": "reference",
+                "composed": True,
+                "sample": (f"reference swiftdec functions at full shape, composed per iteration ({c['L']} x verify "
+                           f"layer over ctx {ctx} with {tree_rows} rows + draft + cache maintenance + sampling + "
+                           f"top-w + n-gram/tree + amortised refresh); {accepted:.2f} tokens/iteration; "
+                           f"{it:.1f} s/iteration; median of {samples} samples")}
     from oracle.cpu_baseline import compose_step, host_cores
     per_step, tps, parts = compose_step(c["d"], c["L"], c["H"], c["Hk"], c["V"], ctx, c["B"], tree_rows=tree_rows,
                                         accepted=accepted)

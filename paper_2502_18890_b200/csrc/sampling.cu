@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(SMP_THREADS) sample_rows_kernel(const void* __
 //      32-key warp chunks for the first cumsum > u (sampling.py:219-224).
 constexpr int SC_CTAS = 8, SC_THREADS = 512;
 
-__global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS)
+__global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 3)
     sample_rows_cluster_kernel(const float* __restrict__ logits, SampleDev a) {
   extern __shared__ float ecache[];  // e = exp(s - max) of this CTA's slice
   __shared__ RowCtx rc;
