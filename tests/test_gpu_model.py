@@ -263,3 +263,29 @@ def test_graph_replay_equals_eager(dtype):
     assert torch.equal(a.q_sum, b.q_sum)
     n = len(a.full)
     assert torch.equal(a.full.k_rot[:, :, :n], b.full.k_rot[:, :, :n])
+
+
+def test_cli_generate_trace_report_roundtrip(tmp_path, capsys):
+    """`generate` on the device engine writes the reference's trace / metrics
+    formats; `report` reads them back (reference cli.py:192-345)."""
+    import json as _json
+
+    from paper_2502_18890_b200 import cli
+    from paper_2502_18890_b200 import metrics as M
+    cfgf = tmp_path / "m.cfg"
+    cfgf.write_text("vocab_size = 512\nnum_layers = 2\nhidden_dim = 64\nnum_heads = 4\nnum_kv_heads = 2\n"
+                    "max_positions = 4096\n")
+    out, trace, met = tmp_path / "o.txt", tmp_path / "t.jsonl", tmp_path / "m.json"
+    rc = cli.main(["generate", "--model", str(cfgf), "--random-prompt", "48", "--target", "40", "--budget", "32",
+                   "--sink", "4", "--min-p", "0.5", "--dtype", "fp32", "--out", str(out), "--trace", str(trace),
+                   "--metrics", str(met)])
+    assert rc == 0
+    toks = [int(t) for t in out.read_text().split()]
+    recs = M.read_trace(trace)
+    assert len(toks) >= 40 and [t for r in recs for t in r.tokens] == toks
+    m = _json.loads(met.read_text())
+    assert m["emitted"] == len(toks) and m["iterations"] == len(recs)
+    capsys.readouterr()
+    assert cli.main(["report", "--trace", str(trace), "--prefix-len", "48"]) == 0
+    rep = _json.loads(capsys.readouterr().out)
+    assert rep["alpha"] == m["alpha"] and rep["emitted"] == len(toks)

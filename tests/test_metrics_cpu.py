@@ -61,3 +61,41 @@ def test_cost_model():
         M.CostParams(bandwidth=0)
     # B200 preset: the SURVEY §8d step bound at cfg3 ctx 54K (~4.96 ms)
     assert 4.8e-3 < M.step_bound_seconds(M.B200, 54096, 4096) < 5.1e-3
+
+
+def test_cli_report_matches_metrics(tmp_path, capsys):
+    """`report` (cli.py:324-345 of the reference): the reference's payload from a
+    trace, the (Gen. Len., alpha, x) CSV row, exit code 2 on a missing trace."""
+    import json as _json
+
+    from paper_2502_18890_b200 import cli
+    r = _recs()
+    p = tmp_path / "t.jsonl"
+    M.write_trace(r, p)
+    csvp = tmp_path / "r.csv"
+    assert cli.main(["report", "--trace", str(p), "--prefix-len", "64", "--csv", str(csvp)]) == 0
+    out = _json.loads(capsys.readouterr().out)
+    want = M.collect_metrics(r, 3, [t for x in r for t in x.tokens]).to_dict()
+    for k, v in want.items():
+        assert out[k] == v
+    assert math.isclose(out["simulated_speedup"], M.simulated_speedup(M.CostParams(), r, 64))
+    lines = csvp.read_text().splitlines()
+    assert lines[0] == "Gen. Len.,alpha,x" and lines[1].startswith("7,0.5833,")
+    assert cli.main(["report", "--trace", str(p), "--b200"]) == 0
+    assert math.isclose(_json.loads(capsys.readouterr().out)["simulated_speedup"],
+                        M.simulated_speedup(M.B200, r, 64))
+    assert cli.main(["report", "--trace", str(tmp_path / "missing.jsonl")]) == 2
+
+
+def test_cli_model_config_parsing(tmp_path):
+    from paper_2502_18890_b200 import cli
+    from paper_2502_18890_b200.engine import ConfigError
+    f = tmp_path / "m.cfg"
+    f.write_text("# tiny\nvocab_size = 512\nnum_layers = 2\nhidden_dim = 256\nnum_heads = 8\nnum_kv_heads = 2\n")
+    assert cli.read_model_config(str(f))["num_kv_heads"] == "2"
+    f.write_text("vocab_size = 512\nbogus = 1\n")
+    with pytest.raises(ConfigError):
+        cli.read_model_config(str(f))
+    f.write_text("backend = table\n")
+    with pytest.raises(ConfigError):
+        cli.read_model_config(str(f))
