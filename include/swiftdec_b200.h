@@ -176,6 +176,12 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
  * (model.py:278, 306-311): h[N] += x[K] . W[K][N]; x_out = h * gain / rms(h)
  * (x_dtype SD_BF16 / SD_F32). The last column block to finish normalises the
  * row, so the pair is one launch; same workspace as sd_gemv. */
+/* one row, the norm folded into the projection's input (model.py:306-311):
+ * h_out = h_in + delta; x = bf16(rmsnorm(h_out) * gain) computed in the kernel;
+ * y = x . W with the sd_gemv epilogues. h_out must not alias h_in. */
+int sd_gemv_norm(const float* h_in, const float* delta, const float* gain, float eps, float* h_out, int K,
+                 const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
+                 sd_stream_t stream);
 int sd_gemv_addnorm(const void* x, int K, const void* w, int N, float* h, const float* gain, float eps, void* x_out,
                     int x_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
 

@@ -64,6 +64,7 @@ _SIGS = {
     "sd_gemv_workspace_bytes": (SZ, [INT, INT]),
     "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_gemv_addnorm": (INT, [P, INT, P, INT, P, P, F32, P, INT, P, SZ, P]),
+    "sd_gemv_norm": (INT, [P, P, P, F32, P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_tile_weight": (INT, [P, INT, INT, P, P]),
     "sd_make_weight_tmap": (INT, [P, INT, INT, P]),
     "sd_gemm_splits": (INT, [INT, INT, INT, INT]),

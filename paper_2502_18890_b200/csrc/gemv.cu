@@ -184,11 +184,25 @@ struct AddNorm {
   int x_bf16;         // 1: bf16 x, 0: fp32 x
 };
 
+// The input row computed in the kernel from the residual stream instead of
+// read as x (model.py:306-311 for one row: h <- h + delta; x = rmsnorm(h) *
+// gain, rounded to bf16): every CTA sums the squares of the whole row in one
+// fixed order (identical on all CTAs), then scales its K slice; the CTAs of
+// column block 0 write the updated stream to h_out (not h_in: other CTAs are
+// still reading it).
+struct XNorm {
+  const float* h_in;   // [K] (NULL: plain bf16 x)
+  const float* delta;  // [K]
+  const float* gain;   // [K]
+  float eps;
+  float* h_out;        // [K]
+};
+
 template <bool ADDNORM>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     gemv_tma_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ x, int K, int N,
                     int splits, int epi, void* __restrict__ y, float* __restrict__ part, int* __restrict__ counters,
-                    AddNorm an) {
+                    AddNorm an, XNorm xn) {
   extern __shared__ __align__(1024) uint8_t gsm[];
   uint8_t* ring = gsm;                                    // NS stages
   float* xs = reinterpret_cast<float*>(gsm + NS * STAGE_BYTES);  // K slice of x
@@ -219,8 +233,44 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     }
     return;
   }
-  pdl_wait();  // x is the previous kernel's output
-  for (int kk = k0 + tid; kk < k1; kk += WARPS * 32) xs[kk - k0] = __bfloat162float(x[kk]);
+  pdl_wait();  // x (or h, delta) is the previous kernels' output
+  if (xn.h_in) {
+    // 16-byte loads, XN_U of each operand in flight per thread per round (K % 4 == 0)
+    constexpr int XN_U = 4;
+    float ss = 0.f;
+    for (int k4 = tid; k4 < K / 4; k4 += WARPS * 32 * XN_U) {
+      float4 hv[XN_U], dv[XN_U];
+#pragma unroll
+      for (int u = 0; u < XN_U; ++u) {
+        const int i = k4 + u * WARPS * 32;
+        hv[u] = i < K / 4 ? __ldcg(reinterpret_cast<const float4*>(xn.h_in) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        dv[u] = i < K / 4 ? __ldcg(reinterpret_cast<const float4*>(xn.delta) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < XN_U; ++u) {
+        const float a = hv[u].x + dv[u].x, b = hv[u].y + dv[u].y, c = hv[u].z + dv[u].z, d = hv[u].w + dv[u].w;
+        ss = fmaf(a, a, ss);
+        ss = fmaf(b, b, ss);
+        ss = fmaf(c, c, ss);
+        ss = fmaf(d, d, ss);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) red[0][warp] = ss;
+    asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < WARPS; ++w) tot += red[0][w];  // fixed order: the same inv on every CTA
+    const float inv = rsqrtf(tot / (float)K + xn.eps);
+    for (int kk = k0 + tid; kk < k1; kk += WARPS * 32) {
+      const float v = xn.h_in[kk] + xn.delta[kk];
+      xs[kk - k0] = __bfloat162float(__float2bfloat16_rn(v * (xn.gain[kk] * inv)));
+      if (cb == 0) xn.h_out[kk] = v;
+    }
+  } else {
+    for (int kk = k0 + tid; kk < k1; kk += WARPS * 32) xs[kk - k0] = __bfloat162float(x[kk]);
+  }
   asm volatile("bar.sync 1, %0;" ::"n"(WARPS * 32) : "memory");
   float acc[8];
 #pragma unroll
@@ -375,7 +425,7 @@ static int weight_map(const void* w, int K, int N, CUtensorMap* out) {
 
 // one launch of the TMA kernel; false when its shared memory would not fit
 static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace,
-                       const AddNorm& an, cudaStream_t st, int* rc) {
+                       const AddNorm& an, cudaStream_t st, int* rc, const XNorm& xn = XNorm{}) {
   const int blocks = (N + COLS - 1) / COLS;
   const int s = tma_splits(K, N);
   const size_t smem = (size_t)NS * STAGE_BYTES + ((K + s - 1) / s + 1) * sizeof(float);
@@ -395,7 +445,7 @@ static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void
     at = smem;
   }
   launch_pdl(kern, dim3(blocks, s), dim3((WARPS + 1) * 32), smem, st, m, (const __nv_bfloat16*)x, K, N,
-             s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an);
+             s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an, xn);
   *rc = check_launch("sd_gemv");
   return true;
 }
@@ -449,6 +499,23 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
   int rc = 0;
   if (gv::launch_tma(x, K, w, N, epi, y, workspace, gv::AddNorm{}, as_stream(stream), &rc)) return rc;
   return gv::launch_ld(x, K, w, N, epi, y, workspace, as_stream(stream));
+}
+
+int sd_gemv_norm(const float* h_in, const float* delta, const float* gain, float eps, float* h_out, int K,
+                 const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes, sd_stream_t stream) {
+  SD_REQUIRE(h_in && delta && gain && h_out && h_out != h_in && w && y && K > 0 && K % 4 == 0 && N > 0 && N % 8 == 0,
+             "sd_gemv_norm: K=%d N=%d", K, N);
+  SD_REQUIRE(((uintptr_t)h_in % 16) == 0 && ((uintptr_t)delta % 16) == 0, "sd_gemv_norm: h / delta alignment");
+  SD_REQUIRE(((uintptr_t)w % 16) == 0, "sd_gemv_norm: W must be 16-byte aligned");
+  SD_REQUIRE(epi == SD_GEMM_EPI_F32 || epi == SD_GEMM_EPI_SILU_BF16, "sd_gemv_norm: epilogue");
+  const int blocks = (N + gv::COLS - 1) / gv::COLS;
+  SD_REQUIRE((size_t)blocks < (size_t)gv::WS_HEAD_INTS, "sd_gemv_norm: N=%d too wide for the counter head", N);
+  SD_REQUIRE(workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N), "sd_gemv_norm: workspace");
+  const gv::XNorm xn{h_in, delta, gain, eps, h_out};
+  int rc = 0;
+  if (gv::launch_tma(nullptr, K, w, N, epi, y, workspace, gv::AddNorm{}, as_stream(stream), &rc, xn)) return rc;
+  set_error("sd_gemv_norm: the TMA weight stream does not fit this shape");
+  return SD_EUNSUPPORTED;
 }
 
 int sd_gemv_addnorm(const void* x, int K, const void* w, int N, float* h, const float* gain, float eps, void* x_out,

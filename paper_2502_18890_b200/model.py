@@ -458,9 +458,52 @@ class TinyTransformer:
         return out
 
     # -------------------------------------------------------- layer stack --
+    # single-row (draft) forward with each residual add + RMSNorm folded into the
+    # next projection's input load (sd_gemv_norm): 2 norm launches per layer fewer
+    fuse_row_norms = os.environ.get("SD_FUSE_ROW_NORMS", "1") != "0"  # A/B switch (tools only)
+
+    def _row_fused_ok(self) -> bool:
+        return (self.fuse_row_norms and self.use_gemv and self._gemv_ws is not None and self.dtype == torch.bfloat16
+                and self.config.hidden_dim % 8 == 0)
+
+    def gemv_norm(self, h_in, delta, gain, h_out, w, silu: bool = False) -> torch.Tensor:
+        """h_out = h_in + delta; y = bf16(rmsnorm(h_out) * gain) @ w in one launch."""
+        K, N = w.shape
+        y = torch.empty((1, N), dtype=self.dtype if silu else torch.float32, device=self.device)
+        L.call("sd_gemv_norm", L.ptr(h_in), L.ptr(delta), L.ptr(gain), 1e-6, L.ptr(h_out), K, L.ptr(w), N,
+               L.GEMM_EPI_SILU_BF16 if silu else L.GEMM_EPI_F32, L.ptr(y), L.ptr(self._gemv_ws),
+               self._gemv_ws.numel(), L.stream())
+        return y
+
+    def _run_layers_row(self, tokens_dev, attend, q_pre=None):
+        """run_layers for one row (the draft forward) with the norms fused into
+        the weight streams; the residual stream ping-pongs between two rows."""
+        h = self.embed_rows(tokens_dev, 1)
+        other = torch.empty_like(h)
+        x = self.norm(h, None, self.layers[0]["ln1"])
+        pending = None  # (h, delta, gain) of the norm that feeds the next projection
+        nl = len(self.layers)
+        for l, ly in enumerate(self.layers):
+            if pending is None:
+                qkv = self.gemv(x, ly["wqkv"])
+            else:
+                qkv = self.gemv_norm(pending[0], pending[1], pending[2], other, ly["wqkv"])
+                h, other = other, h
+            o = self._gather_heads(attend(l, qkv, None if q_pre is None else q_pre[l]))
+            d1 = self.gemv(o, ly["wo"])
+            a = self.gemv_norm(h, d1, ly["ln2"], other, ly["w1"], silu=True)
+            h, other = other, h
+            d2 = self.gemv(a, ly["w2"])
+            if l + 1 < nl:
+                pending = (h, d2, self.layers[l + 1]["ln1"])
+            else:
+                return self.norm(h, d2, self.ln_f, out_dtype=torch.float32)  # h0 (fp32)
+
     def run_layers(self, tokens_dev, T, attend, q_pre=None):
         """Embedding + L layers + final norm. attend(l, qkv, q_pre_l) -> [T, H_local*dh].
         Returns h0 = rmsnorm(h, ln_f) in fp32 [T, d]."""
+        if T == 1 and self._row_fused_ok():
+            return self._run_layers_row(tokens_dev, attend, q_pre)
         h = self.embed_rows(tokens_dev, T)
         x = self.norm(h, None, self.layers[0]["ln1"])
         nl = len(self.layers)

@@ -289,3 +289,45 @@ def test_cli_generate_trace_report_roundtrip(tmp_path, capsys):
     assert cli.main(["report", "--trace", str(trace), "--prefix-len", "48"]) == 0
     rep = _json.loads(capsys.readouterr().out)
     assert rep["alpha"] == m["alpha"] and rep["emitted"] == len(toks)
+
+
+_CFG1 = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "cfg1_run.json")
+
+
+@pytest.mark.skipif(not os.path.exists(_CFG1), reason="tests/golden/cfg1_run.json not generated")
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+def test_cfg1_full_run_vs_reference(dtype):
+    """BASELINE cfg1 end to end against the reference's own 2000-token run
+    (tests/golden/make_golden_cfg1.py; SURVEY §8(c) layering (3)): fp32 —
+    identical tokens and every IterationRecord; bf16 — the greedy tokens equal
+    the oracle's wherever its top-1 margin exceeds 2e-2 (teacher forced on the
+    device's own prefix, oracle/checks.py)."""
+    import json as _json
+
+    from oracle import checks as OC
+    from oracle import model as OM
+    from oracle import sampling as OS
+    from paper_2502_18890_b200 import (EngineConfig, ModelConfig, SamplerConfig, TinyTransformer, TreeConfig,
+                                       Truncation, prefill)
+    from paper_2502_18890_b200.rng import random_prompt
+    g = _json.load(open(_CFG1))
+    mcfg = g["model"]
+    prompt = random_prompt(g["prompt_len"], mcfg["vocab_size"])
+    m = TinyTransformer(ModelConfig(**mcfg), dtype=dtype)
+    cfg = EngineConfig(target_length=g["engine"]["target_length"], sink_size=g["engine"]["sink_size"],
+                       budget=g["engine"]["budget"], tree=TreeConfig((1, 3, 3, 3)), k=g["engine"]["k"],
+                       sampler=SamplerConfig(theta=1.2, window=1024, truncation=Truncation.min_p(1.0)))
+    s = prefill(m, prompt, cfg)
+    while not s.done:
+        s.step()
+    assert s.device_error() == 0
+    if dtype == torch.float32:
+        assert s.emitted == g["emitted"]
+        got = [_json.loads(r.to_json()) for r in s.records]
+        assert got == g["records"]
+        assert g["lossless"] and g["ar"] == g["emitted"][:len(g["ar"])]
+    else:
+        om = OM.TinyTransformer(OM.ModelConfig(**mcfg), params=m.parameters_host())
+        osmp = OS.SamplerConfig(theta=1.2, window=1024, truncation=OS.Truncation.min_p(1.0))
+        bad, undecided = OC.greedy_mismatches(om, prompt, s.emitted, osmp, 2e-2)
+        assert not bad, bad[:4]
