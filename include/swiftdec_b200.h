@@ -269,6 +269,7 @@ int sd_reconcile(int L, const int32_t* result, int base_len, void* k_raw, void* 
 #define SD_IN_LOGITS_F32 0
 #define SD_IN_LOGITS_F64 1
 #define SD_IN_PROBS_F64 2
+#define SD_IN_SCALED_F32 3 /* penalised scaled fp32 logits + per-tile statistics from sd_lmhead_sample_stats */
 
 typedef struct {
   int rows, V, in_kind;
@@ -290,8 +291,31 @@ typedef struct {
   double* probs_out;               /* nullable [rows][V]: penalised softmax */
   double* trunc_out;               /* nullable [rows][V]: truncated + renormalised */
   int32_t* token_out;              /* nullable [rows]: inverse-CDF draw */
+  const double* stats;             /* SD_IN_SCALED_F32 only: [rows][stats_tiles][2] (max, sum exp(s - max)) per
+                                      128-token tile of the penalised, scaled logits (sd_lmhead_sample_stats) */
+  int stats_tiles;
 } sd_sample_args;
 int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t stream);
+
+/* Verification LM head fused with the sampler's first pass (
+ * replaces `logits = h0 @ embed.T` + the penalty/softmax-statistics half of
+ * penalized_probs_masked, engine.py:237-245 / sampling.py:98-153, which the
+ * reference computes over [T, V] in numpy). x: bf16 h0 [M][K] (M <= 128),
+ * embed_tmap: sd_make_lmhead_tmap of the tied bf16 embedding [V][K] re-laid by
+ * sd_tile_lmhead into contiguous 16 KB (128-token x 64-wide) boxes
+ * (sd_lmhead_tiled_bytes). The
+ * penalty fields of `args` (temperature, theta, ctrl_style, member_kind NONE /
+ * WINDOW / TREE with its window and tree record) are applied in the epilogue;
+ * writes logits [M][V] = penalised logits / temperature (fp32) and stats
+ * [M][sd_lmhead_tiles(V)][2] = (max, sum exp(s - max)) per 128-token tile, for
+ * the tree's live rows only. Follow with sd_sample_rows(in_kind =
+ * SD_IN_SCALED_F32, stats, stats_tiles). tcgen05 + TMA, sm_100a. */
+size_t sd_lmhead_tiled_bytes(int V, int K);
+int sd_tile_lmhead(const void* embed, int V, int K, void* tiled, sd_stream_t stream);
+int sd_make_lmhead_tmap(const void* tiled, int V, int K, void* tmap_out_host /* 128 bytes */);
+int sd_lmhead_tiles(int V);
+int sd_lmhead_sample_stats(const void* x, int M, int K, const void* embed_tmap_host, int V,
+                           const sd_sample_args* args_host, float* logits, double* stats, sd_stream_t stream);
 
 /* per-head top-w of the penalised draft distributions, ties to lower id
  * (engine.py:207-215). out: concatenated candidates, head k gets widths[k]. */

@@ -18,7 +18,7 @@ SD_F32, SD_BF16, SD_F64 = 0, 1, 2
 TREE_MAX_ROWS, TREE_MAX_PATHS, TREE_MAX_DEPTH, MASK_WORDS = 256, 512, 8, 8
 MEMBER_NONE, MEMBER_MASK, MEMBER_WINDOW, MEMBER_TREE = 0, 1, 2, 3
 TRUNC_NONE, TRUNC_TOP_P, TRUNC_MIN_P, TRUNC_ETA = 0, 1, 2, 3
-IN_LOGITS_F32, IN_LOGITS_F64, IN_PROBS_F64 = 0, 1, 2
+IN_LOGITS_F32, IN_LOGITS_F64, IN_PROBS_F64, IN_SCALED_F32 = 0, 1, 2, 3
 GEMM_EPI_F32, GEMM_EPI_SILU_BF16 = 0, 1
 ST_RING_HEAD, ST_RING_LEN, ST_HIST_LEN, ST_PENDING, ST_ERROR, ST_BASE = 0, 1, 2, 3, 4, 5
 RES_ACCEPTED, RES_BEST, RES_PICK, RES_ORIGIN, RES_ROWS, RES_PATHS, RES_PENDING, RES_BASE = 0, 1, 2, 3, 4, 5, 6, 7
@@ -45,6 +45,7 @@ class SampleArgs(C.Structure):
         ("trunc_value", F64), ("eta_alpha", F64), ("seed", U64),
         ("positions", P), ("n", I64),
         ("probs_out", P), ("trunc_out", P), ("token_out", P),
+        ("stats", P), ("stats_tiles", INT),
     ]
 
 
@@ -82,6 +83,11 @@ _SIGS = {
                               INT, P, P, P, P, P, P, P]),
     "sd_reconcile": (INT, [INT, P, INT, P, P, P, INT, I64, I64, INT, INT, P, INT, INT, P, P]),
     "sd_sample_rows": (INT, [P, C.POINTER(SampleArgs), P]),
+    "sd_lmhead_tiled_bytes": (SZ, [INT, INT]),
+    "sd_tile_lmhead": (INT, [P, INT, INT, P, P]),
+    "sd_make_lmhead_tmap": (INT, [P, INT, INT, P]),
+    "sd_lmhead_tiles": (INT, [INT]),
+    "sd_lmhead_sample_stats": (INT, [P, INT, INT, P, INT, C.POINTER(SampleArgs), P, P, P]),
     "sd_draft_topw": (INT, [P, INT, INT, P, F64, F64, INT, P, P, P]),
     "sd_ngram_bytes": (SZ, [INT, INT, INT]),
     "sd_ngram_init": (INT, [P, INT, INT, INT, P]),
@@ -131,7 +137,8 @@ def require_cuda():
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
 _NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_refresh_workspace_bytes",
               "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_make_slot_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
-              "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes"}
+              "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes", "sd_make_lmhead_tmap",
+              "sd_lmhead_tiles", "sd_lmhead_tiled_bytes"}
 launch_count = 0
 
 

@@ -12,152 +12,13 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "sample_common.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace sd {
 
 constexpr int SMP_THREADS = 1024;
-constexpr int MAX_PATCH = 2 * SD_TREE_MAX_DEPTH;
-
-struct SampleDev {
-  int rows, V, in_kind;
-  double temperature, theta;
-  int ctrl_style, member_kind;
-  const uint8_t* member_mask;
-  const int32_t* win_count;
-  const int32_t* win_ring;
-  const int64_t* state;
-  int window;
-  const int32_t* tree;
-  int depth;
-  int trunc_kind;
-  double trunc_value, eta_alpha;
-  uint64_t seed;
-  const int32_t* positions;
-  int64_t n;
-  double* probs_out;
-  double* trunc_out;
-  int32_t* token_out;
-};
-
-struct RowCtx {
-  int n_patch;
-  int patch_tok[MAX_PATCH];
-  int patch_val[MAX_PATCH];
-  uint32_t bloom[32];  // bit (v & 1023) set for every patched token v
-  int64_t pos;
-};
-
-__device__ __forceinline__ bool is_member(const SampleDev& a, const RowCtx& rc, int row, int v) {
-  switch (a.member_kind) {
-    case SD_MEMBER_MASK: return a.member_mask[(int64_t)row * a.V + v] != 0;
-    case SD_MEMBER_WINDOW: return a.window > 0 && a.win_count[v] > 0;
-    case SD_MEMBER_TREE: {
-      if (a.window <= 0) return false;
-      bool m = a.win_count[v] > 0;
-      if ((rc.bloom[(v >> 5) & 31] >> (v & 31)) & 1u)  // rare: v may be a patched token
-        for (int i = 0; i < rc.n_patch; ++i)
-          if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
-      return m;
-    }
-    default: return false;
-  }
-}
-
-// is_member split in two: the per-element word (loaded in batches, so a thread
-// keeps several global loads in flight) and the decision from it
-__device__ __forceinline__ int member_word(const SampleDev& a, int row, int v) {
-  switch (a.member_kind) {
-    case SD_MEMBER_MASK: return a.member_mask[(int64_t)row * a.V + v];
-    case SD_MEMBER_WINDOW:
-    case SD_MEMBER_TREE: return a.window > 0 ? a.win_count[v] : 0;
-    default: return 0;
-  }
-}
-__device__ __forceinline__ bool member_from(const SampleDev& a, const RowCtx& rc, int v, int word) {
-  switch (a.member_kind) {
-    case SD_MEMBER_MASK: return word != 0;
-    case SD_MEMBER_WINDOW: return a.window > 0 && word > 0;
-    case SD_MEMBER_TREE: {
-      if (a.window <= 0) return false;
-      bool m = word > 0;
-      if ((rc.bloom[(v >> 5) & 31] >> (v & 31)) & 1u)
-        for (int i = 0; i < rc.n_patch; ++i)
-          if (rc.patch_tok[i] == v) m = rc.patch_val[i] != 0;
-      return m;
-    }
-    default: return false;
-  }
-}
-
-template <int IN>
-__device__ __forceinline__ double load_in(const void* in, int64_t idx) {
-  if (IN == SD_IN_LOGITS_F32) return (double)((const float*)in)[idx];
-  return ((const double*)in)[idx];
-}
-
-// scaled logit l / (t * I) (sampling.py:142-153)
-__device__ __forceinline__ double scaled(double l, bool member, const SampleDev& a) {
-  if (!member) return l / a.temperature;
-  if (a.ctrl_style) return (l < 0.0 ? l * a.theta : l / a.theta) / a.temperature;
-  return l / (a.temperature * a.theta);
-}
-
-// thread 0: per-row patches (engine.py:155-181) and draw position
-__device__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
-  rc.n_patch = 0;
-  for (int i = 0; i < 32; ++i) rc.bloom[i] = 0u;
-  if (a.positions) {
-    rc.pos = a.positions[row];
-  } else {
-    const int64_t n = a.n >= 0 ? a.n : a.state[SD_ST_BASE] + 1;  // n < 0: device-resident step
-    rc.pos = row == 0 ? n : n + a.tree[tree_off::NDEPTH + row - 1] + 1;
-  }
-  if (a.member_kind != SD_MEMBER_TREE || a.window <= 0 || row == 0) return;
-  const int W = a.window;
-  const int node = row - 1;
-  int branch[SD_TREE_MAX_DEPTH];
-  int b = 0;
-  for (int x = node; x >= 0 && b < SD_TREE_MAX_DEPTH; x = a.tree[tree_off::PARENT + x])
-    branch[b++] = a.tree[tree_off::TOK + 1 + x];  // deepest first
-  const int64_t ring = a.state[SD_ST_RING_LEN], head = a.state[SD_ST_RING_HEAD];
-  int64_t cap = a.depth < ring ? a.depth : ring;
-  int64_t drop = ring + b - W;
-  if (drop < 0) drop = 0;
-  if (drop > cap) drop = cap;
-  // tokens slid out of the window (oldest first), with their removal counts
-  for (int64_t j = 0; j < drop; ++j) {
-    const int tok = a.win_ring[(head + j) % W];
-    int found = -1;
-    for (int i = 0; i < rc.n_patch; ++i)
-      if (rc.patch_tok[i] == tok) found = i;
-    if (found < 0) {
-      found = rc.n_patch++;
-      rc.patch_tok[found] = tok;
-      rc.patch_val[found] = 0;  // used as removal counter for now
-    }
-    rc.patch_val[found] += 1;
-  }
-  for (int i = 0; i < rc.n_patch; ++i) rc.patch_val[i] = (a.win_count[rc.patch_tok[i]] - rc.patch_val[i]) > 0;
-  const int tail = b < W ? b : W;  // last min(b, W) branch tokens = the deepest `tail`
-  for (int j = 0; j < tail; ++j) {
-    const int tok = branch[j];
-    int found = -1;
-    for (int i = 0; i < rc.n_patch; ++i)
-      if (rc.patch_tok[i] == tok) found = i;
-    if (found < 0) {
-      found = rc.n_patch++;
-      rc.patch_tok[found] = tok;
-    }
-    rc.patch_val[found] = 1;
-  }
-  for (int i = 0; i < rc.n_patch; ++i) {
-    const int v = rc.patch_tok[i];
-    rc.bloom[(v >> 5) & 31] |= 1u << (v & 31);
-  }
-}
-
 struct DI {
   double v;
   int i;
@@ -508,47 +369,65 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 3)
     if (a.ctrl_style) return (l < 0.f ? l * th : l / th) * inv_t;
     return l * inv_tt;
   };
-  float lm = -INFINITY;
-  double lz = 0.0;
-  constexpr int UB = 4;  // elements per thread per batch: all their loads issued first
-  for (int vb = v0 + tid; vb < v1; vb += SC_THREADS * UB) {
-    float lv[UB];
-    int wv[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int v = vb + u * SC_THREADS;
-      lv[u] = v < v1 ? lg[v] : 0.f;
-      wv[u] = v < v1 ? member_word(a, row, v) : 0;
+  float mf = -INFINITY;
+  double Z = 0.0;
+  if (a.in_kind == SD_IN_SCALED_F32) {
+    // the LM-head epilogue (sd_lmhead_sample_stats) already penalised and scaled
+    // the logits and left (max, sum-exp) per 128-token tile: this CTA only loads
+    // its slice, and every CTA of the cluster combines the row's tile statistics
+    // in the same fixed order (identical mf and Z on all eight)
+    for (int v = v0 + tid; v < v1; v += SC_THREADS) ecache[v - v0] = lg[v];
+    const double2* st = reinterpret_cast<const double2*>(a.stats) + (int64_t)row * a.stats_tiles;
+    double tm = -INFINITY;
+    for (int t = tid; t < a.stats_tiles; t += SC_THREADS) tm = fmax(tm, st[t].x);
+    mf = (float)block_reduce(tm, dred, [](double x, double y) { return fmax(x, y); });
+    double tz = 0.0;
+    for (int t = tid; t < a.stats_tiles; t += SC_THREADS) {
+      const double2 e = st[t];
+      if (e.x != -INFINITY) tz += e.y * exp(e.x - (double)mf);
     }
+    Z = block_reduce(tz, dred, [](double x, double y) { return x + y; });
+  } else {
+    float lm = -INFINITY;
+    double lz = 0.0;
+    constexpr int UB = 4;  // elements per thread per batch: all their loads issued first
+    for (int vb = v0 + tid; vb < v1; vb += SC_THREADS * UB) {
+      float lv[UB];
+      int wv[UB];
 #pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int v = vb + u * SC_THREADS;
-      if (v < v1) {
-        const float sv = scaled_w(lv[u], v, wv[u]);
-        ecache[v - v0] = sv;
-        if (sv > lm) {
-          lz = lz * (double)expf(lm - sv);
-          lm = sv;
+      for (int u = 0; u < UB; ++u) {
+        const int v = vb + u * SC_THREADS;
+        lv[u] = v < v1 ? lg[v] : 0.f;
+        wv[u] = v < v1 ? member_word(a, row, v) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int v = vb + u * SC_THREADS;
+        if (v < v1) {
+          const float sv = scaled_w(lv[u], v, wv[u]);
+          ecache[v - v0] = sv;
+          if (sv > lm) {
+            lz = lz * (double)expf(lm - sv);
+            lm = sv;
+          }
+          lz += (double)expf(sv - lm);
         }
-        lz += (double)expf(sv - lm);
       }
     }
-  }
-  const float cm = block_reduce(lm, fred, [](float x, float y) { return fmaxf(x, y); });
-  lz = lm == -INFINITY ? 0.0 : lz * exp((double)lm - (double)cm);
-  const double cz = block_reduce(lz, dred, [](double x, double y) { return x + y; });
-  if (tid == 0) {
-    s_m = cm;
-    s_z = cz;
-  }
-  cluster.sync();
-  float mf = -INFINITY;
-  for (int r = 0; r < SC_CTAS; ++r) mf = fmaxf(mf, *cluster.map_shared_rank(&s_m, r));
-  double Z = 0.0;
-  for (int r = 0; r < SC_CTAS; ++r) {
-    const float mr = *cluster.map_shared_rank(&s_m, r);
-    const double zr = *cluster.map_shared_rank(&s_z, r);
-    Z += mr == -INFINITY ? 0.0 : zr * exp((double)mr - (double)mf);
+    const float cm = block_reduce(lm, fred, [](float x, float y) { return fmaxf(x, y); });
+    lz = lm == -INFINITY ? 0.0 : lz * exp((double)lm - (double)cm);
+    const double cz = block_reduce(lz, dred, [](double x, double y) { return x + y; });
+    if (tid == 0) {
+      s_m = cm;
+      s_z = cz;
+    }
+    cluster.sync();
+    for (int r = 0; r < SC_CTAS; ++r) mf = fmaxf(mf, *cluster.map_shared_rank(&s_m, r));
+    for (int r = 0; r < SC_CTAS; ++r) {
+      const float mr = *cluster.map_shared_rank(&s_m, r);
+      const double zr = *cluster.map_shared_rank(&s_z, r);
+      Z += mr == -INFINITY ? 0.0 : zr * exp((double)mr - (double)mf);
+    }
   }
   const double invZ = 1.0 / Z;
   // warp-contiguous chunks of this CTA's slice (coalesced; chunk w = [c0, c1))
@@ -865,34 +744,6 @@ __global__ void __cluster_dims__(TW_CTAS, 1, 1) __launch_bounds__(TW_THREADS)
   cluster.sync();  // peers' lists stay alive until rank 0 has read them
 }
 
-static SampleDev to_dev(const sd_sample_args& h) {
-  SampleDev d;
-  d.rows = h.rows;
-  d.V = h.V;
-  d.in_kind = h.in_kind;
-  d.temperature = h.temperature;
-  d.theta = h.theta;
-  d.ctrl_style = h.ctrl_style;
-  d.member_kind = h.member_kind;
-  d.member_mask = h.member_mask;
-  d.win_count = h.win_count;
-  d.win_ring = h.win_ring;
-  d.state = h.state;
-  d.window = h.window;
-  d.tree = h.tree;
-  d.depth = h.depth;
-  d.trunc_kind = h.trunc_kind;
-  d.trunc_value = h.trunc_value;
-  d.eta_alpha = h.eta_alpha;
-  d.seed = h.seed;
-  d.positions = h.positions;
-  d.n = h.n;
-  d.probs_out = h.probs_out;
-  d.trunc_out = h.trunc_out;
-  d.token_out = h.token_out;
-  return d;
-}
-
 }  // namespace sd
 
 using namespace sd;
@@ -910,8 +761,13 @@ int sd_sample_rows(const void* in, const sd_sample_args* args_host, sd_stream_t 
   SD_REQUIRE(h.positions || h.tree, "sd_sample_rows: need positions or tree");
   SampleDev d = to_dev(h);
   auto st = as_stream(stream);
-  if (h.in_kind == SD_IN_LOGITS_F32 && !h.probs_out && !h.trunc_out && h.token_out &&
-      (h.trunc_kind == SD_TRUNC_NONE || h.trunc_kind == SD_TRUNC_MIN_P || h.trunc_kind == SD_TRUNC_TOP_P)) {
+  const bool cluster_ok = !h.probs_out && !h.trunc_out && h.token_out &&
+      (h.trunc_kind == SD_TRUNC_NONE || h.trunc_kind == SD_TRUNC_MIN_P || h.trunc_kind == SD_TRUNC_TOP_P);
+  if (h.in_kind == SD_IN_SCALED_F32)
+    SD_REQUIRE(cluster_ok && h.stats && h.stats_tiles == (h.V + 127) / 128,
+               "sd_sample_rows: scaled input needs the token draw only (no probs/trunc outputs, none/min-p/top-p) "
+               "and the LM head's tile statistics");
+  if ((h.in_kind == SD_IN_LOGITS_F32 || h.in_kind == SD_IN_SCALED_F32) && cluster_ok) {
     // engine path: one CTA cluster per row
     const size_t smem = (size_t)((h.V + SC_CTAS - 1) / SC_CTAS) * sizeof(float);
     SD_REQUIRE(smem <= 200 * 1024, "sd_sample_rows: vocabulary too large for the cluster path");

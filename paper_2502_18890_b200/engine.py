@@ -308,8 +308,6 @@ class Session:
                 return out
 
         h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
-        logits = m.lm_logits(h0)
-        self.verify_logits = logits
         a = L.SampleArgs()
         a.rows, a.V, a.in_kind = T, m.config.vocab_size, L.IN_LOGITS_F32
         _trunc_fields(a, smp)
@@ -319,6 +317,21 @@ class Session:
         a.tree, a.depth = L.ptr(rec), self.depth
         a.positions, a.n = None, -1 if graph else n
         a.token_out = L.ptr(self.y)
+        if m.lmhead_fused_ok(T) and a.trunc_kind in (L.TRUNC_NONE, L.TRUNC_MIN_P, L.TRUNC_TOP_P):
+            # LM head + penalty + per-tile softmax statistics in one tcgen05 launch;
+            # the sampler then skips its first pass (engine.py:237-245)
+            if getattr(self, "_lm_bufs", None) is None:
+                V = m.config.vocab_size
+                tiles = L.load().sd_lmhead_tiles(V)
+                self._lm_bufs = (torch.empty((T, V), dtype=torch.float32, device=m.device),
+                                 torch.empty((T, tiles, 2), dtype=torch.float64, device=m.device),
+                                 torch.empty((T, m.config.hidden_dim), dtype=m.dtype, device=m.device), tiles)
+            logits, stats, xb, tiles = self._lm_bufs
+            m.lm_head_sample_stats(h0, a, logits, stats, xb)
+            a.in_kind, a.stats, a.stats_tiles = L.IN_SCALED_F32, L.ptr(stats), tiles
+        else:
+            logits = m.lm_logits(h0)
+        self.verify_logits = logits
         L.call("sd_sample_rows", L.ptr(logits), a, L.stream())
         L.call("sd_accept_commit", L.ptr(rec), L.ptr(self.y), self.select_seed, -1 if graph else n, self.depth,
                int(cfg.bonus), L.ptr(self.state), L.ptr(self.window.ring), L.ptr(self.window.count), smp.window,

@@ -531,6 +531,33 @@ class TinyTransformer:
     def lm_logits(self, h0: torch.Tensor) -> torch.Tensor:
         return self.mm(h0.to(self.dtype), self.embed.t())
 
+    # verification LM head fused with the penalty + softmax statistics of the
+    # sampler (sd_lmhead_sample_stats). A/B switch: tools only.
+    fuse_lm_head = os.environ.get("SD_FUSE_LM_HEAD", "1") != "0"
+
+    def lmhead_fused_ok(self, T: int) -> bool:
+        return (self.fuse_lm_head and self.dtype == torch.bfloat16 and self.device.type == "cuda" and 0 < T <= 128
+                and self.config.hidden_dim % 64 == 0 and self.embed.is_contiguous())
+
+    def lm_head_sample_stats(self, h0: torch.Tensor, args, logits_out: torch.Tensor, stats_out: torch.Tensor,
+                             x_buf: torch.Tensor | None = None) -> None:
+        """logits_out [T, V] = penalised scaled logits, stats_out [T, tiles, 2]
+        = per-128-token (max, sum-exp), for the penalty fields of `args`
+        (an L.SampleArgs) — one tcgen05 launch streaming the tied embedding."""
+        import ctypes
+        if getattr(self, "_lm_tmap", None) is None:
+            V, d = self.config.vocab_size, self.config.hidden_dim
+            # box-contiguous copy of the tied embedding (+1.05 GB at cfg3), made once
+            self._lm_tiled = torch.empty(L.load().sd_lmhead_tiled_bytes(V, d), dtype=torch.uint8, device=self.device)
+            L.call("sd_tile_lmhead", L.ptr(self.embed), V, d, L.ptr(self._lm_tiled), L.stream())
+            self._lm_tmap = ctypes.create_string_buffer(128)
+            L.call("sd_make_lmhead_tmap", L.ptr(self._lm_tiled), V, d, self._lm_tmap)
+        T = h0.shape[0]
+        x = x_buf if x_buf is not None else torch.empty((T, h0.shape[1]), dtype=self.dtype, device=self.device)
+        x.copy_(h0)
+        L.call("sd_lmhead_sample_stats", L.ptr(x), T, self.config.hidden_dim, self._lm_tmap, self.config.vocab_size,
+               args, L.ptr(logits_out), L.ptr(stats_out), L.stream())
+
     # ------------------------------------------------------ generic API ----
     def forward(self, req: ForwardRequest) -> ForwardResult:
         """Reference forward contract (model.py:251-313) on device."""

@@ -10,6 +10,9 @@ sys.path.insert(0, ".")
 from paper_2502_18890_b200 import _lib as L  # noqa: E402
 
 shapes = {"qkv": (4096, 6144), "wo": (4096, 4096), "w1": (4096, 16384), "w2": (16384, 4096)}
+if os.environ.get("GEMM_SHAPES"):
+    shapes = {k: v for k, v in shapes.items() if k in os.environ["GEMM_SHAPES"].split(",")}
+IMPLS = tuple(os.environ.get("GEMM_IMPLS", "cublas,sd_gemm").split(","))
 dev = "cuda"
 for M in [int(m) for m in os.environ.get("GEMM_MS", "1,101").split(",")]:
     for name, (K, N) in shapes.items():
@@ -29,7 +32,7 @@ for M in [int(m) for m in os.environ.get("GEMM_MS", "1,101").split(",")]:
         epi = 1 if name == "w1" else 0
         ws = torch.zeros(max(256, L.load().sd_gemm_workspace_bytes(M, N, K)), dtype=torch.uint8, device=dev)
         out = []
-        for impl in ("cublas", "sd_gemm"):
+        for impl in IMPLS:
             def run(i):
                 if impl == "cublas":
                     torch.mm(x, Ws[i % copies], out_dtype=torch.float32)
