@@ -97,15 +97,17 @@ static __device__ __forceinline__ double scaled(double l, bool member, const Sam
 }
 
 // thread 0: per-row patches (engine.py:155-181) and draw position
+// the draw key of a row: explicit positions, or n / n + depth + 1 from the tree
+static __device__ __forceinline__ int64_t row_pos(const SampleDev& a, int row) {
+  if (a.positions) return a.positions[row];
+  const int64_t n = a.n >= 0 ? a.n : a.state[SD_ST_BASE] + 1;  // n < 0: device-resident step
+  return row == 0 ? n : n + a.tree[tree_off::NDEPTH + row - 1] + 1;
+}
+
 static __device__ __noinline__ void row_setup(const SampleDev& a, int row, RowCtx& rc) {
   rc.n_patch = 0;
   for (int i = 0; i < 32; ++i) rc.bloom[i] = 0u;
-  if (a.positions) {
-    rc.pos = a.positions[row];
-  } else {
-    const int64_t n = a.n >= 0 ? a.n : a.state[SD_ST_BASE] + 1;  // n < 0: device-resident step
-    rc.pos = row == 0 ? n : n + a.tree[tree_off::NDEPTH + row - 1] + 1;
-  }
+  rc.pos = row_pos(a, row);
   if (a.member_kind != SD_MEMBER_TREE || a.window <= 0 || row == 0) return;
   const int W = a.window;
   const int node = row - 1;

@@ -358,7 +358,12 @@ __global__ void __cluster_dims__(SC_CTAS, 1, 1) __launch_bounds__(SC_THREADS, 3)
   const int V = a.V;
   const int v0 = (int)((int64_t)V * rank / SC_CTAS), v1 = (int)((int64_t)V * (rank + 1) / SC_CTAS);
   const float* lg = logits + (int64_t)row * V;
-  if (live && tid == 0) row_setup(a, row, rc);
+  if (live && tid == 0) {
+    if (a.in_kind == SD_IN_SCALED_F32)
+      rc.pos = row_pos(a, row);  // the LM head already applied the row's penalty splice
+    else
+      row_setup(a, row, rc);
+  }
   __syncthreads();
   const float inv_t = (float)(1.0 / a.temperature), inv_tt = (float)(1.0 / (a.temperature * a.theta));
   const float th = (float)a.theta;
