@@ -292,6 +292,9 @@ def main():
     achieved = alg_bytes / attn["avg_s"] / 1e9
     bound = "hbm" if (alg_flops / (tflops * 1e12)) < (alg_bytes / (hbm * 1e9)) else "tensor"
     kernels = {"draft_attention": time_draft_attention(sess, model, hbm, reps=args.attn_reps)}
+    lm = time_lmhead(sess, model, hbm, reps=args.attn_reps)
+    if lm is not None:
+        kernels["lm_head"] = lm
     if world == 1:
         kernels["refresh"] = time_refresh(sess, model, ctx, hbm, reps=args.attn_reps)
         acc = tokens / max(1, len(recs))
@@ -434,6 +437,28 @@ def _graph_time(fn, reps):
         e1.record(s)
         torch.cuda.synchronize()
     return e0.elapsed_time(e1) / 1e3 / reps
+
+
+def time_lmhead(sess, model, hbm, reps=3):
+    """CUDA-event time of the fused verification LM head (sd_lmhead_sample_stats:
+    embedding stream + penalty + scaled logits + tile statistics) with the
+    session's own arguments and buffers, 4 launches back to back per replay."""
+    import torch
+    a = sess._verify_sample_args(0, True)
+    if not sess._lmhead_fused(a):
+        return None
+    T, V, d = sess.Tmax, model.config.vocab_size, model.config.hidden_dim
+    h0 = torch.randn((T, d), device="cuda")
+
+    def one():
+        sess._lmhead_stats(h0, sess._verify_sample_args(0, True))
+    avg = _graph_time(lambda: [one() for _ in range(4)], reps) / 4
+    live = int(sess.tree_rec[0].item())
+    tiles = (V + 127) // 128
+    alg = V * d * 2 + T * d * 2 + live * V * 4 + live * tiles * 16
+    return {"bound": "hbm", "achieved": alg / avg / 1e9, "peak": hbm, "unit": "GB/s", "frac": alg / avg / 1e9 / hbm,
+            "avg_launch_us": avg * 1e6, "alg_bytes_per_launch": alg, "rows": live,
+            "kernel": "sd_lmhead_sample_stats (tcgen05 tied LM head + penalty + scaled logits + tile softmax stats)"}
 
 
 def time_draft_attention(sess, model, hbm, reps=3):

@@ -308,27 +308,9 @@ class Session:
                 return out
 
         h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
-        a = L.SampleArgs()
-        a.rows, a.V, a.in_kind = T, m.config.vocab_size, L.IN_LOGITS_F32
-        _trunc_fields(a, smp)
-        a.member_kind = L.MEMBER_TREE
-        a.win_count, a.win_ring, a.state = L.ptr(self.window.count), L.ptr(self.window.ring), L.ptr(self.state)
-        a.window = smp.window
-        a.tree, a.depth = L.ptr(rec), self.depth
-        a.positions, a.n = None, -1 if graph else n
-        a.token_out = L.ptr(self.y)
-        if m.lmhead_fused_ok(T) and a.trunc_kind in (L.TRUNC_NONE, L.TRUNC_MIN_P, L.TRUNC_TOP_P):
-            # LM head + penalty + per-tile softmax statistics in one tcgen05 launch;
-            # the sampler then skips its first pass (engine.py:237-245)
-            if getattr(self, "_lm_bufs", None) is None:
-                V = m.config.vocab_size
-                tiles = L.load().sd_lmhead_tiles(V)
-                self._lm_bufs = (torch.empty((T, V), dtype=torch.float32, device=m.device),
-                                 torch.empty((T, tiles, 2), dtype=torch.float64, device=m.device),
-                                 torch.empty((T, m.config.hidden_dim), dtype=m.dtype, device=m.device), tiles)
-            logits, stats, xb, tiles = self._lm_bufs
-            m.lm_head_sample_stats(h0, a, logits, stats, xb)
-            a.in_kind, a.stats, a.stats_tiles = L.IN_SCALED_F32, L.ptr(stats), tiles
+        a = self._verify_sample_args(n, graph)
+        if self._lmhead_fused(a):
+            logits = self._lmhead_stats(h0, a)
         else:
             logits = m.lm_logits(h0)
         self.verify_logits = logits
@@ -339,6 +321,40 @@ class Session:
         F.reconcile_device(-1 if graph else base, self.result, self.q_pre, T, m.H, self.q_sum)
         # admit the accepted rows / evict to the budget (engine.py:281-283), on device
         self.partial.step_device(F, self.result)
+
+    def _verify_sample_args(self, n: int, graph: bool) -> "L.SampleArgs":
+        """Sampler arguments of the verification rows: tree-row penalty splices
+        (engine.py:155-181) over the window, the configured truncation."""
+        m, smp = self.model, self.config.sampler
+        a = L.SampleArgs()
+        a.rows, a.V, a.in_kind = self.Tmax, m.config.vocab_size, L.IN_LOGITS_F32
+        _trunc_fields(a, smp)
+        a.member_kind = L.MEMBER_TREE
+        a.win_count, a.win_ring, a.state = L.ptr(self.window.count), L.ptr(self.window.ring), L.ptr(self.state)
+        a.window = smp.window
+        a.tree, a.depth = L.ptr(self.tree_rec), self.depth
+        a.positions, a.n = None, -1 if graph else n
+        a.token_out = L.ptr(self.y)
+        return a
+
+    def _lmhead_fused(self, a) -> bool:
+        return self.model.lmhead_fused_ok(self.Tmax) and a.trunc_kind in (L.TRUNC_NONE, L.TRUNC_MIN_P, L.TRUNC_TOP_P)
+
+    def _lmhead_stats(self, h0, a):
+        """LM head + penalty + per-tile softmax statistics in one tcgen05 launch;
+        `a` is switched to the sampler's scaled-input mode (engine.py:237-245)."""
+        m = self.model
+        if getattr(self, "_lm_bufs", None) is None:
+            V, T = m.config.vocab_size, self.Tmax
+            tiles = L.load().sd_lmhead_tiles(V)
+            self._lm_bufs = (torch.empty((T, V), dtype=torch.float32, device=m.device),
+                             torch.empty((T, tiles, 2), dtype=torch.float64, device=m.device),
+                             torch.empty((T, m.config.hidden_dim), dtype=m.dtype, device=m.device), tiles)
+        logits, stats, xb, tiles = self._lm_bufs
+        a.in_kind, a.stats, a.stats_tiles = L.IN_LOGITS_F32, None, 0
+        m.lm_head_sample_stats(h0, a, logits, stats, xb)
+        a.in_kind, a.stats, a.stats_tiles = L.IN_SCALED_F32, L.ptr(stats), tiles
+        return logits
 
     def step(self) -> IterationRecord:
         if self.done:
