@@ -144,14 +144,17 @@ launch_count = 0
 
 # PROFILING ONLY: SD_DEBUG_SKIP="sd_attention:0,sd_add_rmsnorm,mm,..." drops those
 # launches (results become garbage) to measure each kernel's marginal cost in the
-# real overlapped step; ":k" matches an sd_attention src_kind (0 verify, 1 draft).
+# real overlapped step; ":k" matches an sd_attention src_kind (0 verify, 1 draft),
+# the row count of sd_rope_stage / sd_add_rmsnorm (1: draft, 101: verify).
 DEBUG_SKIP = frozenset(x for x in os.environ.get("SD_DEBUG_SKIP", "").split(",") if x)
 
 
 def call(name: str, *args):
     global launch_count
     if DEBUG_SKIP and (name in DEBUG_SKIP or (name == "sd_attention" and f"{name}:{args[6]}" in DEBUG_SKIP)
-                       or (name == "sd_gemv" and f"{name}:{args[3]}" in DEBUG_SKIP)):
+                       or (name == "sd_gemv" and f"{name}:{args[3]}" in DEBUG_SKIP)
+                       or (name == "sd_rope_stage" and f"{name}:{args[1]}" in DEBUG_SKIP)
+                       or (name == "sd_add_rmsnorm" and f"{name}:{args[2]}" in DEBUG_SKIP)):
         return 0
     if name not in _NO_LAUNCH:
         launch_count += _LAUNCHES.get(name, 1)
