@@ -292,6 +292,7 @@ def main():
     achieved = alg_bytes / attn["avg_s"] / 1e9
     bound = "hbm" if (alg_flops / (tflops * 1e12)) < (alg_bytes / (hbm * 1e9)) else "tensor"
     kernels = {"draft_attention": time_draft_attention(sess, model, hbm, reps=args.attn_reps)}
+    relaxed_edges = getattr(sess, "relaxed_edges", 0)
     lm = time_lmhead(sess, model, hbm, reps=args.attn_reps)
     if lm is not None:
         kernels["lm_head"] = lm
@@ -318,6 +319,7 @@ def main():
         "e2e": {"value": tokens / wall, "unit": "tokens/s", "h2d_bytes_per_step": 4, "d2h_bytes_per_step": 128,
                 "note": "Session.step() wall clock incl. per-step result D2H"},
         "gpu_launches": launches,
+        "graph_relaxed_edges": relaxed_edges,
         "roofline": {"bound": bound, "achieved": achieved if bound == "hbm" else alg_flops / attn["avg_s"] / 1e12,
                      "peak": hbm if bound == "hbm" else tflops, "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
                      "frac": (achieved / hbm) if bound == "hbm" else (alg_flops / attn["avg_s"] / 1e12) / tflops,

@@ -53,6 +53,13 @@ typedef void* sd_stream_t;
 int sd_version(void);
 const char* sd_last_error(void);
 
+/* Post-process a captured step graph (cudaGraph_t, before instantiation):
+ * programmatic edges from a kernel outside this library (cuBLAS) to one of
+ * ours are moved to the predecessor's launch-completion port, so our kernel
+ * launches while the library kernel runs and waits in griddepcontrol.wait.
+ * Not a reference interface: graph scheduling of the step. */
+int sd_graph_relax_library_edges(void* graph, int* relaxed_out);
+
 /* ---- dense-layer plumbing (model.py:234-236, 278, 306-311) ---- */
 /* h[t,:] = embed[tokens[t],:] (as f32) */
 int sd_embed(const int32_t* tokens, int T, const void* embed, int dtype, int d, float* h, sd_stream_t stream);

@@ -51,6 +51,7 @@ class SampleArgs(C.Structure):
 
 _SIGS = {
     "sd_version": (INT, []),
+    "sd_graph_relax_library_edges": (INT, [P, C.POINTER(INT)]),
     "sd_last_error": (C.c_char_p, []),
     "sd_embed": (INT, [P, INT, P, INT, INT, P, P]),
     "sd_add_rmsnorm": (INT, [P, P, INT, INT, P, F32, P, INT, INT, I64, P]),
@@ -135,7 +136,7 @@ def require_cuda():
 
 # kernels launched per successful entry-point call (for the bench's gpu_launches)
 _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + tree chunk + merge)
-_NO_LAUNCH = {"sd_version", "sd_last_error", "sd_attention_workspace_bytes", "sd_refresh_workspace_bytes",
+_NO_LAUNCH = {"sd_version", "sd_graph_relax_library_edges", "sd_last_error", "sd_attention_workspace_bytes", "sd_refresh_workspace_bytes",
               "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_make_slot_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
               "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes", "sd_make_lmhead_tmap",
               "sd_lmhead_tiles", "sd_lmhead_tiled_bytes"}

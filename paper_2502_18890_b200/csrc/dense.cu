@@ -138,6 +138,8 @@ __global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __
 // 4 elements per thread: one 16-byte load, one 8-byte (bf16) / 16-byte (fp32) store
 template <typename OT>
 __global__ void silu4_kernel(const float4* __restrict__ a, OT* __restrict__ out, size_t n4) {
+  pdl_trigger();
+  pdl_wait();  // a is the projection before (PDL launch: may start under its tail)
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     const float4 v = __ldcs(a + i);
     const float r0 = v.x / (1.f + __expf(-v.x)), r1 = v.y / (1.f + __expf(-v.y));
@@ -332,9 +334,10 @@ int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stre
   auto st = as_stream(stream);
   const bool vec = n % 4 == 0 && ((uintptr_t)a % 16) == 0 && ((uintptr_t)out % 16) == 0;
   if (vec && out_dtype == SD_BF16)
-    silu4_kernel<<<grid_for(n / 4), 256, 0, st>>>((const float4*)a, (__nv_bfloat16*)out, n / 4);
+    launch_pdl(silu4_kernel<__nv_bfloat16>, dim3(grid_for(n / 4)), dim3(256), 0, st, (const float4*)a,
+               (__nv_bfloat16*)out, n / 4);
   else if (vec && out_dtype == SD_F32)
-    silu4_kernel<<<grid_for(n / 4), 256, 0, st>>>((const float4*)a, (float*)out, n / 4);
+    launch_pdl(silu4_kernel<float>, dim3(grid_for(n / 4)), dim3(256), 0, st, (const float4*)a, (float*)out, n / 4);
   else if (out_dtype == SD_BF16)
     silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (__nv_bfloat16*)out, n);
   else if (out_dtype == SD_F32)

@@ -29,6 +29,7 @@ one graph launch (plus a refresh launch every B - S tokens).
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -415,13 +416,18 @@ class Session:
         self.records.append(rec)
         return rec
 
+    # step-graph post-processing (sd_graph_relax_library_edges); A/B switch: tools only
+    relax_library_edges = os.environ.get("SD_RELAX_EDGES", "1") != "0"
+    relaxed_edges = 0
+
     def _capture(self) -> None:
         """Capture draft + verify + result copy as one CUDA graph (step-invariant
         launch arguments; see the module docstring). Capture does not run the
         work: step() replays the graph right after."""
         m, F = self.model, self.full
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
+        relax = self.relax_library_edges
+        g = torch.cuda.CUDAGraph(keep_graph=True) if relax else torch.cuda.CUDAGraph()
         n = len(self.tokens)
         l0 = L.launch_count
         with torch.cuda.graph(g):
@@ -430,6 +436,14 @@ class Session:
             self.result_host.copy_(self.result, non_blocking=True)
         self._graph_launches = L.launch_count - l0  # our kernels per replay
         L.launch_count = l0
+        if relax:
+            # cuBLAS -> our kernel edges fire at the projection's launch completion
+            # (our kernels wait in griddepcontrol.wait): no launch gap after cuBLAS
+            import ctypes
+            n_relaxed = ctypes.c_int(0)
+            L.call("sd_graph_relax_library_edges", g.raw_cuda_graph(), ctypes.byref(n_relaxed))
+            self.relaxed_edges = n_relaxed.value
+            g.instantiate()
         self._graph = g
 
     def metrics(self) -> RunMetrics:
