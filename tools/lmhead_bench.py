@@ -18,7 +18,7 @@ _args, _tree_and_window = _m._args, _m._tree_and_window
 
 import os  # noqa: E402
 
-V, K, T = int(os.environ.get("LMH_V", 128256)), 4096, 101
+V, K, T = int(os.environ.get("LMH_V", 128256)), 4096, int(os.environ.get("LMH_T", 101))
 g = np.random.default_rng(0)
 st, dw, rec, W = _tree_and_window(Lb, V, g)
 E = (torch.randn((V, K), device="cuda") * (3.0 / K ** 0.5)).to(torch.bfloat16)
