@@ -359,3 +359,37 @@ def test_cluster_sampler_vs_oracle_tree_rows():
         a.token_out = Lb.ptr(y)
         Lb.call("sd_sample_rows", Lb.ptr(torch.as_tensor(logits, device="cuda")), a, Lb.stream())
         assert y.cpu().tolist() == want, trunc
+
+
+# the other BASELINE configurations' head layouts at 2 layers (SURVEY §8(c) layering (3)):
+# cfg2 Qwen2.5-1.5B-like (G=6, Hk=2), cfg4 LLaMA2-7B-like (G=1), cfg5 Qwen2.5-14B-like (G=5, d=5120)
+OTHER_CFGS = {
+    "cfg2": dict(vocab_size=151936, num_layers=2, hidden_dim=1536, num_heads=12, num_kv_heads=2, gamma=3,
+                 max_positions=4096, init_seed=2),
+    "cfg4": dict(vocab_size=32000, num_layers=2, hidden_dim=4096, num_heads=32, num_kv_heads=32, gamma=3,
+                 max_positions=4096, init_seed=4),
+    "cfg5": dict(vocab_size=152064, num_layers=2, hidden_dim=5120, num_heads=40, num_kv_heads=8, gamma=3,
+                 max_positions=4096, init_seed=5),
+}
+
+
+@pytest.mark.parametrize("name", sorted(OTHER_CFGS))
+def test_session_greedy_tokens_vs_oracle_other_configs(name):
+    """Graph-replayed sessions at the cfg2 / cfg4 / cfg5 head layouts (tcgen05 verify
+    with G = 6 / 1 / 5, the fused LM head at V = 151936 / 32000 / 152064, budgeted
+    partial cache with a refresh) emit the oracle's greedy tokens wherever its
+    top-1 margin decides them (engine.py:13-18)."""
+    import paper_2502_18890_b200 as sd
+    c = OTHER_CFGS[name]
+    m = sd.TinyTransformer(sd.ModelConfig(**c), dtype=torch.bfloat16, init="reference")
+    om = OM.TinyTransformer(OM.ModelConfig(**c), params=m.parameters_host())
+    dcfg, osmp = engine_cfgs(target=96, budget=64, sink=16)
+    prompt = sd.rng.random_prompt(300, c["vocab_size"], seed=3)
+    s = sd.Session(m, prompt, dcfg)
+    while not s.done:
+        s.step()
+    assert s._graph is not None and s.device_error() == 0
+    assert sum(r.refreshed for r in s.records) >= 1
+    bad, undecided = OC.greedy_mismatches(om, prompt, s.emitted, osmp, MARGIN_TOL)
+    assert not bad, f"{name}: decided tokens differ (i, device, oracle, margin): {bad[:5]}"
+    assert undecided < len(s.emitted) // 4, f"{name}: {undecided} of {len(s.emitted)} positions undecided"
