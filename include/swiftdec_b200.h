@@ -162,6 +162,7 @@ int sd_debug_tc_trace(void* trace_dev, int force_chunks);
 #define SD_GEMM_EPI_F32 0
 #define SD_GEMM_EPI_SILU_BF16 1
 #define SD_GEMM_EPI_ADDNORM 2 /* internal to sd_gemv_addnorm */
+#define SD_GEMM_EPI_ROPE 3    /* internal to sd_gemv_rope */
 int sd_tile_weight(const void* w, int K, int N, void* w_tiled, sd_stream_t stream);
 int sd_make_weight_tmap(const void* w_tiled, int K, int N, void* tmap_out_host);
 int sd_gemm_splits(int M, int N, int K, int epi);
@@ -189,6 +190,16 @@ int sd_gemv(const void* x, int K, const void* w, int N, int epi, void* y, void* 
 int sd_gemv_norm(const float* h_in, const float* delta, const float* gain, float eps, float* h_out, int K,
                  const void* w, int N, int epi, void* y, void* workspace, size_t workspace_bytes,
                  sd_stream_t stream);
+/* The draft row's QKV projection with RoPE + staging as its epilogue (replaces
+ * sd_gemv(_norm) + sd_rope_stage for one row, model.py:216-232, 283-289): the
+ * input is bf16 x, or (h_in, delta, gain) as in sd_gemv_norm; the output is
+ * q_rot [H][dh] (bf16, rotated at *pos and scaled by q_scale), k_rot [Hk][dh]
+ * (rotated) and v [Hk][dh] (bf16); N = (H + 2 Hk) dh; cos/sin tables as
+ * sd_rope_stage. */
+int sd_gemv_rope(const void* x, const float* h_in, const float* delta, const float* gain, float eps, float* h_out,
+                 int K, const void* w, int N, const int32_t* pos, const float* cos_table, const float* sin_table,
+                 float q_scale, int H, int Hk, int dh, void* q_rot, void* k_rot, void* v, void* workspace,
+                 size_t workspace_bytes, sd_stream_t stream);
 int sd_gemv_addnorm(const void* x, int K, const void* w, int N, float* h, const float* gain, float eps, void* x_out,
                     int x_dtype, void* workspace, size_t workspace_bytes, sd_stream_t stream);
 

@@ -67,6 +67,7 @@ _SIGS = {
     "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_gemv_addnorm": (INT, [P, INT, P, INT, P, P, F32, P, INT, P, SZ, P]),
     "sd_gemv_norm": (INT, [P, P, P, F32, P, INT, P, INT, INT, P, P, SZ, P]),
+    "sd_gemv_rope": (INT, [P, P, P, P, F32, P, INT, P, INT, P, P, P, F32, INT, INT, INT, P, P, P, P, SZ, P]),
     "sd_tile_weight": (INT, [P, INT, INT, P, P]),
     "sd_make_weight_tmap": (INT, [P, INT, INT, P]),
     "sd_gemm_splits": (INT, [INT, INT, INT, INT]),

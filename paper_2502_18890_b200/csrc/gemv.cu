@@ -190,6 +190,22 @@ struct AddNorm {
 // fixed order (identical on all CTAs), then scales its K slice; the CTAs of
 // column block 0 write the updated stream to h_out (not h_in: other CTAs are
 // still reading it).
+// RoPE + staging of the single draft row as the QKV projection's epilogue
+// (model.py:216-232 for one row; the sd_rope_stage it replaces): pairs of
+// adjacent columns (held by adjacent lanes) are rotated at the device position
+// *pos; Q is scaled and written as bf16 [H][dh], K rotated into k [Hk][dh], V
+// copied into v [Hk][dh].
+struct RopeOut {
+  const int32_t* pos;  // NULL: plain epilogue
+  const float* cosT;   // [positions][dh / 2]
+  const float* sinT;
+  float q_scale;
+  int H, Hk, dh;
+  __nv_bfloat16* q;
+  __nv_bfloat16* k;
+  __nv_bfloat16* v;
+};
+
 struct XNorm {
   const float* h_in;   // [K] (NULL: plain bf16 x)
   const float* delta;  // [K]
@@ -202,7 +218,7 @@ template <bool ADDNORM>
 __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     gemv_tma_kernel(const __grid_constant__ CUtensorMap wmap, const __nv_bfloat16* __restrict__ x, int K, int N,
                     int splits, int epi, void* __restrict__ y, float* __restrict__ part, int* __restrict__ counters,
-                    AddNorm an, XNorm xn) {
+                    AddNorm an, XNorm xn, RopeOut ro) {
   extern __shared__ __align__(1024) uint8_t gsm[];
   uint8_t* ring = gsm;                                    // NS stages
   float* xs = reinterpret_cast<float*>(gsm + NS * STAGE_BYTES);  // K slice of x
@@ -317,6 +333,26 @@ __global__ void __launch_bounds__((WARPS + 1) * 32, 1)
     for (int sp = 0; sp < splits; ++sp) v += gcol < N ? __ldcg(part + (int64_t)sp * N + gcol) : 0.f;
     if (tid == 0) counters[cb] = 0;
   }
+  if (epi == SD_GEMM_EPI_ROPE) {
+    // lanes c, c ^ 1 hold the pair (2i, 2i + 1) of one head (COLS and dh are even)
+    const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+    if (gcol >= N) return;
+    const int head = gcol / ro.dh, e = gcol - head * ro.dh;
+    if (head < ro.H + ro.Hk) {
+      const int64_t pos = *ro.pos;
+      const int j = e >> 1, half = ro.dh >> 1;
+      const float cs = ro.cosT[pos * half + j], sn = ro.sinT[pos * half + j];
+      const float x0 = (c & 1) ? other : v, x1 = (c & 1) ? v : other;
+      const float r = (c & 1) ? x0 * sn + x1 * cs : x0 * cs - x1 * sn;
+      if (head < ro.H)
+        ro.q[gcol] = __float2bfloat16_rn(r * ro.q_scale);
+      else
+        ro.k[(head - ro.H) * ro.dh + e] = __float2bfloat16_rn(r);
+    } else {
+      ro.v[(head - ro.H - ro.Hk) * ro.dh + e] = __float2bfloat16_rn(v);
+    }
+    return;
+  }
   store(v);
   if constexpr (!ADDNORM) return;
   else {
@@ -425,7 +461,8 @@ static int weight_map(const void* w, int K, int N, CUtensorMap* out) {
 
 // one launch of the TMA kernel; false when its shared memory would not fit
 static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void* y, void* workspace,
-                       const AddNorm& an, cudaStream_t st, int* rc, const XNorm& xn = XNorm{}) {
+                       const AddNorm& an, cudaStream_t st, int* rc, const XNorm& xn = XNorm{},
+                       const RopeOut& ro = RopeOut{}) {
   const int blocks = (N + COLS - 1) / COLS;
   const int s = tma_splits(K, N);
   const size_t smem = (size_t)NS * STAGE_BYTES + ((K + s - 1) / s + 1) * sizeof(float);
@@ -445,7 +482,7 @@ static bool launch_tma(const void* x, int K, const void* w, int N, int epi, void
     at = smem;
   }
   launch_pdl(kern, dim3(blocks, s), dim3((WARPS + 1) * 32), smem, st, m, (const __nv_bfloat16*)x, K, N,
-             s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an, xn);
+             s, epi, y, s > 1 ? (float*)((char*)workspace + WS_HEAD) : nullptr, (int*)workspace, an, xn, ro);
   *rc = check_launch("sd_gemv");
   return true;
 }
@@ -515,6 +552,32 @@ int sd_gemv_norm(const float* h_in, const float* delta, const float* gain, float
   int rc = 0;
   if (gv::launch_tma(nullptr, K, w, N, epi, y, workspace, gv::AddNorm{}, as_stream(stream), &rc, xn)) return rc;
   set_error("sd_gemv_norm: the TMA weight stream does not fit this shape");
+  return SD_EUNSUPPORTED;
+}
+
+int sd_gemv_rope(const void* x, const float* h_in, const float* delta, const float* gain, float eps, float* h_out,
+                 int K, const void* w, int N, const int32_t* pos, const float* cos_table, const float* sin_table,
+                 float q_scale, int H, int Hk, int dh, void* q_rot, void* k_rot, void* v, void* workspace,
+                 size_t workspace_bytes, sd_stream_t stream) {
+  SD_REQUIRE(w && pos && cos_table && sin_table && q_rot && k_rot && v && K > 0 && K % 4 == 0, "sd_gemv_rope: args");
+  SD_REQUIRE(dh > 0 && dh % 2 == 0 && H > 0 && Hk > 0 && N == (H + 2 * Hk) * dh && N % 8 == 0,
+             "sd_gemv_rope: N=%d must be (H + 2 Hk) * dh", N);
+  SD_REQUIRE((x != nullptr) != (h_in != nullptr), "sd_gemv_rope: exactly one of x / h_in");
+  SD_REQUIRE(!h_in || (delta && gain && h_out && h_out != h_in && ((uintptr_t)h_in % 16) == 0 &&
+                       ((uintptr_t)delta % 16) == 0),
+             "sd_gemv_rope: residual norm inputs");
+  SD_REQUIRE(((uintptr_t)w % 16) == 0, "sd_gemv_rope: W must be 16-byte aligned");
+  const int blocks = (N + gv::COLS - 1) / gv::COLS;
+  SD_REQUIRE((size_t)blocks < (size_t)gv::WS_HEAD_INTS, "sd_gemv_rope: N=%d too wide for the counter head", N);
+  SD_REQUIRE(workspace && workspace_bytes >= sd_gemv_workspace_bytes(K, N), "sd_gemv_rope: workspace");
+  const gv::XNorm xn = h_in ? gv::XNorm{h_in, delta, gain, eps, h_out} : gv::XNorm{};
+  const gv::RopeOut ro{pos, cos_table, sin_table, q_scale, H, Hk, dh, (__nv_bfloat16*)q_rot,
+                       (__nv_bfloat16*)k_rot, (__nv_bfloat16*)v};
+  int rc = 0;
+  if (gv::launch_tma(x, K, w, N, SD_GEMM_EPI_ROPE, nullptr, workspace, gv::AddNorm{}, as_stream(stream), &rc, xn,
+                     ro))
+    return rc;
+  set_error("sd_gemv_rope: the TMA weight stream does not fit this shape");
   return SD_EUNSUPPORTED;
 }
 

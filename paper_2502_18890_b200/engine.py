@@ -259,13 +259,14 @@ class Session:
         hi = part.slot_cap  # whole slot range (holes masked): eager and replay split the draft identically
 
         def attend(l, qkv, q_pre):
-            m.rope_stage(qkv, 1, part.count_dev(), q_rot, None, None, kt, vt, m.dh, 0)
+            if qkv is not None:  # else the QKV projection already rotated and staged the row
+                m.rope_stage(qkv, 1, part.count_dev(), q_rot, None, None, kt, vt, m.dh, 0)
             m.attention(q_rot, 1, 1, part.pk[l], part.pv[l], part.head_stride, hi, part.prank[l], kt, vt,
                         m.dh, None, None, out, part.tmaps, l, ws=self.attn_ws)
             return out
 
         pend = self.result[L.RES_PENDING:L.RES_PENDING + 1]
-        h0 = m.run_layers(pend, 1, attend)
+        h0 = m.run_layers(pend, 1, attend, rope=(part.count_dev(), q_rot, kt, vt))
         logits = m.head_logits(h0, self.depth)
         self.draft_logits = logits
         win = self.window.count if smp.window > 0 else None

@@ -475,16 +475,41 @@ class TinyTransformer:
                self._gemv_ws.numel(), L.stream())
         return y
 
-    def _run_layers_row(self, tokens_dev, attend, q_pre=None):
+    # the draft row's RoPE + staging folded into its QKV projection (sd_gemv_rope):
+    # one launch per layer fewer. A/B switch: tools only.
+    fuse_draft_rope = os.environ.get("SD_FUSE_DRAFT_ROPE", "1") != "0"
+
+    def gemv_rope(self, x, pending, w, rope, h_out=None) -> None:
+        """One-row QKV projection whose epilogue rotates Q/K at the device position
+        rope[0] and writes q_rot (scaled) / k / v (rope = (pos, q_rot, k, v))."""
+        K, N = w.shape
+        pos, q_rot, k, v = rope
+        if pending is None:
+            args = (L.ptr(x), None, None, None, 1e-6, None)
+        else:
+            args = (None, L.ptr(pending[0]), L.ptr(pending[1]), L.ptr(pending[2]), 1e-6, L.ptr(h_out))
+        L.call("sd_gemv_rope", *args, K, L.ptr(w), N, L.ptr(pos), L.ptr(self.rope_cos), L.ptr(self.rope_sin),
+               self.q_scale, self.H, self.Hk, self.dh, L.ptr(q_rot), L.ptr(k), L.ptr(v), L.ptr(self._gemv_ws),
+               self._gemv_ws.numel(), L.stream())
+
+    def _run_layers_row(self, tokens_dev, attend, q_pre=None, rope=None):
         """run_layers for one row (the draft forward) with the norms fused into
-        the weight streams; the residual stream ping-pongs between two rows."""
+        the weight streams; the residual stream ping-pongs between two rows.
+        With `rope` the QKV projections also rotate and stage the row, and
+        attend() receives qkv = None."""
         h = self.embed_rows(tokens_dev, 1)
         other = torch.empty_like(h)
         x = self.norm(h, None, self.layers[0]["ln1"])
         pending = None  # (h, delta, gain) of the norm that feeds the next projection
         nl = len(self.layers)
+        rope = rope if (rope is not None and self.fuse_draft_rope) else None
         for l, ly in enumerate(self.layers):
-            if pending is None:
+            if rope is not None:
+                qkv = None
+                self.gemv_rope(x if pending is None else None, pending, ly["wqkv"], rope, h_out=other)
+                if pending is not None:
+                    h, other = other, h
+            elif pending is None:
                 qkv = self.gemv(x, ly["wqkv"])
             else:
                 qkv = self.gemv_norm(pending[0], pending[1], pending[2], other, ly["wqkv"])
@@ -499,11 +524,12 @@ class TinyTransformer:
             else:
                 return self.norm(h, d2, self.ln_f, out_dtype=torch.float32)  # h0 (fp32)
 
-    def run_layers(self, tokens_dev, T, attend, q_pre=None):
+    def run_layers(self, tokens_dev, T, attend, q_pre=None, rope=None):
         """Embedding + L layers + final norm. attend(l, qkv, q_pre_l) -> [T, H_local*dh].
-        Returns h0 = rmsnorm(h, ln_f) in fp32 [T, d]."""
+        Returns h0 = rmsnorm(h, ln_f) in fp32 [T, d]. rope (one row only): see
+        _run_layers_row."""
         if T == 1 and self._row_fused_ok():
-            return self._run_layers_row(tokens_dev, attend, q_pre)
+            return self._run_layers_row(tokens_dev, attend, q_pre, rope)
         h = self.embed_rows(tokens_dev, T)
         x = self.norm(h, None, self.layers[0]["ln1"])
         nl = len(self.layers)

@@ -826,6 +826,52 @@ def test_gemv_shared_workspace_across_shapes(lib, gemv_impl):
         torch.testing.assert_close(y, x.float() @ w.float(), rtol=1e-4, atol=1e-4)
 
 
+@pytest.mark.parametrize("d,H,Hk", [(4096, 32, 8), (1536, 12, 2), (5120, 40, 8)])
+@pytest.mark.parametrize("normed", [False, True])
+def test_gemv_rope_equals_gemv_then_rope_stage(lib, d, H, Hk, normed):
+    """The draft row's QKV projection with RoPE + staging in its epilogue
+    (sd_gemv_rope) equals sd_gemv(_norm) followed by sd_rope_stage bit for bit
+    (same split-K reduction, same rotation arithmetic; model.py:216-232)."""
+    import paper_2502_18890_b200 as sd
+    dev = torch.device("cuda")
+    dh = 128
+    N = (H + 2 * Hk) * dh
+    m = sd.TinyTransformer(sd.ModelConfig(vocab_size=256, num_layers=1, hidden_dim=d, num_heads=H, num_kv_heads=Hk,
+                                          gamma=3, max_positions=4096), dtype=torch.bfloat16, init="device")
+    ws = torch.zeros(lib.load().sd_gemv_workspace_bytes(d, N), dtype=torch.uint8, device=dev)
+    w = (torch.randn((d, N), device=dev) * d ** -0.5).to(torch.bfloat16)
+    pos = torch.tensor([1234], dtype=torch.int32, device=dev)
+    x = torch.randn((1, d), device=dev).to(torch.bfloat16)
+    h_in = torch.randn((1, d), device=dev)
+    delta = torch.randn((1, d), device=dev)
+    gain = torch.rand((d,), device=dev) + 0.5
+    outs = []
+    for fused in (False, True):
+        q = torch.full((1, H, dh), float("nan"), dtype=torch.bfloat16, device=dev)
+        k = torch.full((Hk, 1, dh), float("nan"), dtype=torch.bfloat16, device=dev)
+        v = torch.full((Hk, 1, dh), float("nan"), dtype=torch.bfloat16, device=dev)
+        h_out = torch.empty_like(h_in)
+        if fused:
+            args = ((None, lib.ptr(h_in), lib.ptr(delta), lib.ptr(gain), 1e-6, lib.ptr(h_out)) if normed
+                    else (lib.ptr(x), None, None, None, 1e-6, None))
+            lib.call("sd_gemv_rope", *args, d, lib.ptr(w), N, lib.ptr(pos), lib.ptr(m.rope_cos), lib.ptr(m.rope_sin),
+                     m.q_scale, H, Hk, dh, lib.ptr(q), lib.ptr(k), lib.ptr(v), lib.ptr(ws), ws.numel(), lib.stream())
+        else:
+            y = torch.empty((1, N), device=dev)
+            if normed:
+                lib.call("sd_gemv_norm", lib.ptr(h_in), lib.ptr(delta), lib.ptr(gain), 1e-6, lib.ptr(h_out), d,
+                         lib.ptr(w), N, lib.GEMM_EPI_F32, lib.ptr(y), lib.ptr(ws), ws.numel(), lib.stream())
+            else:
+                lib.call("sd_gemv", lib.ptr(x), d, lib.ptr(w), N, lib.GEMM_EPI_F32, lib.ptr(y), lib.ptr(ws), ws.numel(),
+                         lib.stream())
+            m.rope_stage(y, 1, pos, q, None, None, k, v, dh, 0)
+        outs.append((q.clone(), k.clone(), v.clone(), h_out.clone() if normed else None))
+    for a, b in zip(outs[0][:3], outs[1][:3]):
+        assert torch.equal(a, b)
+    if normed:
+        assert torch.equal(outs[0][3], outs[1][3])
+
+
 @pytest.mark.parametrize("V", [64, 5000, 151936])
 @pytest.mark.parametrize("trunc", ["none", "min_p", "top_p"])
 @pytest.mark.parametrize("pad", [0, 7])
