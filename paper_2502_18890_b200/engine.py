@@ -395,6 +395,9 @@ class Session:
         t1 = time.perf_counter()
         self._ev.record()
         self._ev.synchronize()
+        if self.model.world > 1:  # replicated stages stay in lock step
+            from .parallel import check_lockstep
+            check_lockstep(self.result, self.model.world, self.model.group, step=len(self.records))
         r = self.result_host.tolist()
         a = r[L.RES_ACCEPTED]
         ys = r[L.RES_YS:L.RES_YS + a]

@@ -74,6 +74,26 @@ def gather_head_partials(per_head: torch.Tensor, world: int, group=None) -> torc
     return g.permute(1, 0, 2, 3).reshape(Ln, P * Hkl, n)
 
 
+class ShardDivergence(RuntimeError):
+    """Ranks of a sharded session disagree on a step result."""
+
+
+def check_lockstep(result: torch.Tensor, world: int, group=None, step: int = -1) -> None:
+    """Guard for the replicated sampling / tree / acceptance: all-gather this
+    rank's step result (accepted count, tokens, path; a few dozen ints) and
+    raise ShardDivergence unless every rank holds rank 0's copy. The replicated
+    stages are deterministic functions of identical inputs, so a mismatch means
+    a rank's inputs differed (a collective or kernel fault), and stepping on
+    would silently desynchronise the caches."""
+    if world <= 1:
+        return
+    g = gather_rank_major(result.reshape(-1), world, group).cpu()
+    bad = [r for r in range(1, world) if not torch.equal(g[r], g[0])]
+    if bad:
+        raise ShardDivergence(f"step {step}: ranks {bad} disagree with rank 0 on the step result "
+                              f"({g[bad[0]].tolist()[:8]} vs {g[0].tolist()[:8]})")
+
+
 def sharded_scores(full, q_sum: torch.Tensor, model, start: int, end: int) -> torch.Tensor:
     """Eq. 2 scores over rows [start, end) for all layers, identical on every rank."""
     n = end - start

@@ -135,3 +135,43 @@ def test_score_exchange_selects_the_unsharded_top_k(gathered):
         np.testing.assert_allclose(summed, want, rtol=1e-12, atol=1e-12)
         sink, take = 4, 40
         assert OK.select_body(summed[sink:], sink, CTX, take) == OK.select_body(want[sink:], sink, CTX, take)
+
+
+def _lockstep_worker(rank, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from paper_2502_18890_b200.parallel import ShardDivergence, check_lockstep
+        same = torch.arange(32, dtype=torch.int32)
+        check_lockstep(same, WORLD, step=0)  # identical results: no error
+        diverged = same.clone()
+        diverged[3] += rank  # rank 1's accepted tokens differ
+        try:
+            check_lockstep(diverged, WORLD, step=1)
+            out_q.put((rank, "no error"))
+        except ShardDivergence as e:
+            out_q.put((rank, str(e)))
+    except Exception as e:  # surface worker failures to the test process
+        out_q.put((rank, repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_lockstep_guard_detects_divergent_ranks():
+    """the replicated sampler / tree / acceptance are checked
+    every sharded step; a rank whose step result differs from rank 0's raises
+    ShardDivergence on every rank (each sees the gathered results)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lockstep_worker, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(WORLD))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(WORLD):
+        assert res[r].startswith("step 1: ranks [1] disagree"), res[r]
