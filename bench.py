@@ -359,34 +359,32 @@ def seed_unique_ngrams(sess, model, c, k=20, weight=64):
 
 
 def time_verify_attention(sess, model, rows, ctx, reps=3):
-    """CUDA-event time of the verification attention alone, one launch per
-    layer (each layer's K/V is a distinct >L2 buffer), on the launching stream."""
+    """CUDA-event time of the verification attention alone (tcgen05 kernel +
+    split merge), one launch per layer (each layer's K/V is a distinct >L2
+    buffer), captured in a CUDA graph and replayed on the launching stream, so
+    the host's per-call overhead (~30 us of Python + ctypes, which would floor
+    small-context shapes) is not in the number."""
     import torch
     F = sess.full
     T = rows
     q = torch.randn((T, model.H, model.dh), device="cuda").mul_(0.1).to(model.dtype)
     out = torch.empty((T, model.H * model.dh), dtype=model.dtype, device="cuda")
+    from paper_2502_18890_b200 import _lib as L
     from paper_2502_18890_b200.model import mask_bits_from_bool
     import numpy as np
     m = np.tril(np.ones((T, T), dtype=bool))
     bits = torch.as_tensor(mask_bits_from_bool(m), device="cuda")
-    st = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     base = min(ctx, len(F))
-    for l in range(model.config.num_layers):  # warm
-        model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                        F.v[l, :, base:], F.head_stride, bits, None, out, F.tmaps, l)
-    torch.cuda.synchronize()
-    n = 0
-    e0.record(st)
-    for _ in range(reps):
-        for l in range(model.config.num_layers):
+    ws = torch.zeros(L.load().sd_attention_workspace_bytes(T, model.H, model.dh, base), dtype=torch.uint8,
+                     device="cuda")
+    Ln = model.config.num_layers
+
+    def layers():
+        for l in range(Ln):
             model.attention(q, T, 0, F.k_rot[l], F.v[l], F.head_stride, base, None, F.k_rot[l, :, base:],
-                            F.v[l, :, base:], F.head_stride, bits, None, out, F.tmaps, l)
-            n += 1
-    e1.record(st)
-    torch.cuda.synchronize()
-    return {"avg_s": e0.elapsed_time(e1) / 1e3 / n, "launches": n}
+                            F.v[l, :, base:], F.head_stride, bits, None, out, F.tmaps, l, ws=ws)
+    avg = _graph_time(layers, reps) / Ln
+    return {"avg_s": avg, "launches": reps * Ln}
 
 
 def time_refresh(sess, model, ctx, hbm, reps=3):

@@ -38,7 +38,10 @@ namespace sd {
 namespace tc {
 
 constexpr int BN = 64;          // keys per tile
-constexpr int MIN_CHUNK = 256;  // keys per split at least
+#ifndef SD_TC_MIN_CHUNK
+#define SD_TC_MIN_CHUNK 256
+#endif
+constexpr int MIN_CHUNK = SD_TC_MIN_CHUNK;  // keys per split at least
 constexpr int DH = 128;
 // K and V stream in 128-key slots (one TMA pair = 2 x 16 KB per slot; one
 // full/empty barrier pair per slot) while S / P / softmax work on 64-key

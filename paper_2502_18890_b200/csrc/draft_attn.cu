@@ -52,7 +52,10 @@ constexpr int THREADS = 32 * (NCW + 1);
 constexpr int HALF_BYTES = STAGE_KEYS * 128; // one dh half of a stage (64 slots x 128 B)
 constexpr int STAGE_BYTES = 4 * HALF_BYTES;  // K lo, K hi, V lo, V hi
 constexpr int MAX_KPS = 2048;                // slots per split (ranks staged in shared memory)
-constexpr int MIN_KPS = 128;                 // slots per split at least (merge cost vs parallelism)
+#ifndef SD_DR_MIN_KPS
+#define SD_DR_MIN_KPS 128
+#endif
+constexpr int MIN_KPS = SD_DR_MIN_KPS;                 // slots per split at least (merge cost vs parallelism)
 constexpr int OFF_RANK = NST * STAGE_BYTES;
 constexpr int OFF_FREQ = OFF_RANK + MAX_KPS * 4;
 constexpr int OFF_BAR = OFF_FREQ + 64 * 8;
