@@ -6,6 +6,9 @@ from paper_2502_18890_b200 import FullCache, _lib as L
 from paper_2502_18890_b200.model import mask_bits_from_bool
 SHAPES = [(12048, 42, 12, 2), (2048, 42, 12, 2), (4096, 41, 32, 8), (12048, 41, 32, 8), (54096, 41, 32, 8),
           (54096, 42, 40, 8)]
+import os
+if os.environ.get('TC_SHAPES'):
+    SHAPES = [tuple(int(x) for x in t.split(',')) for t in os.environ['TC_SHAPES'].split(';')]
 for (ctx, T, H, Hk) in SHAPES:
     dh = 128
     F = FullCache(1, Hk, dh, capacity=ctx + T + 64, dtype=torch.bfloat16)
