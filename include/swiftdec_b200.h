@@ -170,6 +170,17 @@ size_t sd_gemm_workspace_bytes(int M, int N, int K);
 int sd_gemm(const void* x, int M, int K, const void* w_tmap_host, int N, int epi, void* y, int64_t ldy,
             void* workspace, size_t workspace_bytes, sd_stream_t stream);
 
+/* ---- few-row weight streaming (the verification forward's tree rows,
+ * model.py:283-285, 306-309) ----
+ * y = S = sd_gemm_rows_splits(K, N) fp32 split-K slices [S][T][N] whose in-order
+ * sum is x[T][K] . W[K][N]; x, W bf16 (W row-major, the reference layout);
+ * T <= 112, K % 32 == 0, N % 256 == 0. With rows_dev (device int: the tree
+ * record's live row count) only rows < min(*rows_dev, T) are computed and
+ * written. sd_add_rmsnorm / sd_rope_stage take the slices directly. */
+int sd_gemm_rows_splits(int K, int N);
+int sd_gemm_rows(const void* x, int T, int K, const void* w, int N, const int32_t* rows_dev, float* y,
+                 sd_stream_t stream);
+
 /* ---- single-row weight streaming (the draft forward's projections and draft
  * heads, model.py:104-120, 283-285, 306-309) ----
  * y[N] = x[K] . W[K][N]; x, W bf16 (W row-major, the reference layout), fp32

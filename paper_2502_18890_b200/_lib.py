@@ -65,6 +65,8 @@ _SIGS = {
     "sd_make_slot_tmap": (INT, [P, INT, INT, INT, INT, P]),
     "sd_gemv_workspace_bytes": (SZ, [INT, INT]),
     "sd_gemv": (INT, [P, INT, P, INT, INT, P, P, SZ, P]),
+    "sd_gemm_rows_splits": (INT, [INT, INT]),
+    "sd_gemm_rows": (INT, [P, INT, INT, P, INT, P, P, P]),
     "sd_gemv_addnorm": (INT, [P, INT, P, INT, P, P, F32, P, INT, P, SZ, P]),
     "sd_gemv_norm": (INT, [P, P, P, F32, P, INT, P, INT, INT, P, P, SZ, P]),
     "sd_gemv_rope": (INT, [P, P, P, P, F32, P, INT, P, INT, P, P, P, F32, INT, INT, INT, P, P, P, P, SZ, P]),
@@ -140,7 +142,7 @@ _LAUNCHES = {"sd_attention": 2, "sd_reconcile": 2}  # tensor-core path: 3 (tc + 
 _NO_LAUNCH = {"sd_version", "sd_graph_relax_library_edges", "sd_last_error", "sd_attention_workspace_bytes", "sd_refresh_workspace_bytes",
               "sd_ngram_bytes", "sd_tree_layout", "sd_make_kv_tmap", "sd_make_slot_tmap", "sd_debug_tc_trace", "sd_make_weight_tmap",
               "sd_gemm_splits", "sd_gemm_workspace_bytes", "sd_gemv_workspace_bytes", "sd_make_lmhead_tmap",
-              "sd_lmhead_tiles", "sd_lmhead_tiled_bytes"}
+              "sd_lmhead_tiles", "sd_lmhead_tiled_bytes", "sd_gemm_rows_splits"}
 launch_count = 0
 
 

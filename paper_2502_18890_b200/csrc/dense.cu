@@ -66,6 +66,28 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* x, int64_t 
   *reinterpret_cast<uint2*>(x + i) = v;
 }
 
+// x[0] + x[s * stride] for s = 1 .. splits-1, summed in slice order (split-K
+// slices of a projection); the loads of up to 8 slices are issued before any
+// add, so a 9-slice sum costs two L2 round trips instead of nine
+__device__ __forceinline__ float4 sum_slices4(const float* p, int splits, int64_t stride) {
+  float4 acc = *reinterpret_cast<const float4*>(p);
+  for (int s0 = 1; s0 < splits; s0 += 8) {
+    float4 e[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      e[u] = s0 + u < splits ? *reinterpret_cast<const float4*>(p + (s0 + u) * stride) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (s0 + u < splits) {
+        acc.x += e[u].x;
+        acc.y += e[u].y;
+        acc.z += e[u].z;
+        acc.w += e[u].w;
+      }
+  }
+  return acc;
+}
+
 template <typename XT, int PER>
 __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restrict__ delta, int d,
                                    const float* __restrict__ gain, float eps, XT* __restrict__ x, int splits,
@@ -89,11 +111,7 @@ __global__ void add_rmsnorm_kernel(float* __restrict__ h, const float* __restric
     if (i < d) {
       v[k] = *reinterpret_cast<const float4*>(h + base + i);
       if (delta) {
-        float4 dd = *reinterpret_cast<const float4*>(delta + base + i);
-        for (int s = 1; s < splits; ++s) {  // split-K slices, summed in order
-          const float4 e = *reinterpret_cast<const float4*>(delta + s * split_stride + base + i);
-          dd.x += e.x; dd.y += e.y; dd.z += e.z; dd.w += e.w;
-        }
+        const float4 dd = sum_slices4(delta + base + i, splits, split_stride);  // split-K slices, in order
         v[k].x += dd.x; v[k].y += dd.y; v[k].z += dd.z; v[k].w += dd.w;
         *reinterpret_cast<float4*>(h + base + i) = v[k];
       }
@@ -214,8 +232,11 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   constexpr int PF = 4;  // rotation tables prefetched for a thread's first PF quads
   float2 pc[PF], ps[PF];
 #pragma unroll
+  // a row may be spread over gridDim.y CTAs (split-K input: the slice reads of
+  // one row would otherwise bound a single CTA)
+  const int u0 = threadIdx.x + blockIdx.y * blockDim.x, ustep = blockDim.x * gridDim.y;
   for (int k = 0; k < PF; ++k) {
-    const int u = threadIdx.x + k * blockDim.x;
+    const int u = u0 + k * ustep;
     if (u < quads_rot) {
       const int j = ((4 * u) % dh) >> 1;
       pc[k] = *reinterpret_cast<const float2*>(cosT + pos * half + j);
@@ -224,12 +245,8 @@ __global__ void rope_stage_kernel(const float* __restrict__ qkv, int H, int Hk, 
   }
   pdl_wait();
   int k = 0;
-  for (int u = threadIdx.x; u < quads_all; u += blockDim.x, ++k) {
-    float4 x = *reinterpret_cast<const float4*>(row + 4 * u);
-    for (int s = 1; s < splits; ++s) {  // split-K slices of the QKV GEMM, summed in order
-      const float4 e = *reinterpret_cast<const float4*>(row + s * split_stride + 4 * u);
-      x.x += e.x; x.y += e.y; x.z += e.z; x.w += e.w;
-    }
+  for (int u = u0; u < quads_all; u += ustep, ++k) {
+    float4 x = sum_slices4(row + 4 * u, splits, split_stride);  // split-K slices of the QKV GEMM, in order
     const int col = 4 * u, head = col / dh, e = col - head * dh;
     if (u < quads_rot) {
       const int j = e >> 1;  // pair index of x.x/x.y; x.z/x.w is j + 1
@@ -364,8 +381,10 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
   if (qkv_splits < 1) qkv_splits = 1;
   SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 4) == 0, "sd_rope_stage: head_dim must be a multiple of 4");
   auto st = as_stream(stream);
+  // split-K input: one CTA per 512 quads of a row, so each row's slice reads spread over several SMs
+  const int rc = qkv_splits > 1 ? ((H + 2 * Hk) * dh / 4 + 511) / 512 : 1;
 #define SD_RS(QT, KT)                                                                                          \
-  launch_pdl(rope_stage_kernel<QT, KT>, dim3(T), dim3(512), 0, st, qkv, H, Hk, dh, positions, rope_cos, rope_sin,  \
+  launch_pdl(rope_stage_kernel<QT, KT>, dim3(T, rc), dim3(512), 0, st, qkv, H, Hk, dh, positions, rope_cos, rope_sin,  \
              q_scale, (QT*)q_rot, q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev,       \
              qkv_splits, qkv_split_stride)
   if (q_dtype == SD_F32 && kv_dtype == SD_F32)

@@ -309,7 +309,11 @@ class Session:
                             F.v[l, :, base:], F.head_stride, bits, rows_dev, out, F.tmaps, l, ws=self.attn_ws)
                 return out
 
-        h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
+        m.rows_hint = rows_dev  # projections skip the padded tree rows (sd_gemm_rows)
+        try:
+            h0 = m.run_layers(toks, T, attend, q_pre=self.q_pre)
+        finally:
+            m.rows_hint = None
         a = self._verify_sample_args(n, graph)
         if self._lmhead_fused(a):
             logits = self._lmhead_stats(h0, a)

@@ -338,12 +338,40 @@ class TinyTransformer:
     # overlaps the next projection's weight prefetch (cfg3 step 8.69 vs 8.47 ms).
     fuse_norm = False
 
+    # few-row weight streaming (sd_gemm_rows, tcgen05 swap-AB) for the verification
+    # forward's projections whose consumers take split-K slices (RoPE staging,
+    # residual add + RMSNorm); rows_hint: the tree record's live row count (device
+    # int), set by the engine around the verify forward (padded graph rows are
+    # skipped). Off by default: faster than cuBLAS per projection when timed alone
+    # (qkv 10.5 vs 12.1 us, wo 8.5 vs 9.3 us), but the cfg3 step is 0.16-0.3 ms
+    # slower with it (the consumers re-read 6-9 fp32 slices per row; per-launch
+    # ramp), profiles/r02_gemm_rows_experiment.txt. SD_ROWS_KEYS=wqkv,wo turns it on.
+    rows_keys = tuple(k for k in os.environ.get("SD_ROWS_KEYS", "").split(",") if k)
+    rows_hint: torch.Tensor | None = None
+
+    def _rows_ok(self, x: torch.Tensor, w: torch.Tensor, key: str) -> bool:
+        K, N = w.shape
+        return (key in self.rows_keys and self.dtype == torch.bfloat16 and x.dtype == torch.bfloat16
+                and x.is_contiguous() and 1 < x.shape[0] <= 112 and K % 32 == 0 and N % 256 == 0)
+
+    def gemm_rows(self, x: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+        """x [T, K] bf16 @ w [K, N] -> [S, T, N] fp32 split-K slices (sd_gemm_rows)."""
+        if L.DEBUG_SKIP and f"mm:{w.shape[1]}" in L.DEBUG_SKIP:  # profiling only
+            return torch.empty((1, x.shape[0], w.shape[1]), dtype=torch.float32, device=x.device)
+        K, N = w.shape
+        T = x.shape[0]
+        y = torch.empty((L.load().sd_gemm_rows_splits(K, N), T, N), dtype=torch.float32, device=self.device)
+        L.call("sd_gemm_rows", L.ptr(x), T, K, L.ptr(w), N, L.ptr(self.rows_hint), L.ptr(y), L.stream())
+        return y
+
     def dense(self, x: torch.Tensor, ly: dict, key: str, silu: bool = False) -> torch.Tensor:
         """x @ ly[key] -> fp32 [T, N], or [S, T, N] split-K slices whose in-order
         sum is the product (consumed by norm() / rope_stage()); silu=True gives
         bf16 silu(x @ w) (the MLP up-projection)."""
         if self._gemv_ok(x, ly[key]):
             return self.gemv(x, ly[key], silu)
+        if not silu and self._rows_ok(x, ly[key], key):
+            return self.gemm_rows(x, ly[key])
         tm = ly.get("tm_" + key)
         T = x.shape[0]
         if tm is None or T > 128 or not self.use_gemm or not x.is_contiguous():
