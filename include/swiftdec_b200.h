@@ -70,6 +70,10 @@ int sd_add_rmsnorm(float* h, const float* delta, int T, int d, const float* gain
                    void* x, int x_dtype, int delta_splits, int64_t delta_split_stride, sd_stream_t stream);
 /* out = a / (1 + exp(-a)) */
 int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stream);
+/* sd_silu over a [T][N] projection whose rows past *rows_dev (the tree record's
+ * live row count; NULL: all T) are padding and left untouched. */
+int sd_silu_rows(const float* a, void* out, int out_dtype, int T, int N, const int32_t* rows_dev,
+                 sd_stream_t stream);
 /* out = a + b (f32), cast_out = (cast_dtype) out (nullable) */
 int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int cast_dtype, size_t n,
                 sd_stream_t stream);

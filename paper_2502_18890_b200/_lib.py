@@ -56,6 +56,7 @@ _SIGS = {
     "sd_embed": (INT, [P, INT, P, INT, INT, P, P]),
     "sd_add_rmsnorm": (INT, [P, P, INT, INT, P, F32, P, INT, INT, I64, P]),
     "sd_silu": (INT, [P, P, INT, SZ, P]),
+    "sd_silu_rows": (INT, [P, P, INT, INT, INT, P, P]),
     "sd_add_cast": (INT, [P, P, P, P, INT, SZ, P]),
     "sd_rope_stage": (INT, [P, INT, INT, INT, INT, P, P, P, F32, P, INT, P, P, P, P, INT, I64, I64, P, INT, I64, P]),
     "sd_attention_workspace_bytes": (SZ, [INT, INT, INT, INT]),

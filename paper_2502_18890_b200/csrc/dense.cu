@@ -155,9 +155,12 @@ __global__ void add_rmsnorm_scalar_kernel(float* __restrict__ h, const float* __
 
 // 4 elements per thread: one 16-byte load, one 8-byte (bf16) / 16-byte (fp32) store
 template <typename OT>
-__global__ void silu4_kernel(const float4* __restrict__ a, OT* __restrict__ out, size_t n4) {
+__global__ void silu4_kernel(const float4* __restrict__ a, OT* __restrict__ out, size_t n4,
+                             const int32_t* __restrict__ rows_dev, int64_t row_quads) {
   pdl_trigger();
   pdl_wait();  // a is the projection before (PDL launch: may start under its tail)
+  // rows_dev (the tree record's live row count): padded rows past it are skipped
+  if (rows_dev) n4 = min(n4, (size_t)(*rows_dev) * (size_t)row_quads);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     const float4 v = __ldcs(a + i);
     const float r0 = v.x / (1.f + __expf(-v.x)), r1 = v.y / (1.f + __expf(-v.y));
@@ -352,9 +355,10 @@ int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stre
   const bool vec = n % 4 == 0 && ((uintptr_t)a % 16) == 0 && ((uintptr_t)out % 16) == 0;
   if (vec && out_dtype == SD_BF16)
     launch_pdl(silu4_kernel<__nv_bfloat16>, dim3(grid_for(n / 4)), dim3(256), 0, st, (const float4*)a,
-               (__nv_bfloat16*)out, n / 4);
+               (__nv_bfloat16*)out, n / 4, (const int32_t*)nullptr, (int64_t)0);
   else if (vec && out_dtype == SD_F32)
-    launch_pdl(silu4_kernel<float>, dim3(grid_for(n / 4)), dim3(256), 0, st, (const float4*)a, (float*)out, n / 4);
+    launch_pdl(silu4_kernel<float>, dim3(grid_for(n / 4)), dim3(256), 0, st, (const float4*)a, (float*)out, n / 4,
+               (const int32_t*)nullptr, (int64_t)0);
   else if (out_dtype == SD_BF16)
     silu_kernel<<<grid_for(n), 256, 0, st>>>(a, (__nv_bfloat16*)out, n);
   else if (out_dtype == SD_F32)
@@ -362,6 +366,23 @@ int sd_silu(const float* a, void* out, int out_dtype, size_t n, sd_stream_t stre
   else
     SD_REQUIRE(false, "sd_silu: dtype");
   return check_launch("sd_silu");
+}
+
+int sd_silu_rows(const float* a, void* out, int out_dtype, int T, int N, const int32_t* rows_dev,
+                 sd_stream_t stream) {
+  SD_REQUIRE(T > 0 && N > 0 && N % 4 == 0 && ((uintptr_t)a % 16) == 0 && ((uintptr_t)out % 16) == 0,
+             "sd_silu_rows: N %% 4 and 16-byte alignment");
+  auto st = as_stream(stream);
+  const size_t n4 = (size_t)T * N / 4;
+  if (out_dtype == SD_BF16)
+    launch_pdl(silu4_kernel<__nv_bfloat16>, dim3(grid_for(n4)), dim3(256), 0, st, (const float4*)a,
+               (__nv_bfloat16*)out, n4, rows_dev, (int64_t)(N / 4));
+  else if (out_dtype == SD_F32)
+    launch_pdl(silu4_kernel<float>, dim3(grid_for(n4)), dim3(256), 0, st, (const float4*)a, (float*)out, n4, rows_dev,
+               (int64_t)(N / 4));
+  else
+    SD_REQUIRE(false, "sd_silu_rows: dtype");
+  return check_launch("sd_silu_rows");
 }
 
 int sd_add_cast(const float* a, const float* b, float* out, void* cast_out, int cast_dtype, size_t n,

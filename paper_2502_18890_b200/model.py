@@ -480,8 +480,14 @@ class TinyTransformer:
                L.ptr(h), L.stream())
         return h
 
+    silu_rows = os.environ.get("SD_SILU_ROWS", "1") != "0"  # A/B switch (tools only)
+
     def silu(self, a):
         out = torch.empty(a.shape, dtype=self.dtype, device=self.device)
+        if self.silu_rows and self.rows_hint is not None and a.dim() == 2 and a.shape[1] % 4 == 0:  # skip padding
+            L.call("sd_silu_rows", L.ptr(a), L.ptr(out), L.dcode(self.dtype), a.shape[0], a.shape[1],
+                   L.ptr(self.rows_hint), L.stream())
+            return out
         L.call("sd_silu", L.ptr(a), L.ptr(out), L.dcode(self.dtype), a.numel(), L.stream())
         return out
 

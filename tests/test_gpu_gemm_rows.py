@@ -56,3 +56,18 @@ def test_gemm_rows_rejects_bad_shapes(lib):
     y = torch.zeros((8, 4, 256), dtype=torch.float32, device="cuda")
     with pytest.raises(lib.LibraryError):
         lib.call("sd_gemm_rows", lib.ptr(x), 4, 100, lib.ptr(w), 256, None, lib.ptr(y), lib.stream())
+
+
+@pytest.mark.parametrize("live", [41, 101, 1])
+def test_silu_rows_skips_padding(lib, live):
+    """sd_silu_rows: silu of the live verify rows (engine path: the tree record's
+    row count), padded rows untouched."""
+    T, N = 101, 16384
+    a = torch.randn((T, N), device="cuda")
+    out = torch.full((T, N), 3.0, dtype=torch.bfloat16, device="cuda")
+    rows = torch.tensor([live], dtype=torch.int32, device="cuda")
+    lib.call("sd_silu_rows", lib.ptr(a), lib.ptr(out), lib.SD_BF16, T, N, lib.ptr(rows), lib.stream())
+    torch.cuda.synchronize()
+    want = torch.nn.functional.silu(a[:live]).to(torch.bfloat16).float()
+    torch.testing.assert_close(out[:live].float(), want, rtol=1e-2, atol=1e-2)
+    assert bool((out[live:] == 3.0).all())
