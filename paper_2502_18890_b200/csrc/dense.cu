@@ -403,7 +403,8 @@ int sd_rope_stage(const float* qkv, int T, int H, int Hk, int dh, const int32_t*
   SD_REQUIRE(T > 0 && H > 0 && Hk > 0 && dh > 0 && (dh % 4) == 0, "sd_rope_stage: head_dim must be a multiple of 4");
   auto st = as_stream(stream);
   // split-K input: one CTA per 512 quads of a row, so each row's slice reads spread over several SMs
-  const int rc = qkv_splits > 1 ? ((H + 2 * Hk) * dh / 4 + 511) / 512 : 1;
+  static const bool spread_all = getenv("SD_ROPE_SPREAD") && atoi(getenv("SD_ROPE_SPREAD")) != 0;  // A/B (tools)
+  const int rc = (qkv_splits > 1 || (spread_all && T > 1)) ? ((H + 2 * Hk) * dh / 4 + 511) / 512 : 1;
 #define SD_RS(QT, KT)                                                                                          \
   launch_pdl(rope_stage_kernel<QT, KT>, dim3(T, rc), dim3(512), 0, st, qkv, H, Hk, dh, positions, rope_cos, rope_sin,  \
              q_scale, (QT*)q_rot, q_pre, (KT*)k_raw, (KT*)k_rot, (KT*)v, head_stride, row_offset, rows_dev,       \

@@ -1,7 +1,6 @@
-# draft RoPE folded into the QKV weight stream: tests + same-box A/B
-mkdir -p gpurun_out
-timeout 1500 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/rope_tests.log 2>&1; tail -1 gpurun_out/rope_tests.log
-for f in 0 1 0 1; do
-  SD_FUSE_DRAFT_ROPE=$f timeout 300 python bench.py --no-cpu-baseline --attn-reps 1 2>/dev/null | tail -1 > gpurun_out/rope.json
-  python -c "import json; d=json.load(open('gpurun_out/rope.json')); print('fuse=$f', round(d['ms_per_step'],3), 'ms', d['gpu_launches'], d['clocks']['sm_mhz'])"
+#!/bin/bash
+SD_ROPE_SPREAD=1 timeout 600 python -m pytest tests/test_gpu_production.py -x -q 2>&1 | tail -1
+for v in 0 1 0 1 0 1; do
+  echo "== SD_ROPE_SPREAD=$v"
+  SD_ROPE_SPREAD=$v timeout 300 python bench.py --no-cpu-baseline --steps 20 --warmup 5 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), 'ms', round(d['value'],1), 'tok/s', d['clocks']['sm_mhz'])"
 done
