@@ -14,6 +14,10 @@ current CUDA stream, and makes exactly one C-ABI call. The names follow SURVEY
   reconcile_rows       kvcache.py:116-127, engine.py:278-280
   ngram_update         ngram.py:35-50
   ngram_retrieve       ngram.py:52-66
+  draft_topw           engine.py:207-215 (penalised per-head top-w, ties to the lower id)
+  tree_build           tree.py:87-175
+  verify_sample        engine.py:155-181, 237-245, sampling.py:142-224 (tree-row splice, draw)
+  accept               engine.py:247-290, rng.py:23-38 (paths, uniform pick, commit)
 
 Validation and the typed exceptions stay in the Python mirror (model.py,
 kvcache.py, ngram.py); an operator raises _lib.LibraryError when the library
@@ -54,6 +58,16 @@ _SCHEMAS = {
     "ngram_update": "ngram_update(Tensor(a!) table, Tensor seq, int n_tail, int n_new) -> ()",
     "ngram_retrieve": "ngram_retrieve(Tensor table, Tensor first, int k, Tensor(a!) out_grams, "
                       "Tensor(b!) out_count) -> ()",
+    "draft_topw": "draft_topw(Tensor logits, Tensor? win_count, float temperature, float theta, int ctrl_style, "
+                  "int[] widths, Tensor(a!) out) -> ()",
+    "tree_build": "tree_build(Tensor per_head, int[] widths, int depth, Tensor grams, int n_grams, Tensor? state, "
+                  "int base_pos, Tensor(a!) tree) -> ()",
+    "verify_sample": "verify_sample(Tensor logits, Tensor win_count, Tensor win_ring, Tensor state, int window, "
+                     "Tensor tree, int depth, float temperature, float theta, int trunc_kind, float trunc_value, "
+                     "int seed, int n, Tensor(a!) token_out) -> ()",
+    "accept": "accept(Tensor tree, Tensor y, int select_seed, int n, int depth, bool bonus, Tensor(a!) state, "
+              "Tensor(b!) win_ring, Tensor(c!) win_count, int window, Tensor(d!) history, Tensor(e!) result, "
+              "Tensor(f!)? ngram_table=None) -> ()",
 }
 for _s in _SCHEMAS.values():
     _lib.define(_s)
@@ -176,6 +190,50 @@ def _ngram_update(table, seq, n_tail, n_new):
 @_impl("ngram_retrieve")
 def _ngram_retrieve(table, first, k, out_grams, out_count):
     L.call("sd_ngram_retrieve", L.ptr(table), L.ptr(first), k, L.ptr(out_grams), L.ptr(out_count), L.stream())
+
+
+@_impl("draft_topw")
+def _draft_topw(logits, win_count, temperature, theta, ctrl_style, widths, out):
+    """logits [heads, V] fp32 -> out: concatenated candidates, head k gets widths[k]."""
+    heads, V = logits.shape
+    L.call("sd_draft_topw", L.ptr(logits), heads, V, L.ptr(win_count), temperature, theta, ctrl_style,
+           L.host_i32(widths), L.ptr(out), L.stream())
+
+
+@_impl("tree_build")
+def _tree_build(per_head, widths, depth, grams, n_grams, state, base_pos, tree):
+    """per_head: concatenated candidates; grams [n_grams, depth]; tree: the
+    device tree record (sd_tree_layout)."""
+    L.call("sd_tree_build", L.ptr(per_head), L.host_i32(widths), depth, L.ptr(grams), None, n_grams, L.ptr(state),
+           base_pos, L.ptr(tree), L.stream())
+
+
+@_impl("verify_sample")
+def _verify_sample(logits, win_count, win_ring, state, window, tree, depth, temperature, theta, trunc_kind,
+                   trunc_value, seed, n, token_out):
+    """logits [rows, V] fp32 of the tree rows; each row's window is the committed
+    window spliced with its branch (member kind TREE); one draw per row at the
+    tree-derived position key (row 0 -> n, node -> n + depth + 1)."""
+    rows, V = logits.shape
+    a = L.SampleArgs()
+    a.rows, a.V, a.in_kind = rows, V, L.IN_LOGITS_F32
+    a.temperature, a.theta, a.ctrl_style = temperature, theta, 0
+    a.trunc_kind, a.trunc_value, a.eta_alpha = trunc_kind, trunc_value, -1.0
+    a.seed = seed & ((1 << 64) - 1)
+    a.member_kind = L.MEMBER_TREE
+    a.win_count, a.win_ring, a.state, a.window = L.ptr(win_count), L.ptr(win_ring), L.ptr(state), window
+    a.tree, a.depth = L.ptr(tree), depth
+    a.positions, a.n = None, n
+    a.token_out = L.ptr(token_out)
+    L.call("sd_sample_rows", L.ptr(logits), a, L.stream())
+
+
+@_impl("accept")
+def _accept(tree, y, select_seed, n, depth, bonus, state, win_ring, win_count, window, history, result,
+            ngram_table=None):
+    L.call("sd_accept_commit", L.ptr(tree), L.ptr(y), select_seed & ((1 << 64) - 1), n, depth, int(bonus),
+           L.ptr(state), L.ptr(win_ring), L.ptr(win_count), window, L.ptr(history), L.ptr(ngram_table),
+           L.ptr(result), L.stream())
 
 
 def schemas() -> dict:

@@ -167,3 +167,58 @@ def test_ngram_ops_match_the_table():
     OPS.ngram_retrieve(tabs[1].buf, first, 8, grams, cnt)
     got = [tuple(r) for r in grams[:int(cnt.item())].tolist()]
     assert got == tabs[0].retrieve(5, 8)
+
+
+def test_topw_tree_sample_accept_ops_match_the_call_paths():
+    """One draft -> tree -> verify-sample -> accept chain through the operators and
+    through direct C-ABI calls on cloned state: identical records and results."""
+    V, depth, W = 4096, 4, 64
+    widths = [1, 3, 3, 3]
+    g = torch.Generator(device="cuda")
+    g.manual_seed(9)
+    head_logits = torch.randn((depth, V), device="cuda", generator=g)
+    Tmax = 101
+    lay = L.tree_layout()
+
+    def fresh():
+        st = torch.zeros(16, dtype=torch.int64, device="cuda")
+        st[L.ST_PENDING if hasattr(L, "ST_PENDING") else 3] = 7
+        return dict(state=st, ring=torch.zeros(W, dtype=torch.int32, device="cuda"),
+                    count=torch.zeros(V, dtype=torch.int32, device="cuda"),
+                    hist=torch.zeros(256, dtype=torch.int32, device="cuda"),
+                    result=torch.zeros(32, dtype=torch.int32, device="cuda"),
+                    per_head=torch.zeros(sum(widths), dtype=torch.int32, device="cuda"),
+                    tree=torch.zeros(lay["TOTAL"], dtype=torch.int32, device="cuda"),
+                    y=torch.zeros(Tmax, dtype=torch.int32, device="cuda"))
+    grams = torch.zeros((1, depth), dtype=torch.int32, device="cuda")
+    row_logits = torch.randn((Tmax, V), device="cuda", generator=g)
+    outs = []
+    for use_op in (False, True):
+        s = fresh()
+        if use_op:
+            OPS.draft_topw(head_logits, s["count"], 1.0, 1.2, 0, widths, s["per_head"])
+            OPS.tree_build(s["per_head"], widths, depth, grams, 0, s["state"], 100, s["tree"])
+            OPS.verify_sample(row_logits, s["count"], s["ring"], s["state"], W, s["tree"], depth, 1.0, 1.2,
+                              L.TRUNC_MIN_P, 0.1, 1234, 100, s["y"])
+            OPS.accept(s["tree"], s["y"], 99, 100, depth, True, s["state"], s["ring"], s["count"], W, s["hist"],
+                       s["result"])
+        else:
+            L.call("sd_draft_topw", L.ptr(head_logits), depth, V, L.ptr(s["count"]), 1.0, 1.2, 0,
+                   L.host_i32(widths), L.ptr(s["per_head"]), L.stream())
+            L.call("sd_tree_build", L.ptr(s["per_head"]), L.host_i32(widths), depth, L.ptr(grams), None, 0,
+                   L.ptr(s["state"]), 100, L.ptr(s["tree"]), L.stream())
+            a = L.SampleArgs()
+            a.rows, a.V, a.in_kind = Tmax, V, L.IN_LOGITS_F32
+            a.temperature, a.theta, a.ctrl_style = 1.0, 1.2, 0
+            a.trunc_kind, a.trunc_value, a.eta_alpha, a.seed = L.TRUNC_MIN_P, 0.1, -1.0, 1234
+            a.member_kind = L.MEMBER_TREE
+            a.win_count, a.win_ring, a.state, a.window = L.ptr(s["count"]), L.ptr(s["ring"]), L.ptr(s["state"]), W
+            a.tree, a.depth, a.positions, a.n, a.token_out = L.ptr(s["tree"]), depth, None, 100, L.ptr(s["y"])
+            L.call("sd_sample_rows", L.ptr(row_logits), a, L.stream())
+            L.call("sd_accept_commit", L.ptr(s["tree"]), L.ptr(s["y"]), 99, 100, depth, 1, L.ptr(s["state"]),
+                   L.ptr(s["ring"]), L.ptr(s["count"]), W, L.ptr(s["hist"]), None, L.ptr(s["result"]), L.stream())
+        torch.cuda.synchronize()
+        outs.append(s)
+    for k in outs[0]:
+        assert torch.equal(outs[0][k], outs[1][k]), k
+    assert int(outs[1]["result"][L.RES_ACCEPTED]) >= 1

@@ -10,7 +10,7 @@ import paper_2502_18890_b200  # noqa: F401  (registers the operators)
 from paper_2502_18890_b200 import ops
 
 NAMES = ["verify_attention", "draft_attention", "stage_kv_rope", "score_select_gather", "partial_admit_evict",
-         "reconcile_rows", "ngram_update", "ngram_retrieve"]
+         "reconcile_rows", "ngram_update", "ngram_retrieve", "draft_topw", "tree_build", "verify_sample", "accept"]
 
 
 def test_every_boundary_operator_is_registered():
