@@ -448,11 +448,14 @@ __device__ __forceinline__ float4 load4(const __half* p) {
 template <typename OT, typename PT = float, int MK = 3>
 __global__ void __launch_bounds__(256) merge128_kernel(const PT* __restrict__ ws_o, const float* __restrict__ ws_lse,
                                                        int nsplit, int TH, int H, const int32_t* __restrict__ rows_dev,
-                                                       OT* __restrict__ out) {
+                                                       OT* __restrict__ out, int fused_max_rows = 0) {
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);  // t * H + head
   pdl_trigger();
   pdl_wait();  // the split partials are the predecessor's output
+  // fused_max_rows > 0: the tcgen05 kernel merged in place because the live rows
+  // fit one row group (live rows <= fused_max_rows); nothing left to do here
+  if (fused_max_rows > 0 && rows_dev && *rows_dev <= fused_max_rows) return;
   if (row >= TH) return;
   OT* dst = out + (int64_t)row * 128 + 4 * lane;
   if (rows_dev && row / H >= *rows_dev) {  // padded row: defined zeros
@@ -521,7 +524,7 @@ template <typename OT>
 static void launch_merge(const float* ws_o, const float* ws_lse, int nsplit, int TH, int H, const int32_t* rows_dev,
                          OT* out, int dh, cudaStream_t st) {
   if (dh == 128 && nsplit <= 96)
-    launch_pdl(merge128_kernel<OT>, dim3((TH + 7) / 8), dim3(256), 0, st, ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
+    launch_pdl(merge128_kernel<OT>, dim3((TH + 7) / 8), dim3(256), 0, st, ws_o, ws_lse, nsplit, TH, H, rows_dev, out, 0);
   else
     attn_merge_kernel<128, OT><<<TH, 128, 0, st>>>(ws_o, ws_lse, nsplit, TH, H, rows_dev, out);
 }
@@ -1044,7 +1047,8 @@ int tc_split_target(int kv_heads_total);
 int tc_grid_chunks(int ctx_bound, int n_target);
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st);
+                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, void* merge_out, int* merge_counters,
+                     cudaStream_t st);
 template <int DH, typename OT>
 __global__ void attn_merge_kernel(const float* __restrict__ ws_o, const float* __restrict__ ws_lse, int nsplit,
                                   int TH, int H, const int32_t* __restrict__ rows_dev, OT* __restrict__ out);
@@ -1137,15 +1141,30 @@ int sd_attention(const void* q, int q_dtype, int T, int H, int Hk, int dh, int s
     // relative, below the bf16 output's own rounding), lse in fp32
     __half* ws_oh = reinterpret_cast<__half*>(p.ws_o);
     float* ws_lse = reinterpret_cast<float*>(ws_oh + (size_t)nc * T * H * dh);
+    // the split merge fused into the kernel when the whole grid is co-resident
+    // (one row group, one CTA per SM): CTAs of a kv head wait for each other
+    static int n_sm = 0;
+    if (!n_sm) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+    // (the kernel checks the live rows on device: a padded launch whose live rows
+    // need two row groups merges in merge128_kernel below instead)
+    // off by default: measured no faster alone (52.8 vs 52.2 us at ctx 54K: the CTAs of a head wait for
+    // its slowest chunk either way) and 0.19 ms slower per cfg3 step; SD_TC_FUSED_MERGE=1 turns it on
+    static const bool fuse_env = getenv("SD_TC_FUSED_MERGE") && atoi(getenv("SD_TC_FUSED_MERGE")) != 0;
+    const int max_rows_fused = 256 / (H / Hk);  // live rows whose G * rows fit one row group (tc ROWS)
+    const bool fused = fuse_env && nc * Hk <= n_sm && 2 * Hk * (int)sizeof(int) <= 2048 && max_rows_fused > 0;
     int rc = launch_verify_tc(tmap_k_host, tmap_v_host, q, T, H, Hk, layer, ctx, rows_dev, ctx_dev, mask_bits,
-                              mask_words, ws_oh, ws_lse, nc, n_target, st);
+                              mask_words, ws_oh, ws_lse, nc, n_target, fused ? out : nullptr,
+                              fused ? counters + 512 : nullptr, st);
     if (rc) return rc;
+    if (fused && T <= max_rows_fused) return SD_OK;  // every launch merges in the kernel
     if (nc > 160) {
       set_error("sd_attention(tc): %d splits > 160", nc);
       return SD_EINVAL;
     }
+#ifndef SD_TC_NO_MERGE  // debug-only timing builds (tools/gpu_nomerge.sh): the split merge left out
     launch_pdl(nc <= 96 ? merge128_kernel<__nv_bfloat16, __half, 3> : merge128_kernel<__nv_bfloat16, __half, 5>, dim3((T * H + 7) / 8), dim3(256), 0, st, (const __half*)ws_oh,
-               (const float*)ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out);
+               (const float*)ws_lse, nc, T * H, H, rows_dev, (__nv_bfloat16*)out, fused ? max_rows_fused : 0);
+#endif
     return check_launch("sd_attention(tc merge)");
   }
   if (T == 1 && src_kind == 1 && dh == 128 && p.G <= 16 && !rows_dev && !ctx_dev && tmap_k_host && tmap_v_host &&

@@ -98,6 +98,8 @@ struct Params {
   int mask_words;
   __half* ws_o;  // [split][T][H][128] fp16 partial o / l
   float* ws_lse;
+  __nv_bfloat16* merge_out;  // non-null: the split merge runs in this kernel (fused_merge) into out [T][H][128]
+  int* merge_counters;       // [Hk][2] arrival / departure counters, zero between launches
 };
 
 
@@ -237,6 +239,115 @@ __device__ __forceinline__ void issue_loop(uint8_t* smem, int n_tiles, uint32_t 
     if (j + 2 < n_tiles) {
       wait_k(j + 2);
       issue_qk(j + 2);
+    }
+  }
+}
+
+// The split merge inside the kernel (replaces merge128_kernel when the whole
+// grid is co-resident: one row group, <= one CTA per SM). Every live chunk CTA
+// of a kv head publishes its fp16 partials, arrives on the head's counter and
+// waits until all n_live have arrived; then CTA x merges rows [x R / n_live,
+// (x+1) R / n_live) of the head's R = T*G output rows — the same arithmetic,
+// in the same order, as merge128_kernel (bitwise equal output). The last CTA
+// to leave resets the counters for the next launch (a graph replay, or the
+// next layer: every launch passes griddepcontrol.wait first, i.e. after the
+// previous launch's reset). Spinning cannot deadlock: the host fuses only when
+// the grid fits on the SMs at one CTA each, and nothing the CTAs wait for
+// depends on this kernel.
+__device__ __noinline__ void fused_merge(const Params& p, int kvh, int n_live, int T_live) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  int* arrive = p.merge_counters + 2 * kvh;
+  int* depart = arrive + 1;
+  __threadfence();  // this CTA's partials visible at gpu scope before it arrives
+  __syncthreads();
+  if (tid == 0) {
+    atomicAdd(arrive, 1);
+    int seen;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+      if (seen >= n_live) break;
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  const int G = p.G, R = p.T * G;
+  const int r0 = (int)((int64_t)blockIdx.x * R / n_live), r1 = (int)((int64_t)(blockIdx.x + 1) * R / n_live);
+  constexpr int MK = 5, MU = 8;  // <= 160 splits (lane c % 32, register c / 32); MU partials in flight
+  for (int rho = r0 + warp; rho < r1; rho += THREADS / 32) {
+    const int t = rho / G, h = kvh * G + (rho - t * G);
+    __nv_bfloat16* dst = p.merge_out + ((int64_t)t * p.H + h) * DH + 4 * lane;
+    if (t >= T_live) {  // padded row: defined zeros
+      *reinterpret_cast<uint2*>(dst) = make_uint2(0u, 0u);
+      continue;
+    }
+    float lv[MK], wv[MK];
+#pragma unroll
+    for (int k = 0; k < MK; ++k) {
+      const int c = lane + 32 * k;
+      lv[k] = c < n_live ? __ldcg(p.ws_lse + ((int64_t)c * p.T + t) * p.H + h) : -INFINITY;
+    }
+    float m = lv[0];
+#pragma unroll
+    for (int k = 1; k < MK; ++k) m = fmaxf(m, lv[k]);
+    m = warp_max(m);
+    float lsum = 0.f;
+#pragma unroll
+    for (int k = 0; k < MK; ++k) {
+      wv[k] = lv[k] == -INFINITY ? 0.f : __expf(lv[k] - m);
+      lsum += wv[k];
+    }
+    lsum = warp_sum(lsum);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const __half* base = p.ws_o + ((int64_t)t * p.H + h) * DH + 4 * lane;
+    const int64_t cstride = (int64_t)p.T * p.H * DH;
+#pragma unroll
+    for (int k = 0; k < MK; ++k) {
+      unsigned live = __ballot_sync(0xffffffffu, lv[k] != -INFINITY);
+      while (live) {
+        int cs[MU];
+        float ws4[MU];
+        int n = 0;
+#pragma unroll
+        for (int u = 0; u < MU; ++u) {
+          cs[u] = live ? __ffs(live) - 1 : 0;
+          ws4[u] = __shfl_sync(0xffffffffu, wv[k], cs[u]);
+          if (live) {
+            live &= live - 1;
+            ++n;
+          } else {
+            ws4[u] = 0.f;
+          }
+        }
+        float4 o[MU];
+#pragma unroll
+        for (int u = 0; u < MU; ++u) {
+          const uint2 raw = __ldcg(reinterpret_cast<const uint2*>(base + (int64_t)(32 * k + cs[u]) * cstride));
+          const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&raw.x));
+          const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&raw.y));
+          o[u] = make_float4(a.x, a.y, b.x, b.y);
+        }
+#pragma unroll
+        for (int u = 0; u < MU; ++u) {
+          if (u < n) {
+            acc.x = fmaf(ws4[u], o[u].x, acc.x);
+            acc.y = fmaf(ws4[u], o[u].y, acc.y);
+            acc.z = fmaf(ws4[u], o[u].z, acc.z);
+            acc.w = fmaf(ws4[u], o[u].w, acc.w);
+          }
+        }
+      }
+    }
+    const float inv = lsum > 0.f ? 1.f / lsum : 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x * inv, acc.y * inv), hi = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+    *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(depart, 1) == n_live - 1) {  // everyone has passed the wait: reset for the next launch
+      *arrive = 0;
+      *depart = 0;
+      __threadfence();
     }
   }
 }
@@ -781,6 +892,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
+  if (p.merge_out && GT <= ROWS) fused_merge(p, kvh, n_live, T);  // live rows in one row group: merge here
 }
 
 }  // namespace tc
@@ -849,7 +961,8 @@ int tc_grid_chunks(int ctx_bound, int n_target) {
 
 int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int T, int H, int Hk, int layer, int ctx,
                      const int32_t* rows_dev, const int32_t* ctx_dev, const uint32_t* mask, int mask_words,
-                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, cudaStream_t st) {
+                     __half* ws_o, float* ws_lse, int n_chunks, int n_target, void* merge_out, int* merge_counters,
+                     cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
@@ -869,6 +982,8 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   p.mask_words = mask_words;
   p.ws_o = ws_o;
   p.ws_lse = ws_lse;
+  p.merge_out = (__nv_bfloat16*)merge_out;
+  p.merge_counters = merge_counters;
   const int groups = (p.G * T + tc::ROWS - 1) / tc::ROWS;
   dim3 grid(n_chunks, Hk, groups);
   CUtensorMap mk, mv;

@@ -1,0 +1,11 @@
+#!/bin/bash
+# verify attention with the split merge fused into the tcgen05 kernel: parity, timing, step A/B
+mkdir -p gpurun_out
+timeout 300 python -m pytest tests/test_gpu_kernels.py -x -q -k "tcgen05 or verify_attention or ctx_dev or rows_dev" > gpurun_out/fm_kernels.log 2>&1; echo "kernel tests rc=$?"; tail -2 gpurun_out/fm_kernels.log
+timeout 600 python -m pytest tests/test_gpu_production.py tests/test_gpu_ops.py -x -q > gpurun_out/fm_prod.log 2>&1; echo "prod tests rc=$?"; tail -2 gpurun_out/fm_prod.log
+export TC_SHAPES="54096,41,32,8;12048,41,32,8;4096,41,32,8;54096,101,32,8"
+for v in 0 1 0 1; do echo "== SD_TC_FUSED_MERGE=$v"; SD_TC_FUSED_MERGE=$v timeout 120 python tools/time_tc_cfg.py 2>&1 | tail -4; done
+for v in 0 1 0 1; do
+  echo "== bench SD_TC_FUSED_MERGE=$v"
+  SD_TC_FUSED_MERGE=$v timeout 300 python bench.py --no-cpu-baseline --steps 20 --warmup 5 2>&1 | grep '^{' | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), 'ms', round(d['value'],1), 'tok/s', 'attn', round(d['roofline']['avg_launch_us'],2), round(d['roofline']['frac'],3), d['clocks']['sm_mhz'])"
+done
