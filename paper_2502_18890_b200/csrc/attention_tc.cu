@@ -352,6 +352,9 @@ __device__ __noinline__ void fused_merge(const Params& p, int kvh, int n_live, i
   }
 }
 
+// FUSED: the fused_merge tail (SD_TC_FUSED_MERGE=1) is a separate instantiation so
+// the production kernel's code is unchanged by it
+template <bool FUSED>
 __global__ void __launch_bounds__(THREADS, 1)
     verify_attn_tc_kernel(const __grid_constant__ CUtensorMap tmap_k, const __grid_constant__ CUtensorMap tmap_v,
                           Params p) {
@@ -892,7 +895,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
   }
-  if (p.merge_out && GT <= ROWS) fused_merge(p, kvh, n_live, T);  // live rows in one row group: merge here
+  if constexpr (FUSED) {
+    if (p.merge_out && GT <= ROWS) fused_merge(p, kvh, n_live, T);  // live rows in one row group: merge here
+  }
 }
 
 }  // namespace tc
@@ -965,7 +970,8 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
                      cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc::verify_attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
+    cudaFuncSetAttribute(tc::verify_attn_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
+    cudaFuncSetAttribute(tc::verify_attn_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_ALLOC);
     attr_set = true;
   }
   tc::Params p;
@@ -989,7 +995,10 @@ int launch_verify_tc(const void* tmap_k, const void* tmap_v, const void* q, int 
   CUtensorMap mk, mv;
   memcpy(&mk, tmap_k, sizeof(CUtensorMap));
   memcpy(&mv, tmap_v, sizeof(CUtensorMap));
-  launch_pdl(tc::verify_attn_tc_kernel, grid, dim3(tc::THREADS), tc::SMEM_ALLOC, st, mk, mv, p);
+  if (merge_out)
+    launch_pdl(tc::verify_attn_tc_kernel<true>, grid, dim3(tc::THREADS), tc::SMEM_ALLOC, st, mk, mv, p);
+  else
+    launch_pdl(tc::verify_attn_tc_kernel<false>, grid, dim3(tc::THREADS), tc::SMEM_ALLOC, st, mk, mv, p);
   return check_launch("sd_attention(tcgen05)");
 }
 
